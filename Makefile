@@ -1,0 +1,30 @@
+# Native build: input generator (gen/), CPU oracle (oracle/, test infrastructure), and the
+# B200 library libchfsi.so (paper_1404_4161_b200/). `python -c "import __graft_entry__ as g; g.build()"`
+# runs this.
+NVCC ?= /usr/local/cuda/bin/nvcc
+HOSTCC := $(shell test -x /usr/bin/gcc && echo /usr/bin/gcc || echo gcc)
+CUDA_HOME ?= /usr/local/cuda
+CFLAGS_HOST = -O2 -fno-fast-math -ffp-contract=off -fPIC -fopenmp -std=c11 -Wall -Wno-unknown-pragmas
+NVCCFLAGS = -ccbin $(shell test -x /usr/bin/g++ && echo /usr/bin/g++ || echo g++) -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
+            -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+PKG = paper_1404_4161_b200
+CSRC = $(PKG)/csrc
+LIBCHFSI = $(PKG)/libchfsi.so
+CU_SRCS = $(wildcard $(CSRC)/*.cu)
+CU_HDRS = $(wildcard $(CSRC)/*.cuh) include/chfsi.h
+
+all: gen/libgen.so oracle/liboracle.so $(LIBCHFSI)
+
+gen/libgen.so: gen/gen.c gen/gen.h
+	$(HOSTCC) $(CFLAGS_HOST) -shared -o $@ gen/gen.c -lm
+
+oracle/liboracle.so: oracle/oracle.c oracle/oracle.h
+	$(HOSTCC) $(CFLAGS_HOST) -shared -o $@ oracle/oracle.c -lm
+
+$(LIBCHFSI): $(CU_SRCS) $(CU_HDRS)
+	$(NVCC) $(NVCCFLAGS) -Iinclude -shared -o $@ $(CU_SRCS) -lcublas -lcusolver -ldl
+
+clean:
+	rm -f gen/libgen.so oracle/liboracle.so $(LIBCHFSI)
+
+.PHONY: all clean

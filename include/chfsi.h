@@ -1,0 +1,151 @@
+/* chfsi.h -- C-ABI of the B200-native Chebyshev Filtered Subspace Iteration library (libchfsi.so).
+ *
+ * Paper: Berljafa, Wortmann, Di Napoli, "An Optimized and Scalable Eigensolver for Sequences of
+ * Eigenvalue Problems" (arXiv:1404.4161). Citations: P:n = /root/reference/PAPER.md line n (with
+ * the section / algorithm / equation it falls in); R<k> = the reading of the paper listed in
+ * DESIGN.md section 3.
+ *
+ * Conventions (all entry points)
+ *  - Complex data: interleaved complex128 (double re, double im), column-major, explicit leading
+ *    dimension (ld >= rows). Device pointers unless stated "host".
+ *  - Distribution (nranks = p >= 1): the rank owns global rows [row0, row0 + nloc) of every n-row
+ *    matrix (Y, Q, X). H is passed as its column slab Hp = H[:, row0:row0+nloc] (n x nloc, ldh >= n);
+ *    for Hermitian H this is the conjugate of the rank's row panel, and the library applies
+ *    (H y)[r] = sum_q conj(Hp[q, r - row0]) y[q] (R13). p == 1: row0 = 0, nloc = n.
+ *  - Streams: all device work is enqueued on the context's CUDA stream. A call returns once its
+ *    host-visible outputs are valid; device outputs are stream-ordered.
+ *  - Ownership: the caller allocates and frees H, Y, Q, X and all host arrays; the library never
+ *    frees caller memory. It owns only its workspace (allocated by chfsi_ctx_reserve or on first
+ *    use, freed by chfsi_ctx_destroy).
+ *  - Errors: every entry point returns a chfsi_status; no exception or abort crosses the ABI. On an
+ *    error other than CHFSI_ERR_NOCONV the outputs are unspecified; chfsi_last_error() describes it.
+ *  - SPMD (p > 1): every rank calls with identical n, k, degrees, scalars and options.
+ *  - There is no CPU fallback: without a usable CUDA device every call returns CHFSI_ERR_CUDA.
+ */
+#ifndef CHFSI_H
+#define CHFSI_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct chfsi_ctx_s* chfsi_ctx;
+
+typedef enum {
+  CHFSI_OK = 0,
+  CHFSI_ERR_ARG = 1,       /* bad dimension / ld / degree / interval / option */
+  CHFSI_ERR_NONFINITE = 2, /* NaN or Inf in a filter output */
+  CHFSI_ERR_NOCONV = 3,    /* max_loops reached; outputs hold partial results */
+  CHFSI_ERR_QR = 4,        /* CholeskyQR2 and its Householder fallback both failed */
+  CHFSI_ERR_CUDA = 5,      /* CUDA / cuBLAS / cuSOLVER failure, or no device */
+  CHFSI_ERR_NCCL = 6,      /* NCCL failure or unavailable when nranks > 1 */
+  CHFSI_ERR_NOMEM = 7      /* workspace allocation failed */
+} chfsi_status;
+
+#define CHFSI_MAX_DEGREE 64
+
+/* Create a context on `device` using `cuda_stream` (a cudaStream_t, or NULL for a library-owned
+ * stream). nccl_comm: an ncclComm_t spanning the `nranks` ranks (NULL when nranks == 1). */
+chfsi_status chfsi_ctx_create(chfsi_ctx* out, int32_t device, void* cuda_stream, void* nccl_comm,
+                              int32_t rank, int32_t nranks);
+/* Optional: preallocate workspace for problems up to n rows globally, nloc rows per rank and kmax
+ * block columns, so no allocation happens inside a timed loop. */
+chfsi_status chfsi_ctx_reserve(chfsi_ctx ctx, int64_t n, int64_t nloc, int64_t kmax);
+void chfsi_ctx_destroy(chfsi_ctx ctx);
+const char* chfsi_last_error(chfsi_ctx ctx);
+/* Number of kernels of this library launched on the context since creation (instrumentation). */
+int64_t chfsi_kernel_launches(chfsi_ctx ctx);
+
+/* Chebyshev filter -- Algorithm 2 with the three-term recurrence of eq:3term
+ * (P:764-768), reading R1 (line 8's trailing term is Y_{i-1}), R2 (columns run to k), R3 (active
+ * start s = #{j : deg[j] <= i} before step i).
+ *   Y_1     = (sigma_1/e) (H - cI) Y_0,                            sigma_1 = e/(lambda1 - c)  (l2-3)
+ *   Y_{i+1} = (2 sigma_{i+1}/e)(H - cI) Y_i - sigma_{i+1} sigma_i Y_{i-1},
+ *             sigma_{i+1} = 1/(2/sigma_1 - sigma_i)                                     (l6, l8)
+ * on the active columns only; column j leaves the recurrence after deg[j] steps (l7, l9), so it
+ * equals p_{deg[j]}(H) y_j with p_m(t) = C_m((t-c)/e)/C_m((lambda1-c)/e) (App. A of
+ * SURVEY.md).
+ *   Hp     device, n x nloc column slab of H (see Conventions), ldh >= n. Read only.
+ *   Y      device, nloc x k, ldy >= nloc. In: Y_0 (this rank's rows). Out: the filtered block.
+ *   deg    host int32[k], ascending, 1 <= deg[j] <= CHFSI_MAX_DEGREE.
+ *   lambda1, c, e: the interval [c-e, c+e] = [alpha, beta] to damp and the scaling point lambda1
+ *          (gamma); requires e > 0 and lambda1 < c - e.
+ *   matvecs host, nullable: receives sum(deg), the number of column mat-vecs with H (global).
+ * Errors: CHFSI_ERR_ARG (dims, ld, unsorted / out-of-range degree, e <= 0, lambda1 >= c - e),
+ *         CHFSI_ERR_NONFINITE (non-finite output), CHFSI_ERR_CUDA, CHFSI_ERR_NCCL. */
+chfsi_status chfsi_filter(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp,
+                          int64_t ldh, void* Y, int64_t ldy, int64_t k, const int32_t* deg,
+                          double lambda1, double c, double e, int64_t* matvecs);
+
+/* Lanczos spectral bounds -- Alg 1 line 3, reading R17: `steps` iterations
+ * with full reorthogonalisation from the normalised counter-based start vector of DESIGN.md R22
+ * (seed, stream (4 << 16) | restart); a breakdown restarts with the next stream, at most 3 times.
+ *   theta_min, theta_max (host): extreme eigenvalues of the Lanczos tridiagonal T;
+ *   upper_bound (host): theta_max + ||f_steps||, the filter's upper interval end beta.
+ * Errors: CHFSI_ERR_ARG (steps < 1), CHFSI_ERR_NOCONV (breakdown after 3 restarts), CUDA/NCCL. */
+chfsi_status chfsi_lanczos_bounds(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc,
+                                  const void* Hp, int64_t ldh, int32_t steps, uint64_t seed,
+                                  double* theta_min, double* theta_max, double* upper_bound);
+
+/* QR -- Alg 1 line 6, reading R14/R15: Y[:, nlocked:k] is orthonormalised
+ * against Y[:, 0:nlocked] (left bit-identical) by CGS2, then by CholeskyQR2 (S = Y^H Y = R^H R,
+ * Y <- Y R^{-1}, twice). If a Cholesky pivot fails or ||Q^H Q - I||_max > 1e-12 the block is
+ * re-orthonormalised by Householder QR instead (*used_fallback = 1). Q has R with real positive
+ * diagonal (Y_in = Q R).
+ *   Y  device, nloc x k, ldy >= nloc, in/out.  used_fallback host, nullable.
+ * Errors: CHFSI_ERR_ARG, CHFSI_ERR_QR (fallback failed), CUDA/NCCL. */
+chfsi_status chfsi_qr(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, void* Y, int64_t ldy,
+                      int64_t k, int64_t nlocked, int32_t* used_fallback);
+
+/* Rayleigh-Ritz -- Alg 1 lines 7-9: G = Q^H H Q (hermitised), G W = W M,
+ * Q <- Q W. Q must have orthonormal columns.
+ *   Q     device, nloc x k, ldq >= nloc, in/out (Ritz vectors, ascending Ritz values).
+ *   ritz  host double[k], ascending.
+ *   resid host double[k], nullable: ||H q_j - mu_j q_j||_2 / normH (R8), computed from (HQ)W
+ *         without a second n^2 k product.
+ * Errors: CHFSI_ERR_ARG (normH <= 0 with resid != NULL), CUDA/NCCL. */
+chfsi_status chfsi_rayleigh_ritz(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc,
+                                 const void* Hp, int64_t ldh, void* Q, int64_t ldq, int64_t k,
+                                 double normH, double* ritz, double* resid);
+
+typedef struct {
+  int32_t nev, nex;      /* wanted eigenpairs and extra buffer columns, k = nev + nex <= n */
+  int32_t deg0;          /* starting degree of each problem's first loop (R12; default 8) */
+  int32_t deg_cap;       /* degree cap (default 40), <= CHFSI_MAX_DEGREE */
+  int32_t max_loops;     /* default 50 */
+  int32_t lanczos_steps; /* default 25 (R17) */
+  double tol;            /* residual tolerance, relative to ||H||_est (R8), e.g. 1e-10 */
+  uint64_t seed;         /* Lanczos start-vector seed; problem ell uses seed + ell */
+  int32_t random_start;  /* 1: ignore X on input and draw a counter-based start block (R22) */
+} chfsi_opts;
+
+typedef struct {
+  int32_t loops, qr_fallbacks, capped, converged;
+  int64_t matvecs_filter, matvecs_total;
+  double filter_flops; /* algorithmic: 8 n^2 sum(deg) over all filter calls */
+  double t_lanczos, t_filter, t_qr, t_rr, t_resid, t_opt, t_total; /* seconds, CUDA events */
+  double theta_min, theta_max, beta_up, normH;
+} chfsi_report;
+
+/* Callback giving problem ell's column slab (device pointer and its leading dimension). */
+typedef chfsi_status (*chfsi_get_h)(void* user, int32_t ell, const void** Hp, int64_t* ldh);
+
+/* ChFSI on a sequence -- Algorithm 1 for ell = 0..nprob-1, the eigenvectors and
+ * (lambda_1, lambda_k) of problem ell seeding problem ell+1 (Def 1).
+ *   X       device, nloc x (nev+nex), ldx >= nloc. In: the start basis of problem 0 (unless
+ *           opts.random_start). Out: the final block of the last problem; its first nev columns are
+ *           the eigenvectors, ascending.
+ *   lambda  host double[nprob * nev]: eigenvalues of problem ell at lambda[ell*nev + i], ascending.
+ *   resid   host double[nprob * nev], nullable: their residuals (R8).
+ *   reports host chfsi_report[nprob], nullable.
+ * Errors: CHFSI_ERR_ARG, CHFSI_ERR_NOCONV (a problem hit max_loops; the sequence continues and the
+ *         partial results are returned), CHFSI_ERR_QR, CUDA/NCCL. */
+chfsi_status chfsi_solve_sequence(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc,
+                                  int32_t nprob, chfsi_get_h get_h, void* user,
+                                  const chfsi_opts* opts, void* X, int64_t ldx, double* lambda,
+                                  double* resid, chfsi_report* reports);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
