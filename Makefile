@@ -12,6 +12,7 @@ CSRC = $(PKG)/csrc
 LIBCHFSI = $(PKG)/libchfsi.so
 CU_SRCS = $(wildcard $(CSRC)/*.cu)
 CU_HDRS = $(wildcard $(CSRC)/*.cuh) include/chfsi.h
+NCCL_INC := $(shell python -c 'import os,nvidia;print(os.path.join(list(nvidia.__path__)[0],"nccl","include"))' 2>/dev/null)
 
 all: gen/libgen.so oracle/liboracle.so $(LIBCHFSI)
 
@@ -22,7 +23,7 @@ oracle/liboracle.so: oracle/oracle.c oracle/oracle.h
 	$(HOSTCC) $(CFLAGS_HOST) -shared -o $@ oracle/oracle.c -lm
 
 $(LIBCHFSI): $(CU_SRCS) $(CU_HDRS)
-	$(NVCC) $(NVCCFLAGS) -Iinclude -shared -o $@ $(CU_SRCS) -lcublas -lcusolver -ldl
+	$(NVCC) $(NVCCFLAGS) -Iinclude -I$(NCCL_INC) -shared -o $@ $(CU_SRCS) -lcublas -lcusolver -ldl
 
 clean:
 	rm -f gen/libgen.so oracle/liboracle.so $(LIBCHFSI)

@@ -1,0 +1,251 @@
+"""Python binding of libchfsi.so -- the B200-native ChFSI library (arXiv:1404.4161).
+
+Argument marshalling only: every step runs in the library's CUDA kernels (or cuBLAS / cuSOLVER /
+NCCL calls it makes). PyTorch supplies device memory, streams and the NCCL communicator. There is no
+CPU fallback: importing this module on a machine without the built library raises, and creating a
+context without a B200 raises.
+
+Matrices are column-major complex128: pass (rows x cols) torch tensors with stride (1, ld), e.g. from
+`colmajor(rows, cols)` or `t.t().contiguous().t()` -- the same memory layout as the C-ABI
+(include/chfsi.h).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libchfsi.so")
+MAX_DEGREE = 64
+
+STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_NOCONV", 4: "ERR_QR", 5: "ERR_CUDA", 6: "ERR_NCCL",
+          7: "ERR_NOMEM"}
+
+EXPORTS = ("chfsi_ctx_create", "chfsi_ctx_reserve", "chfsi_ctx_destroy", "chfsi_last_error",
+           "chfsi_kernel_launches", "chfsi_filter", "chfsi_lanczos_bounds", "chfsi_qr", "chfsi_rayleigh_ritz",
+           "chfsi_solve_sequence")
+
+
+class ChfsiError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("nev", ctypes.c_int32), ("nex", ctypes.c_int32), ("deg0", ctypes.c_int32),
+                ("deg_cap", ctypes.c_int32), ("max_loops", ctypes.c_int32), ("lanczos_steps", ctypes.c_int32),
+                ("tol", ctypes.c_double), ("seed", ctypes.c_uint64), ("random_start", ctypes.c_int32)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("loops", ctypes.c_int32), ("qr_fallbacks", ctypes.c_int32), ("capped", ctypes.c_int32),
+                ("converged", ctypes.c_int32), ("matvecs_filter", ctypes.c_int64), ("matvecs_total", ctypes.c_int64),
+                ("filter_flops", ctypes.c_double), ("t_lanczos", ctypes.c_double), ("t_filter", ctypes.c_double),
+                ("t_qr", ctypes.c_double), ("t_rr", ctypes.c_double), ("t_resid", ctypes.c_double),
+                ("t_opt", ctypes.c_double), ("t_total", ctypes.c_double), ("theta_min", ctypes.c_double),
+                ("theta_max", ctypes.c_double), ("beta_up", ctypes.c_double), ("normH", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+GET_H = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p),
+                         ctypes.POINTER(ctypes.c_int64))
+
+_lib = None
+
+
+def lib():
+    """Load libchfsi.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: build it with `make` or __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        i64, u64, i32, dbl, vp = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
+        pd, pi64, pi32 = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)
+        L.chfsi_ctx_create.argtypes = [ctypes.POINTER(vp), i32, vp, vp, i32, i32]
+        L.chfsi_ctx_reserve.argtypes = [vp, i64, i64, i64]
+        L.chfsi_ctx_destroy.argtypes = [vp]
+        L.chfsi_ctx_destroy.restype = None
+        L.chfsi_last_error.argtypes = [vp]
+        L.chfsi_last_error.restype = ctypes.c_char_p
+        L.chfsi_kernel_launches.argtypes = [vp]
+        L.chfsi_kernel_launches.restype = i64
+        L.chfsi_filter.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, i64, pi32, dbl, dbl, dbl, pi64]
+        L.chfsi_lanczos_bounds.argtypes = [vp, i64, i64, i64, vp, i64, i32, u64, pd, pd, pd]
+        L.chfsi_qr.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, pi32]
+        L.chfsi_rayleigh_ritz.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, i64, dbl, pd, pd]
+        L.chfsi_solve_sequence.argtypes = [vp, i64, i64, i64, i32, GET_H, vp, ctypes.POINTER(Opts), vp, i64, pd, pd,
+                                           ctypes.POINTER(Report)]
+        for name in ("chfsi_ctx_create", "chfsi_ctx_reserve", "chfsi_filter", "chfsi_lanczos_bounds", "chfsi_qr",
+                     "chfsi_rayleigh_ritz", "chfsi_solve_sequence"):
+            getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def colmajor(rows: int, cols: int, device="cuda", dtype=None):
+    """An uninitialised (rows x cols) column-major complex128 tensor (stride (1, rows))."""
+    import torch
+
+    dtype = dtype or torch.complex128
+    return torch.empty((cols, rows), dtype=dtype, device=device).t()
+
+
+def to_colmajor(a, device="cuda"):
+    """Copy a numpy / torch (rows x cols) array into a column-major complex128 device tensor."""
+    import torch
+
+    t = torch.as_tensor(np.asarray(a) if not isinstance(a, torch.Tensor) else a)
+    out = colmajor(t.shape[0], t.shape[1], device=device)
+    out.copy_(t.to(torch.complex128))
+    return out
+
+
+def _mat(t, rows=None, cols=None, name="matrix"):
+    """(pointer, ld) of a column-major complex128 CUDA tensor."""
+    import torch
+
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.complex128 or not t.is_cuda or t.dim() != 2:
+        raise TypeError(f"{name}: need a 2-D complex128 CUDA tensor")
+    if rows is not None and t.shape[0] != rows or cols is not None and t.shape[1] != cols:
+        raise ValueError(f"{name}: shape {tuple(t.shape)} != ({rows}, {cols})")
+    if t.shape[1] > 1 and t.stride(0) != 1 or t.shape[1] <= 1 and t.shape[0] > 1 and t.stride(0) != 1:
+        raise ValueError(f"{name}: must be column-major (stride (1, ld))")
+    ld = t.stride(1) if t.shape[1] > 1 else max(t.shape[0], 1)
+    return ctypes.c_void_p(t.data_ptr()), ld
+
+
+class Context:
+    """A library context on one device (one per rank). Work runs on `stream` (default: torch's current
+    stream). For nranks > 1 pass `nccl_comm` (an ncclComm_t as int, e.g. from torch's ProcessGroupNCCL)."""
+
+    def __init__(self, device: int = 0, stream=None, nccl_comm: int | None = None, rank: int = 0, nranks: int = 1):
+        import torch
+
+        L = lib()
+        self.device = device
+        self.rank, self.nranks = rank, nranks
+        torch.cuda.set_device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = ctypes.c_void_p()
+        st = L.chfsi_ctx_create(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream),
+                                ctypes.c_void_p(nccl_comm or 0), rank, nranks)
+        if st != 0:
+            raise ChfsiError(st, "chfsi_ctx_create failed (no B200 / CUDA device?)")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().chfsi_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st != 0 and st != 3:
+            raise ChfsiError(st, lib().chfsi_last_error(self.h).decode())
+        return st
+
+    @property
+    def kernel_launches(self) -> int:
+        return lib().chfsi_kernel_launches(self.h)
+
+    def reserve(self, n, nloc, kmax):
+        self._check(lib().chfsi_ctx_reserve(self.h, n, nloc, kmax))
+
+    # -- Alg 2 -------------------------------------------------------------------------------------
+    def filter(self, Hp, Y, deg, lambda1, c, e, n=None, row0=0):
+        """In place: Y <- filtered block (chfsi_filter). Returns the mat-vec count sum(deg)."""
+        nloc, k = Y.shape
+        n = n or Hp.shape[0]
+        hp, ldh = _mat(Hp, n, nloc, "Hp")
+        yp, ldy = _mat(Y, nloc, k, "Y")
+        d = (ctypes.c_int32 * max(k, 1))(*[int(x) for x in deg])
+        mv = ctypes.c_int64()
+        self._check(lib().chfsi_filter(self.h, n, row0, nloc, hp, ldh, yp, ldy, k, d, lambda1, c, e, ctypes.byref(mv)))
+        return mv.value
+
+    # -- Alg 1 l3 ----------------------------------------------------------------------------------
+    def lanczos_bounds(self, Hp, steps=25, seed=0, n=None, row0=0):
+        n = n or Hp.shape[0]
+        nloc = Hp.shape[1]
+        hp, ldh = _mat(Hp, n, nloc, "Hp")
+        a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        self._check(lib().chfsi_lanczos_bounds(self.h, n, row0, nloc, hp, ldh, steps, seed, ctypes.byref(a),
+                                               ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    # -- Alg 1 l6 ----------------------------------------------------------------------------------
+    def qr(self, Y, nlocked=0, n=None, row0=0):
+        nloc, k = Y.shape
+        n = n or nloc
+        yp, ldy = _mat(Y, nloc, k, "Y")
+        fb = ctypes.c_int32()
+        self._check(lib().chfsi_qr(self.h, n, row0, nloc, yp, ldy, k, nlocked, ctypes.byref(fb)))
+        return fb.value
+
+    # -- Alg 1 l7-9 --------------------------------------------------------------------------------
+    def rayleigh_ritz(self, Hp, Q, normH=None, n=None, row0=0):
+        nloc, k = Q.shape
+        n = n or Hp.shape[0]
+        hp, ldh = _mat(Hp, n, nloc, "Hp")
+        qp, ldq = _mat(Q, nloc, k, "Q")
+        ritz = np.zeros(k)
+        res = np.zeros(k) if normH else None
+        self._check(lib().chfsi_rayleigh_ritz(
+            self.h, n, row0, nloc, hp, ldh, qp, ldq, k, float(normH or 0.0),
+            ritz.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+            res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if res is not None else None))
+        return ritz, res
+
+    # -- Alg 1 over a sequence ----------------------------------------------------------------------
+    def solve_sequence(self, get_h, nprob, X, nev, nex, tol, deg_cap=40, deg0=8, max_loops=50, lanczos_steps=25,
+                       seed=0, random_start=False, n=None, row0=0):
+        """get_h(ell) -> column-major CUDA tensor Hp (n x nloc) of problem ell (kept alive by the caller
+        until the next call). Returns dict(status, lam (nprob x nev), resid, reports)."""
+        nloc, k = X.shape
+        assert k == nev + nex
+        n = n or nloc
+        xp, ldx = _mat(X, nloc, k, "X")
+        keep = {}
+
+        def cb(user, ell, hp_out, ldh_out):
+            try:
+                t = get_h(int(ell))
+                p, ld = _mat(t, n, nloc, "Hp")
+                keep["h"] = t
+                hp_out[0] = p.value
+                ldh_out[0] = ld
+                return 0
+            except Exception as ex:  # surfaced as ERR_ARG through the C-ABI
+                keep["exc"] = ex
+                return 1
+
+        cbf = GET_H(cb)
+        opts = Opts(nev, nex, deg0, deg_cap, max_loops, lanczos_steps, tol, seed, 1 if random_start else 0)
+        lam = np.zeros(nprob * nev)
+        res = np.zeros(nprob * nev)
+        reps = (Report * nprob)()
+        st = lib().chfsi_solve_sequence(self.h, n, row0, nloc, nprob, cbf, None, ctypes.byref(opts), xp, ldx,
+                                        lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                        res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), reps)
+        if "exc" in keep:
+            raise keep["exc"]
+        self._check(st)
+        return dict(status=st, lam=lam.reshape(nprob, nev), resid=res.reshape(nprob, nev),
+                    reports=[r.as_dict() for r in reps])
+
+
+def filter_flops(n: int, deg) -> float:
+    """Algorithmic flops of one filter call: 8 n^2 sum(deg) (complex MAC = 8 real flops)."""
+    return 8.0 * n * n * float(sum(int(d) for d in deg))

@@ -1,0 +1,393 @@
+// chfsi.cu -- context management, TMA descriptor encoding, and the Chebyshev filter driver
+// (chfsi_filter: Alg 2) plus H*Q for Rayleigh-Ritz, both on the K1 kernel.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "ctx.cuh"
+#include "filter_step.cuh"
+
+namespace chfsi {
+
+void set_err(chfsi_ctx ctx, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+}
+
+chfsi_status ensure(chfsi_ctx ctx, DevBuf& b, size_t bytes) {
+  if (b.bytes >= bytes) return CHFSI_OK;
+  if (b.ptr) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(b.ptr);
+    b.ptr = nullptr;
+    b.bytes = 0;
+  }
+  bytes = std::max<size_t>(bytes, 256);
+  if (cudaMalloc(&b.ptr, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    set_err(ctx, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+    return CHFSI_ERR_NOMEM;
+  }
+  b.bytes = bytes;
+  return CHFSI_OK;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+chfsi_status make_tmap_2d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64_t kreal, int64_t rows,
+                          int64_t ld_doubles, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) {
+    set_err(ctx, "cuTensorMapEncodeTiled unavailable");
+    return CHFSI_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)kreal, (cuuint64_t)std::max<int64_t>(rows, 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld_doubles * 8)};
+  cuuint32_t box[2] = {(cuuint32_t)kBKHalf, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_err(ctx, "cuTensorMapEncodeTiled(2d) failed: " + std::to_string((int)r));
+    return CHFSI_ERR_CUDA;
+  }
+  return CHFSI_OK;
+}
+
+chfsi_status make_tmap_3d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64_t kreal, int64_t cols,
+                          int64_t chunks, int64_t ld_doubles, int64_t chunk_doubles, int box_cols) {
+  auto enc = get_encode();
+  if (!enc) {
+    set_err(ctx, "cuTensorMapEncodeTiled unavailable");
+    return CHFSI_ERR_CUDA;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)kreal, (cuuint64_t)std::max<int64_t>(cols, 1),
+                        (cuuint64_t)std::max<int64_t>(chunks, 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld_doubles * 8), (cuuint64_t)(std::max<int64_t>(chunk_doubles, ld_doubles) * 8)};
+  cuuint32_t box[3] = {(cuuint32_t)kBKHalf, (cuuint32_t)box_cols, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_err(ctx, "cuTensorMapEncodeTiled(3d) failed: " + std::to_string((int)r));
+    return CHFSI_ERR_CUDA;
+  }
+  return CHFSI_OK;
+}
+
+static inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// Common driver for one K1 launch over the active columns [col0, k) of the B operand.
+struct Operand {
+  CUtensorMap tm;
+  int32_t b_col0;
+};
+
+// Build the B-operand descriptor for the current step.
+//  p == 1: B = local state buffer (nloc x kcols, ld), column coordinate = absolute column.
+//  p > 1 : B = packed [rank][ka][nloc] buffer, column coordinate = column - col0.
+static chfsi_status b_operand(chfsi_ctx ctx, Operand* op, const void* buf, int64_t n_or_nloc, int64_t ld,
+                              int64_t kcols, int64_t col0, int nranks, int box_cols) {
+  if (nranks == 1) {
+    op->b_col0 = (int32_t)col0;
+    return make_tmap_3d(ctx, &op->tm, buf, 2 * n_or_nloc, kcols, 1, 2 * ld, 2 * ld * kcols, box_cols);
+  }
+  op->b_col0 = 0;
+  const int64_t ka = kcols - col0;
+  return make_tmap_3d(ctx, &op->tm, buf, 2 * n_or_nloc, ka, nranks, 2 * n_or_nloc, 2 * n_or_nloc * ka, box_cols);
+}
+
+chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
+                       const void* Q, int64_t ldq, int64_t k, void* out, int64_t ldo) {
+  (void)row0;
+  if (k == 0) return CHFSI_OK;
+  const int p = ctx->nranks;
+  TileChoice t = choose_filter_tile(nloc, k, ctx->num_sms);
+  CUtensorMap tmA;
+  chfsi_status st = make_tmap_2d(ctx, &tmA, Hp, 2 * n, nloc, 2 * ldh, t.bm);
+  if (st) return st;
+  Operand op;
+  const void* bsrc = Q;
+  int64_t bld = ldq;
+  if (p > 1) {
+    // gather the full-height Q into R0 = [rank][k][nloc]
+    st = ensure(ctx, ctx->R0, sizeof(double) * 2 * (size_t)n * (size_t)k);
+    if (st) return st;
+    double* R = static_cast<double*>(ctx->R0.ptr);
+    double* mine = R + (size_t)2 * nloc * k * ctx->rank;
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(mine, 16 * nloc, Q, 16 * ldq, 16 * nloc, k, cudaMemcpyDeviceToDevice,
+                                          ctx->stream));
+    st = comm_allgather_inplace(ctx, R, (size_t)2 * nloc * k);
+    if (st) return st;
+    bsrc = R;
+    bld = nloc;
+  }
+  st = b_operand(ctx, &op, bsrc, p == 1 ? n : nloc, bld, k, 0, p, t.bnc);
+  if (st) return st;
+  StepParams sp{};
+  sp.nrows = nloc;
+  const int64_t kr = p == 1 ? 2 * n : 2 * nloc;
+  sp.kt_per_rank = (int32_t)((kr + kBK - 1) / kBK);
+  sp.num_kt = sp.kt_per_rank * p;
+  sp.a_rank_stride = (int32_t)(2 * nloc);
+  sp.col0 = 0;
+  sp.col_end = (int32_t)k;
+  sp.fin_end = (int32_t)k;
+  sp.b_col0 = op.b_col0;
+  sp.flags = 0;
+  sp.a = 1.0;
+  sp.b = 0.0;
+  sp.c = 0.0;
+  sp.out = static_cast<double2*>(out);
+  sp.ld_out = ldo;
+  CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, sp, ctx->stream));
+  ctx->launches++;
+  return CHFSI_OK;
+}
+
+chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
+                         void* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c, double e,
+                         bool check_finite) {
+  (void)row0;
+  if (k == 0) return CHFSI_OK;
+  const int p = ctx->nranks;
+  const int32_t mk = deg[k - 1];
+  // sigma schedule (Alg 2 l2, l6) in double on the host, as printed
+  std::vector<double> sigma(mk + 1);
+  sigma[0] = e / (lambda1 - c);
+  for (int i = 1; i < mk; ++i) sigma[i] = 1.0 / (2.0 / sigma[0] - sigma[i - 1]);
+
+  const int64_t ldl = round_up(nloc, 2);
+  chfsi_status st = ensure(ctx, ctx->L0, sizeof(double) * 2 * (size_t)ldl * k);
+  if (!st) st = ensure(ctx, ctx->L1, sizeof(double) * 2 * (size_t)ldl * k);
+  if (!st) st = ensure(ctx, ctx->flag, 64);
+  if (p > 1 && !st) st = ensure(ctx, ctx->R0, sizeof(double) * 2 * (size_t)n * k);
+  if (p > 1 && !st) st = ensure(ctx, ctx->R1, sizeof(double) * 2 * (size_t)n * k);
+  if (st) return st;
+  double2* L[2] = {static_cast<double2*>(ctx->L0.ptr), static_cast<double2*>(ctx->L1.ptr)};
+  double* R[2] = {static_cast<double*>(ctx->R0.ptr), static_cast<double*>(ctx->R1.ptr)};
+  int* flag = static_cast<int*>(ctx->flag.ptr);
+  if (check_finite) CHFSI_CUDA_TRY(ctx, cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+  // Y_0 -> L0 (the caller's Y is the output and must never be the B operand)
+  CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(L[0], 16 * ldl, Y, 16 * ldy, 16 * nloc, k, cudaMemcpyDeviceToDevice,
+                                        ctx->stream));
+  if (p > 1) {
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(R[0] + (size_t)2 * nloc * k * ctx->rank, 16 * nloc, Y, 16 * ldy, 16 * nloc,
+                                          k, cudaMemcpyDeviceToDevice, ctx->stream));
+    st = comm_allgather_inplace(ctx, R[0], (size_t)2 * nloc * k);
+    if (st) return st;
+  }
+  CUtensorMap tmA;
+  int last_bm = -1;
+  int64_t s = 0;  // active start s_i = #{j : deg[j] <= i}
+  for (int i = 0; i < mk; ++i) {
+    while (s < k && deg[s] <= i) ++s;
+    if (s >= k) break;
+    int64_t s_next = s;
+    while (s_next < k && deg[s_next] <= i + 1) ++s_next;
+    const int64_t ka = k - s;
+    TileChoice t = choose_filter_tile(nloc, ka, ctx->num_sms);
+    if (t.bm != last_bm) {
+      st = make_tmap_2d(ctx, &tmA, Hp, 2 * n, nloc, 2 * ldh, t.bm);
+      if (st) return st;
+      last_bm = t.bm;
+    }
+    const int cur = i & 1, oth = cur ^ 1;
+    Operand op;
+    if (p == 1)
+      st = b_operand(ctx, &op, L[cur], n, ldl, k, s, 1, t.bnc);
+    else
+      st = b_operand(ctx, &op, R[cur], nloc, nloc, k, s, p, t.bnc);
+    if (st) return st;
+    StepParams sp{};
+    sp.nrows = nloc;
+    const int64_t kr = p == 1 ? 2 * n : 2 * nloc;
+    sp.kt_per_rank = (int32_t)((kr + kBK - 1) / kBK);
+    sp.num_kt = sp.kt_per_rank * p;
+    sp.a_rank_stride = (int32_t)(2 * nloc);
+    sp.col0 = (int32_t)s;
+    sp.col_end = (int32_t)k;
+    sp.fin_end = (int32_t)s_next;
+    sp.b_col0 = op.b_col0;
+    if (i == 0) {  // Y_1 = (sigma_1/e)(H - cI) Y_0
+      sp.a = sigma[0] / e;
+      sp.b = 0.0;
+      sp.flags = 1;
+    } else {  // Y_{i+1} = (2 sigma_{i+1}/e)(H - cI) Y_i - sigma_{i+1} sigma_i Y_{i-1}
+      sp.a = 2.0 * sigma[i] / e;
+      sp.b = sigma[i] * sigma[i - 1];
+      sp.flags = 3;
+    }
+    sp.c = c;
+    sp.y_cur = L[cur];
+    sp.ld_cur = ldl;
+    sp.y_prev = L[oth];
+    sp.ld_prev = ldl;
+    sp.y_next = L[oth];
+    sp.ld_next = ldl;
+    sp.out = static_cast<double2*>(Y);
+    sp.ld_out = ldy;
+    const int64_t ka_next = k - s_next;
+    if (p > 1 && ka_next > 0) {
+      sp.r_next = reinterpret_cast<double2*>(R[oth] + (size_t)2 * nloc * ka_next * ctx->rank);
+      sp.ld_r_next = nloc;
+    }
+    sp.nonfinite = check_finite ? flag : nullptr;
+    CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, sp, ctx->stream));
+    ctx->launches++;
+    if (p > 1 && ka_next > 0) {
+      st = comm_allgather_inplace(ctx, R[oth], (size_t)2 * nloc * ka_next);
+      if (st) return st;
+    }
+  }
+  if (check_finite) {
+    int h = 0;
+    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (h) {
+      set_err(ctx, "chfsi_filter: non-finite value in the filtered block");
+      return CHFSI_ERR_NONFINITE;
+    }
+  }
+  return CHFSI_OK;
+}
+
+}  // namespace chfsi
+
+using namespace chfsi;
+
+// ------------------------------------------------------------------------------------------------
+extern "C" {
+
+chfsi_status chfsi_ctx_create(chfsi_ctx* out, int32_t device, void* cuda_stream, void* nccl_comm, int32_t rank,
+                              int32_t nranks) {
+  if (!out) return CHFSI_ERR_ARG;
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_comm)) return CHFSI_ERR_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return CHFSI_ERR_CUDA;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return CHFSI_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return CHFSI_ERR_CUDA;
+  if (prop.major != 10) return CHFSI_ERR_CUDA;  // sm_100a build only
+  chfsi_ctx ctx = new chfsi_ctx_s();
+  ctx->device = device;
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  ctx->num_sms = prop.multiProcessorCount;
+  ctx->nccl_comm = nccl_comm;
+  if (cuda_stream) {
+    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      return CHFSI_ERR_CUDA;
+    }
+    ctx->own_stream = true;
+  }
+  if (cublasCreate(&ctx->cublas) != CUBLAS_STATUS_SUCCESS ||
+      cublasSetStream(ctx->cublas, ctx->stream) != CUBLAS_STATUS_SUCCESS ||
+      cusolverDnCreate(&ctx->cusolver) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnSetStream(ctx->cusolver, ctx->stream) != CUSOLVER_STATUS_SUCCESS) {
+    chfsi_ctx_destroy(ctx);
+    return CHFSI_ERR_CUDA;
+  }
+  chfsi_status st = comm_init(ctx);
+  if (st) {
+    chfsi_ctx_destroy(ctx);
+    return st;
+  }
+  *out = ctx;
+  return CHFSI_OK;
+}
+
+chfsi_status chfsi_ctx_reserve(chfsi_ctx ctx, int64_t n, int64_t nloc, int64_t kmax) {
+  if (!ctx || n < 1 || nloc < 1 || kmax < 1 || nloc > n) return CHFSI_ERR_ARG;
+  cudaSetDevice(ctx->device);
+  const size_t ldl = (size_t)round_up(nloc, 2);
+  const size_t blk = sizeof(double) * 2 * ldl * kmax;
+  chfsi_status st = CHFSI_OK;
+  if (!st) st = ensure(ctx, ctx->L0, blk);
+  if (!st) st = ensure(ctx, ctx->L1, blk);
+  if (!st) st = ensure(ctx, ctx->flag, 64);
+  if (ctx->nranks > 1) {
+    if (!st) st = ensure(ctx, ctx->R0, sizeof(double) * 2 * (size_t)n * kmax);
+    if (!st) st = ensure(ctx, ctx->R1, sizeof(double) * 2 * (size_t)n * kmax);
+  }
+  return st;
+}
+
+void chfsi_ctx_destroy(chfsi_ctx ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  comm_destroy(ctx);
+  DevBuf* bufs[] = {&ctx->L0, &ctx->L1, &ctx->R0, &ctx->R1, &ctx->flag, &ctx->w1, &ctx->w2, &ctx->w3, &ctx->w4,
+                    &ctx->small1, &ctx->small2, &ctx->small3, &ctx->solver_ws, &ctx->devinfo, &ctx->lz};
+  for (DevBuf* b : bufs)
+    if (b->ptr) cudaFree(b->ptr);
+  if (ctx->cublas) cublasDestroy(ctx->cublas);
+  if (ctx->cusolver) cusolverDnDestroy(ctx->cusolver);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* chfsi_last_error(chfsi_ctx ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t chfsi_kernel_launches(chfsi_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+chfsi_status chfsi_filter(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
+                          void* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c, double e,
+                          int64_t* matvecs) {
+  if (!ctx) return CHFSI_ERR_ARG;
+  ctx->err.clear();
+  if (n < 1 || nloc < 1 || nloc > n || row0 < 0 || row0 + nloc > n || ldh < n || ldy < nloc || k < 0 ||
+      (k > 0 && (!Hp || !Y || !deg))) {
+    set_err(ctx, "chfsi_filter: bad dimensions / leading dimensions / pointers");
+    return CHFSI_ERR_ARG;
+  }
+  if (ctx->nranks > 1 && (nloc * ctx->nranks != n || row0 != nloc * ctx->rank)) {
+    set_err(ctx, "chfsi_filter: nranks > 1 needs equal row panels (n = nranks * nloc, row0 = rank * nloc)");
+    return CHFSI_ERR_ARG;
+  }
+  if (2 * n > INT32_MAX / 2) {
+    set_err(ctx, "chfsi_filter: n too large");
+    return CHFSI_ERR_ARG;
+  }
+  if (!(e > 0.0) || !(lambda1 < c - e) || !std::isfinite(c) || !std::isfinite(e) || !std::isfinite(lambda1)) {
+    set_err(ctx, "chfsi_filter: need e > 0 and lambda1 < c - e (the scaling point left of [alpha, beta])");
+    return CHFSI_ERR_ARG;
+  }
+  int64_t mv = 0;
+  for (int64_t j = 0; j < k; ++j) {
+    if (deg[j] < 1 || deg[j] > CHFSI_MAX_DEGREE || (j > 0 && deg[j] < deg[j - 1])) {
+      set_err(ctx, "chfsi_filter: degrees must be ascending in [1, CHFSI_MAX_DEGREE]");
+      return CHFSI_ERR_ARG;
+    }
+    mv += deg[j];
+  }
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return CHFSI_ERR_CUDA;
+  chfsi_status st = filter_impl(ctx, n, row0, nloc, Hp, ldh, Y, ldy, k, deg, lambda1, c, e, true);
+  if (st == CHFSI_OK && matvecs) *matvecs = mv;
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,82 @@
+// ctx.cuh -- the library context behind the chfsi_ctx handle, workspace management, TMA descriptor
+// encoding and the communication layer used by every entry point.
+#pragma once
+#include <cublas_v2.h>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <string>
+#include <vector>
+
+#include "chfsi.h"
+#include "common.cuh"
+
+namespace chfsi {
+
+// A device buffer owned by the context; grows on demand (never inside a step loop once reserved).
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct Comm;  // comm.cu: NCCL (loaded with dlopen) or a single rank
+
+}  // namespace chfsi
+
+struct chfsi_ctx_s {
+  int device = 0;
+  int rank = 0, nranks = 1;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void* nccl_comm = nullptr;
+  chfsi::Comm* comm = nullptr;
+  cublasHandle_t cublas = nullptr;
+  cusolverDnHandle_t cusolver = nullptr;
+  std::string err;
+  int64_t launches = 0;
+
+  // workspace
+  chfsi::DevBuf L0, L1;          // filter local state (nloc x k each)
+  chfsi::DevBuf R0, R1;          // p > 1: packed full-height B operands
+  chfsi::DevBuf flag;            // int nonfinite flag (+ small scalars)
+  chfsi::DevBuf w1, w2, w3, w4;  // general nloc x k / k x k scratch for QR / RR / solver
+  chfsi::DevBuf small1, small2, small3;
+  chfsi::DevBuf solver_ws;       // cuSOLVER workspace
+  chfsi::DevBuf devinfo;
+  chfsi::DevBuf lz;              // Lanczos basis
+  chfsi::DevBuf host_pinned_dummy;
+  std::vector<char> hbuf;        // host staging
+};
+
+namespace chfsi {
+
+chfsi_status ensure(chfsi_ctx ctx, DevBuf& b, size_t bytes);
+void set_err(chfsi_ctx ctx, const std::string& msg);
+
+// TMA descriptors (FLOAT64, 128B swizzle, OOB -> zero fill)
+//  A: real K-major matrix of `rows` rows with `kreal` doubles each, row stride ld_doubles; box (16, box_rows)
+//  B: 3-D (kreal, cols, chunks) with column stride ld_doubles and chunk stride chunk_doubles
+chfsi_status make_tmap_2d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64_t kreal, int64_t rows,
+                          int64_t ld_doubles, int box_rows);
+chfsi_status make_tmap_3d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64_t kreal, int64_t cols,
+                          int64_t chunks, int64_t ld_doubles, int64_t chunk_doubles, int box_cols);
+
+// Communication (comm.cu). With nranks == 1 every collective is a no-op / local copy.
+chfsi_status comm_init(chfsi_ctx ctx);
+void comm_destroy(chfsi_ctx ctx);
+// in-place allgather: buf holds nranks chunks of `count` doubles; chunk `rank` is the send part
+chfsi_status comm_allgather_inplace(chfsi_ctx ctx, double* buf, size_t count);
+chfsi_status comm_allreduce_sum(chfsi_ctx ctx, double* buf, size_t count);
+chfsi_status comm_bcast(chfsi_ctx ctx, double* buf, size_t count, int root);
+
+// internal (no status marshalling) versions of the public entry points, used by the solver
+chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
+                         void* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c, double e,
+                         bool check_finite);
+// HQ: out (nloc x k) = H Q for Q (nloc x k, this rank's rows). Uses the K1 kernel, plain epilogue.
+chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
+                       const void* Q, int64_t ldq, int64_t k, void* out, int64_t ldo);
+
+}  // namespace chfsi

@@ -1,0 +1,140 @@
+"""GPU parity of chfsi_filter (K1 through the C-ABI) against the oracle (Alg 2, naive C) and against
+the closed forms of App. A. Tolerances from BASELINE.json: filter <= 1e-11 relative per column (error
+budget sqrt(n) eps per step x <= 40 steps), diagonal closed form <= 1e-13."""
+import os
+
+import numpy as np
+import pytest
+
+import gen as G
+import oracle as O
+from gen.configs import C4_INTERVAL, CONFIGS, c4_ramp
+
+pytestmark = pytest.mark.gpu
+VARIANTS = ["0", "1", "2", "3"]
+
+
+def crand(rng, *shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+@pytest.fixture
+def ctx(gpu_lib):
+    c = gpu_lib.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.fixture(params=VARIANTS)
+def variant(request):
+    os.environ["CHFSI_FILTER_VARIANT"] = request.param
+    yield request.param
+    os.environ.pop("CHFSI_FILTER_VARIANT", None)
+
+
+def run_filter(chfsi, ctx, H, Y0, deg, l1, c, e):
+    Hd = chfsi.to_colmajor(H)
+    Yd = chfsi.to_colmajor(Y0)
+    mv = ctx.filter(Hd, Yd, deg, l1, c, e)
+    assert mv == sum(deg)
+    return Yd.cpu().numpy()
+
+
+def colrel(A, B):
+    return np.linalg.norm(A - B, axis=0) / np.linalg.norm(B, axis=0)
+
+
+def test_filter_diag_closed_form(gpu_lib, ctx, variant):
+    rng = np.random.default_rng(1)
+    n = 203  # ragged in every tile dimension
+    d = np.sort(rng.uniform(-2.0, 40.0, n))
+    deg = sorted(rng.integers(1, 41, 37).tolist())
+    Y0 = crand(rng, n, len(deg))
+    l1, a, b = -2.3, -1.2, 40.5
+    c, e = (a + b) / 2, (b - a) / 2
+    Y = run_filter(gpu_lib, ctx, np.diag(d.astype(complex)), Y0, deg, l1, c, e)
+    Yc = O.filter_diag_closed(d, Y0, deg, l1, c, e)
+    assert colrel(Y, Yc).max() <= 1e-13
+
+
+@pytest.mark.parametrize("n,k", [(512, 48), (300, 37), (129, 5)])
+def test_filter_dense_vs_oracle(gpu_lib, ctx, variant, n, k):
+    w = G.wy(n, int(0.9 * n), n + k)
+    H = w.full()
+    rng = np.random.default_rng(n * k)
+    deg = sorted(rng.integers(1, 21, k).tolist())
+    Y0 = crand(rng, n, k)
+    l1, a, b = w.lam[0] - 0.05, w.lam[k], 45.0
+    c, e = (a + b) / 2, (b - a) / 2
+    Y = run_filter(gpu_lib, ctx, H, Y0, deg, l1, c, e)
+    Yo, _ = O.chebyshev_filter(H, Y0, deg, l1, c, e)
+    assert colrel(Y, Yo).max() <= 1e-11
+    Yc = O.filter_wy_closed(w, Y0, deg, l1, c, e)
+    assert colrel(Y, Yc).max() <= 1e-11
+
+
+def test_filter_column_independence_bitwise(gpu_lib, ctx):
+    n = 257
+    Gm = G.gue(n, 3, G.stream(5, n))
+    rng = np.random.default_rng(4)
+    deg = [1, 2, 2, 6, 9, 9, 13]
+    Y0 = crand(rng, n, len(deg))
+    iv = C4_INTERVAL
+    c, e = (iv["alpha"] + iv["beta"]) / 2, (iv["beta"] - iv["alpha"]) / 2
+    Y = run_filter(gpu_lib, ctx, Gm, Y0, deg, iv["lambda1"], c, e)
+    for j in (0, 3, 6):
+        Yj = run_filter(gpu_lib, ctx, Gm, Y0[:, j:j + 1], [deg[j]], iv["lambda1"], c, e)
+        assert np.array_equal(Yj[:, 0], Y[:, j])
+
+
+def test_filter_ld_and_panel_views(gpu_lib, ctx):
+    # ld > rows for Y and H (sub-views of larger allocations)
+    import torch
+
+    n, k = 130, 9
+    w = G.wy(n, 100, 2)
+    H = w.full()
+    rng = np.random.default_rng(2)
+    Y0 = crand(rng, n, k)
+    deg = [3] * 4 + [7] * 5
+    l1, a, b = w.lam[0] - 0.1, w.lam[20], 44.0
+    c, e = (a + b) / 2, (b - a) / 2
+    Hbig = gpu_lib.colmajor(n + 6, n + 3)
+    Hbig[:n, :n].copy_(torch.as_tensor(H))
+    Ybig = gpu_lib.colmajor(n + 10, k)
+    Ybig[:n].copy_(torch.as_tensor(Y0))
+    ctx.filter(Hbig[:n, :n], Ybig[:n], deg, l1, c, e)
+    Yo, _ = O.chebyshev_filter(H, Y0, deg, l1, c, e)
+    assert colrel(Ybig[:n].cpu().numpy(), Yo).max() <= 1e-11
+
+
+def test_filter_errors(gpu_lib, ctx):
+    n = 16
+    H = gpu_lib.to_colmajor(np.eye(n))
+    Y = gpu_lib.to_colmajor(np.ones((n, 2)))
+    with pytest.raises(gpu_lib.ChfsiError, match="ERR_ARG"):
+        ctx.filter(H, Y, [3, 1], -2.0, 0.0, 1.0)
+    with pytest.raises(gpu_lib.ChfsiError, match="ERR_ARG"):
+        ctx.filter(H, Y, [1, 1], -2.0, 0.0, 0.0)
+    with pytest.raises(gpu_lib.ChfsiError, match="ERR_ARG"):
+        ctx.filter(H, Y, [1, 1], 0.5, 0.0, 1.0)  # lambda1 inside [alpha, beta]
+    with pytest.raises(gpu_lib.ChfsiError, match="ERR_ARG"):
+        ctx.filter(H, Y, [1, 65], -2.0, 0.0, 1.0)  # degree > CHFSI_MAX_DEGREE
+    Y2 = gpu_lib.to_colmajor(np.full((n, 2), np.nan))
+    with pytest.raises(gpu_lib.ChfsiError, match="ERR_NONFINITE"):
+        ctx.filter(H, Y2, [1, 2], -2.0, 0.0, 1.0)
+    assert ctx.filter(H, gpu_lib.colmajor(n, 0), [], -2.0, 0.0, 1.0) == 0  # empty block
+
+
+def test_filter_c1_shape_sampled(gpu_lib, ctx):
+    # c1 shape (n = 4096, k = 240) with the c4 ramp degrees 8..40; oracle on a column sample
+    n, k = 4096, 240
+    Gm = G.gue(n, 7, G.stream(5, n))
+    Y0 = G.start_basis(n, k, 7)
+    deg = c4_ramp(k)
+    iv = C4_INTERVAL
+    c, e = (iv["alpha"] + iv["beta"]) / 2, (iv["beta"] - iv["alpha"]) / 2
+    Y = run_filter(gpu_lib, ctx, Gm, Y0, deg, iv["lambda1"], c, e)
+    cols = [0, 1, 119, 238, 239]
+    Yo, _ = O.chebyshev_filter(Gm, Y0[:, cols], [deg[j] for j in cols], iv["lambda1"], c, e)
+    assert colrel(Y[:, cols], Yo).max() <= 1e-11
