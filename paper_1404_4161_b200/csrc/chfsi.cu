@@ -341,7 +341,8 @@ void chfsi_ctx_destroy(chfsi_ctx ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   comm_destroy(ctx);
   DevBuf* bufs[] = {&ctx->L0, &ctx->L1, &ctx->R0, &ctx->R1, &ctx->flag, &ctx->w1, &ctx->w2, &ctx->w3, &ctx->w4,
-                    &ctx->small1, &ctx->small2, &ctx->small3, &ctx->solver_ws, &ctx->devinfo, &ctx->lz};
+                    &ctx->small1, &ctx->small2, &ctx->small3, &ctx->solver_ws, &ctx->devinfo, &ctx->lz,
+                    &ctx->ya,    &ctx->xl,     &ctx->tb,     &ctx->idx};
   for (DevBuf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   if (ctx->cublas) cublasDestroy(ctx->cublas);

@@ -46,6 +46,7 @@ struct chfsi_ctx_s {
   chfsi::DevBuf solver_ws;       // cuSOLVER workspace
   chfsi::DevBuf devinfo;
   chfsi::DevBuf lz;              // Lanczos basis
+  chfsi::DevBuf ya, xl, tb, idx;  // solver: active block, locked block, filter block, column indices
   chfsi::DevBuf host_pinned_dummy;
   std::vector<char> hbuf;        // host staging
 };

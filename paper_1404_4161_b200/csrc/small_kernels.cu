@@ -1,0 +1,223 @@
+// small_kernels.cu -- see small_kernels.cuh.
+#include "small_kernels.cuh"
+
+namespace chfsi {
+
+namespace {
+
+__global__ void hemv_kernel(int64_t n, int64_t nloc, const double2* __restrict__ Hp, int64_t ldh,
+                            const double2* __restrict__ v, double2* __restrict__ w) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= nloc) return;
+  const double2* h = Hp + r * ldh;
+  double sr0 = 0, si0 = 0, sr1 = 0, si1 = 0;
+  int64_t q = lane;
+  for (; q + 32 < n; q += 64) {
+    const double2 a = __ldcs(h + q), b = __ldcs(h + q + 32);
+    const double2 x = __ldg(v + q), y = __ldg(v + q + 32);
+    sr0 += a.x * x.x + a.y * x.y;
+    si0 += a.x * x.y - a.y * x.x;
+    sr1 += b.x * y.x + b.y * y.y;
+    si1 += b.x * y.y - b.y * y.x;
+  }
+  if (q < n) {
+    const double2 a = __ldcs(h + q);
+    const double2 x = __ldg(v + q);
+    sr0 += a.x * x.x + a.y * x.y;
+    si0 += a.x * x.y - a.y * x.x;
+  }
+  double sr = warp_sum(sr0 + sr1), si = warp_sum(si0 + si1);
+  if (lane == 0) w[r] = make_double2(sr, si);
+}
+
+template <int NT>
+__device__ double block_sum(double v) {
+  __shared__ double red[NT / 32];
+  v = warp_sum(v);
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double s = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NT / 32; ++i) s += red[i];
+  }
+  return s;
+}
+
+constexpr int kRedThreads = 256;
+
+__global__ void colnorm2_kernel(int64_t rows, const double2* __restrict__ X, int64_t ldx, double* out) {
+  const double2* x = X + (int64_t)blockIdx.x * ldx;
+  double s = 0;
+  for (int64_t r = threadIdx.x; r < rows; r += kRedThreads) {
+    const double2 a = x[r];
+    s += a.x * a.x + a.y * a.y;
+  }
+  s = block_sum<kRedThreads>(s);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+__global__ void resid2_kernel(int64_t rows, const double2* __restrict__ HY, int64_t ld1, const double2* __restrict__ Y,
+                              int64_t ld2, const double* __restrict__ mu, double* out) {
+  const double2* hy = HY + (int64_t)blockIdx.x * ld1;
+  const double2* y = Y + (int64_t)blockIdx.x * ld2;
+  const double m = mu[blockIdx.x];
+  double s = 0;
+  for (int64_t r = threadIdx.x; r < rows; r += kRedThreads) {
+    const double2 a = hy[r], b = y[r];
+    const double dr = a.x - m * b.x, di = a.y - m * b.y;
+    s += dr * dr + di * di;
+  }
+  s = block_sum<kRedThreads>(s);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+__global__ void hermitize_kernel(int64_t k, double2* G, int64_t ldg) {
+  const int64_t j = blockIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > j || j >= k) return;
+  const double2 a = G[j * ldg + i], b = G[i * ldg + j];
+  if (i == j) {
+    G[j * ldg + i] = make_double2(a.x, 0.0);
+    return;
+  }
+  // upper (i,j) = (a + conj(b))/2, lower (j,i) = conj(upper)
+  const double2 u = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+  G[j * ldg + i] = u;
+  G[i * ldg + j] = make_double2(u.x, -u.y);
+}
+
+__global__ void col_gather_kernel(int64_t rows, const double2* __restrict__ src, int64_t lds, const int* __restrict__ idx,
+                                  double2* __restrict__ dst, int64_t ldd) {
+  const int64_t j = blockIdx.y;
+  const double2* s = src + (int64_t)idx[j] * lds;
+  double2* d = dst + j * ldd;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+    d[r] = s[r];
+}
+
+__global__ void col_phase_kernel(int64_t rows, double2* Q, int64_t ldq, const double2* R, int64_t ldr) {
+  const int64_t j = blockIdx.y;
+  const double2 d = R[j * ldr + j];
+  const double a = hypot(d.x, d.y);
+  const double pr = a > 0 ? d.x / a : 1.0, pi = a > 0 ? d.y / a : 0.0;
+  double2* q = Q + j * ldq;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const double2 x = q[r];
+    q[r] = make_double2(x.x * pr - x.y * pi, x.x * pi + x.y * pr);
+  }
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void random_block_kernel(int64_t rows, int64_t row0, uint64_t seed, uint64_t stream_base,
+                                    uint64_t stream_stride, double2* X, int64_t ldx) {
+  const int64_t j = blockIdx.y;
+  const uint64_t strm = stream_base | (stream_stride * (uint64_t)j);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = (uint64_t)(row0 + r);
+    const uint64_t h0 = splitmix64(seed ^ (strm << 40) ^ (2 * g));
+    const uint64_t h1 = splitmix64(seed ^ (strm << 40) ^ (2 * g + 1));
+    const double u0 = (double)(h0 >> 11) * (1.0 / 9007199254740992.0);
+    const double u1 = (double)(h1 >> 11) * (1.0 / 9007199254740992.0);
+    X[j * ldx + r] = make_double2(__dadd_rn(__dmul_rn(2.0, u0), -1.0), __dadd_rn(__dmul_rn(2.0, u1), -1.0));
+  }
+}
+
+__global__ void scale_kernel(int64_t rows, double2* x, double s) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const double2 a = x[r];
+    x[r] = make_double2(a.x * s, a.y * s);
+  }
+}
+
+__global__ void orth_err_kernel(int64_t k, const double2* G, int64_t ldg, unsigned long long* out) {
+  const int64_t j = blockIdx.y;
+  double m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 a = G[j * ldg + i];
+    const double e = hypot(a.x - (i == j ? 1.0 : 0.0), a.y);
+    m = fmax(m, e);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __double_as_longlong(m));  // m >= 0: bit order == value order
+}
+
+inline unsigned grid1(int64_t rows, int threads) {
+  int64_t b = (rows + threads - 1) / threads;
+  return (unsigned)(b < 1 ? 1 : (b > 1024 ? 1024 : b));
+}
+
+}  // namespace
+
+cudaError_t launch_hemv(int64_t n, int64_t nloc, const double2* Hp, int64_t ldh, const double2* v, double2* w,
+                        cudaStream_t st) {
+  const int warps = 8;
+  hemv_kernel<<<(unsigned)((nloc + warps - 1) / warps), warps * 32, 0, st>>>(n, nloc, Hp, ldh, v, w);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colnorm2(int64_t rows, int64_t cols, const double2* X, int64_t ldx, double* out, cudaStream_t st) {
+  if (cols <= 0) return cudaSuccess;
+  colnorm2_kernel<<<(unsigned)cols, kRedThreads, 0, st>>>(rows, X, ldx, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resid2(int64_t rows, int64_t cols, const double2* HY, int64_t ld1, const double2* Y, int64_t ld2,
+                          const double* mu, double* out, cudaStream_t st) {
+  if (cols <= 0) return cudaSuccess;
+  resid2_kernel<<<(unsigned)cols, kRedThreads, 0, st>>>(rows, HY, ld1, Y, ld2, mu, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hermitize(int64_t k, double2* G, int64_t ldg, cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((k + 127) / 128), (unsigned)k);
+  hermitize_kernel<<<grid, 128, 0, st>>>(k, G, ldg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_col_gather(int64_t rows, int64_t cols, const double2* src, int64_t lds, const int* idx,
+                              double2* dst, int64_t ldd, cudaStream_t st) {
+  if (cols <= 0 || rows <= 0) return cudaSuccess;
+  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), (unsigned)cols);
+  col_gather_kernel<<<grid, 256, 0, st>>>(rows, src, lds, idx, dst, ldd);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_col_phase(int64_t rows, int64_t cols, double2* Q, int64_t ldq, const double2* R, int64_t ldr,
+                             cudaStream_t st) {
+  if (cols <= 0 || rows <= 0) return cudaSuccess;
+  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), (unsigned)cols);
+  col_phase_kernel<<<grid, 256, 0, st>>>(rows, Q, ldq, R, ldr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_random_block(int64_t rows, int64_t cols, int64_t row0, uint64_t seed, uint64_t stream_base,
+                                uint64_t stream_stride, double2* X, int64_t ldx, cudaStream_t st) {
+  if (cols <= 0 || rows <= 0) return cudaSuccess;
+  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), (unsigned)cols);
+  random_block_kernel<<<grid, 256, 0, st>>>(rows, row0, seed, stream_base, stream_stride, X, ldx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale(int64_t rows, double2* x, double s, cudaStream_t st) {
+  scale_kernel<<<grid1(rows, 256), 256, 0, st>>>(rows, x, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_orth_err(int64_t k, const double2* G, int64_t ldg, double* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((k + 255) / 256), (unsigned)k);
+  orth_err_kernel<<<grid, 256, 0, st>>>(k, G, ldg, reinterpret_cast<unsigned long long*>(out));
+  return cudaGetLastError();
+}
+
+}  // namespace chfsi

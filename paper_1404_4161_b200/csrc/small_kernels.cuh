@@ -1,0 +1,36 @@
+// small_kernels.cuh -- the supporting (non-filter) device kernels of ChFSI: the Lanczos mat-vec (K2,
+// HBM-bound), per-column reductions for norms / residuals (K6), Hermitisation (K9), column gathers
+// and scalings (K7), and the counter-based random block (R22). All reductions run in a fixed order
+// (deterministic, independent of launch timing).
+#pragma once
+#include "common.cuh"
+
+namespace chfsi {
+
+// w[r] = sum_q conj(Hp[q, r]) v[q] for the nloc local rows r (K2: one warp per row, HBM-bound:
+// 16 n nloc bytes per call)
+cudaError_t launch_hemv(int64_t n, int64_t nloc, const double2* Hp, int64_t ldh, const double2* v, double2* w,
+                        cudaStream_t st);
+// out[j] = sum_r |X[r, j]|^2 (rows x cols)
+cudaError_t launch_colnorm2(int64_t rows, int64_t cols, const double2* X, int64_t ldx, double* out, cudaStream_t st);
+// out[j] = sum_r |HY[r, j] - mu[j] Y[r, j]|^2 (mu on device)
+cudaError_t launch_resid2(int64_t rows, int64_t cols, const double2* HY, int64_t ld1, const double2* Y, int64_t ld2,
+                          const double* mu, double* out, cudaStream_t st);
+// G <- (G + G^H)/2, imaginary diagonal set to 0
+cudaError_t launch_hermitize(int64_t k, double2* G, int64_t ldg, cudaStream_t st);
+// dst[:, j] = src[:, idx[j]] for j < cols (idx on device); src and dst must not overlap
+cudaError_t launch_col_gather(int64_t rows, int64_t cols, const double2* src, int64_t lds, const int* idx,
+                              double2* dst, int64_t ldd, cudaStream_t st);
+// Q[:, j] *= phase(R[j, j]) (Householder fallback: make R's diagonal real positive)
+cudaError_t launch_col_phase(int64_t rows, int64_t cols, double2* Q, int64_t ldq, const double2* R, int64_t ldr,
+                             cudaStream_t st);
+// X[r, j] = (2u_{2g} - 1) + i (2u_{2g+1} - 1), g = row0 + r, u from splitmix64(seed ^ (stream_j << 40) ^ idx),
+// stream_j = stream_base | j (R22)
+cudaError_t launch_random_block(int64_t rows, int64_t cols, int64_t row0, uint64_t seed, uint64_t stream_base,
+                                uint64_t stream_stride, double2* X, int64_t ldx, cudaStream_t st);
+// x[i] *= s (device scalar s = 1/beta computed on the host)
+cudaError_t launch_scale(int64_t rows, double2* x, double s, cudaStream_t st);
+// G[i,j] for i<k: make identity minus G, return max |entry| into out[0] via atomicMax on the bit pattern
+cudaError_t launch_orth_err(int64_t k, const double2* G, int64_t ldg, double* out, cudaStream_t st);
+
+}  // namespace chfsi

@@ -1,0 +1,17 @@
+// supporting.cuh -- internal entry points of the supporting ChFSI steps (supporting.cu), used by the
+// public C-ABI wrappers and by the sequence solver (solver.cu).
+#pragma once
+#include "ctx.cuh"
+
+namespace chfsi {
+
+chfsi_status lanczos_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
+                          int32_t steps, uint64_t seed, double* theta_min, double* theta_max, double* upper);
+// Orthonormalise Y (nloc x ka) against XL (nloc x nl, orthonormal, untouched) and itself.
+chfsi_status qr_impl(chfsi_ctx ctx, int64_t n, int64_t nloc, const void* XL, int64_t ldxl, int64_t nl, void* Y,
+                     int64_t ldy, int64_t ka, int32_t* used_fallback);
+// Rayleigh-Ritz on Q (in/out); mu host[ka] ascending; resid host[ka] nullable (R8).
+chfsi_status rr_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh, void* Q,
+                     int64_t ldq, int64_t ka, double normH, double* mu, double* resid);
+
+}  // namespace chfsi

@@ -1,0 +1,217 @@
+"""GPU parity of the supporting ChFSI steps (Lanczos, QR, Rayleigh-Ritz) and of the sequence solver
+(Alg 1) through the C-ABI, against the oracle and against exactly known spectra (H^(1) from the
+generator). Tolerances: BASELINE.json (eigenvalues <= 1e-10 relative, residual <= tol w.r.t. ||H||);
+QR / RR to rounding."""
+import numpy as np
+import pytest
+
+import gen as G
+import oracle as O
+from gen.configs import CONFIGS, DEG0, HNORM
+
+pytestmark = pytest.mark.gpu
+
+
+def crand(rng, *shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+@pytest.fixture
+def ctx(gpu_lib):
+    c = gpu_lib.Context(0)
+    yield c
+    c.close()
+
+
+# ---- Lanczos (Alg 1 l3) -------------------------------------------------------------------------------
+def test_lanczos_vs_oracle_and_exact(gpu_lib, ctx):
+    w = G.wy(512, 480, 1404416100)
+    H = w.full()
+    Hd = gpu_lib.to_colmajor(H)
+    for seed in (0, 5):
+        tmin, tmax, beta = ctx.lanczos_bounds(Hd, 25, seed)
+        otmin, otmax, obeta = O.lanczos(H, 25, seed)
+        assert tmax <= 40.0 + 1e-10 and beta >= 40.0
+        assert abs(tmax - otmax) <= 1e-10 * 40 and abs(tmin - otmin) <= 1e-10 * 40
+        assert abs(beta - obeta) <= 1e-8 * 40
+
+
+def test_lanczos_exact_krylov(gpu_lib, ctx):
+    Hd = gpu_lib.to_colmajor(np.diag(np.arange(1.0, 6.0)).astype(complex))
+    tmin, tmax, beta = ctx.lanczos_bounds(Hd, 5, 1)
+    assert tmin == pytest.approx(1.0, abs=1e-12) and tmax == pytest.approx(5.0, abs=1e-12)
+
+
+# ---- QR (Alg 1 l6) -----------------------------------------------------------------------------------
+@pytest.mark.parametrize("n,k,nl", [(300, 40, 0), (300, 40, 11), (1000, 130, 37)])
+def test_qr_vs_oracle(gpu_lib, ctx, n, k, nl):
+    rng = np.random.default_rng(n + k + nl)
+    Y = crand(rng, n, k)
+    if nl:
+        Y[:, :nl] = np.linalg.qr(Y[:, :nl])[0]
+    Yd = gpu_lib.to_colmajor(Y)
+    fb = ctx.qr(Yd, nlocked=nl)
+    Q = Yd.cpu().numpy()
+    assert fb == 0
+    assert np.array_equal(Q[:, :nl], Y[:, :nl])  # R15: locked columns untouched
+    assert np.abs(Q.conj().T @ Q - np.eye(k)).max() <= 1e-13
+    # reference: CGS2 against the locked block, then Householder QR (positive diagonal R: unique)
+    A = Y[:, nl:].copy()
+    X = Y[:, :nl]
+    for _ in range(2):
+        A = A - X @ O.zgemm("C", "N", X, A) if nl else A
+    Qo, _, _ = O.householder_qr(A)
+    assert np.abs(Q[:, nl:] - Qo).max() <= 1e-11
+
+
+def test_qr_ill_conditioned_block(gpu_lib, ctx):
+    rng = np.random.default_rng(9)
+    n, k = 200, 12
+    Y = crand(rng, n, k)
+    Y[:, 5] = Y[:, 4] + 1e-11 * crand(rng, n)  # kappa ~ 1e11
+    Yd = gpu_lib.to_colmajor(Y)
+    ctx.qr(Yd)
+    Q = Yd.cpu().numpy()
+    assert np.abs(Q.conj().T @ Q - np.eye(k)).max() <= 1e-13
+    P = Q @ Q.conj().T  # span of the well-conditioned leading columns preserved
+    assert np.linalg.norm(P @ Y[:, :4] - Y[:, :4]) <= 1e-12 * np.linalg.norm(Y[:, :4])
+
+
+def test_qr_householder_fallback(gpu_lib, ctx):
+    # a zero column makes the Cholesky factorisation of Y^H Y fail -> Householder fallback
+    rng = np.random.default_rng(10)
+    n, k = 150, 9
+    Y = crand(rng, n, k)
+    Y[:, 3] = 0
+    Yd = gpu_lib.to_colmajor(Y)
+    fb = ctx.qr(Yd)
+    Q = Yd.cpu().numpy()
+    assert fb == 1
+    assert np.abs(Q.conj().T @ Q - np.eye(k)).max() <= 1e-13
+    P = Q @ Q.conj().T
+    keep = [0, 1, 2, 4, 5, 6, 7, 8]
+    assert np.linalg.norm(P @ Y[:, keep] - Y[:, keep]) <= 1e-12 * np.linalg.norm(Y[:, keep])
+    Qo, _, _ = O.householder_qr(Y[:, :3])  # columns before the zero one: the unique QR
+    assert np.abs(Q[:, :3] - Qo).max() <= 1e-12
+
+
+# ---- Rayleigh-Ritz (Alg 1 l7-9) ------------------------------------------------------------------------
+def test_rr_exact_subspace(gpu_lib, ctx):
+    n = 400
+    w = G.wy(n, 360, 17)
+    H = w.full()
+    idx = [0, 1, 2, 10, 399]
+    X = w.eigvecs(idx)
+    rng = np.random.default_rng(3)
+    Q, _ = np.linalg.qr(X @ crand(rng, 5, 5))
+    Qd = gpu_lib.to_colmajor(Q)
+    ritz, res = ctx.rayleigh_ritz(gpu_lib.to_colmajor(H), Qd, normH=HNORM)
+    np.testing.assert_allclose(ritz, w.lam[idx], rtol=0, atol=1e-12 * HNORM)
+    assert res.max() <= 1e-13
+
+
+def test_rr_vs_oracle(gpu_lib, ctx):
+    n, k = 350, 30
+    Gm = G.gue(n, 8, G.stream(5, n))
+    rng = np.random.default_rng(5)
+    Q, _ = np.linalg.qr(crand(rng, n, k))
+    Qd = gpu_lib.to_colmajor(Q)
+    ritz, res = ctx.rayleigh_ritz(gpu_lib.to_colmajor(Gm), Qd, normH=2.0)
+    ro, Yo = O.rayleigh_ritz(Gm, Q)
+    np.testing.assert_allclose(ritz, ro, rtol=0, atol=1e-13)
+    Yg = Qd.cpu().numpy()
+    # Ritz vectors agree up to phase (simple Ritz values)
+    ov = np.abs(np.sum(Yg.conj() * Yo, axis=0))
+    assert np.abs(ov - 1).max() <= 1e-10
+    ro_res = O.residuals(Gm, Yo, ro, 2.0)
+    np.testing.assert_allclose(res, ro_res, rtol=1e-8, atol=1e-15)
+
+
+# ---- the sequence solver (Alg 1; Def 1) ---------------------------------------------------------------
+def test_solve_c0_exact_and_vs_oracle(gpu_lib, ctx):
+    cf = CONFIGS["c0"]
+    n, nev, nex = cf["n"], cf["nev"], cf["nex"]
+    w = G.wy(n, cf["nd"], cf["seed"])
+    H = w.full()
+    X0 = G.start_basis(n, nev + nex, cf["seed"])
+    Hd = gpu_lib.to_colmajor(H)
+    Xd = gpu_lib.to_colmajor(X0)
+    out = ctx.solve_sequence(lambda ell: Hd, 1, Xd, nev, nex, cf["tol"], deg_cap=cf["cap"], seed=cf["seed"])
+    assert out["status"] == 0
+    lam = out["lam"][0]
+    assert np.max(np.abs(lam - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
+    X = Xd.cpu().numpy()[:, :nev]
+    res = np.linalg.norm(H @ X - X * lam, axis=0) / HNORM
+    assert res.max() <= cf["tol"]
+    assert np.abs(X.conj().T @ X - np.eye(nev)).max() <= 1e-12
+    ro = O.chfsi_solve(H, X0, nev, nex, cf["tol"], cf["cap"], seed=cf["seed"])
+    assert np.max(np.abs(lam - ro["lam"]) / np.abs(ro["lam"])) <= 1e-10
+    rep = out["reports"][0]
+    assert rep["converged"] == nev and rep["matvecs_filter"] > 0
+    assert rep["filter_flops"] == pytest.approx(8.0 * n * n * rep["matvecs_filter"])
+
+
+def test_solve_random_start_block_formula(gpu_lib, ctx):
+    # R22: random_start draws column j from stream (3 << 16) | j; the oracle builds the same block from
+    # its own implementation of the formula, so both solves start from identical bits
+    n, nev, nex = 256, 12, 4
+    k = nev + nex
+    w = G.wy(n, 230, 3)
+    H = w.full()
+    Hd = gpu_lib.to_colmajor(H)
+    Xd = gpu_lib.to_colmajor(np.zeros((n, k)))
+    out = ctx.solve_sequence(lambda ell: Hd, 1, Xd, nev, nex, 1e-10, deg_cap=20, seed=42, random_start=True)
+    assert out["status"] == 0
+    np.testing.assert_allclose(out["lam"][0], w.lam[:nev], rtol=1e-10)
+    X0 = np.stack([O.random_vector(n, 42, (3 << 16) | j) for j in range(k)], axis=1)
+    ro = O.chfsi_solve(H, X0, nev, nex, 1e-10, 20, seed=42)
+    np.testing.assert_allclose(out["lam"][0], ro["lam"], rtol=1e-10)
+    # same start bits and the same readings -> the same number of ChFSI loops (trajectory, unpinned
+    # in general, agrees on this well-separated case)
+    assert out["reports"][0]["loops"] == ro["report"]["loops"]
+
+
+def test_solve_exact_input_one_loop(gpu_lib, ctx):
+    n, nev, nex = 256, 12, 4
+    w = G.wy(n, 230, 3)
+    H = w.full()
+    k = nev + nex
+    Hd = gpu_lib.to_colmajor(H)
+    # problem 0 converges from the exact eigenvectors; problem 1 (same H) must take one loop
+    Xd = gpu_lib.to_colmajor(w.eigvecs(range(k)))
+    out = ctx.solve_sequence(lambda ell: Hd, 2, Xd, nev, nex, 1e-10, deg_cap=20, seed=1)
+    assert out["status"] == 0
+    assert out["reports"][1]["loops"] == 1
+    assert out["reports"][1]["matvecs_filter"] <= k * DEG0
+    np.testing.assert_allclose(out["lam"][1], w.lam[:nev], rtol=1e-12)
+
+
+@pytest.mark.slow
+def test_solve_c1_sequence(gpu_lib, ctx):
+    """c1: n = 4096, 5 correlated problems, nev = 200, nex = 40. Problem 1 against the exact spectrum,
+    every problem against numpy.eigvalsh (library routine) and by its residuals (R8, J)."""
+    cf = CONFIGS["c1"]
+    n, nev, nex = cf["n"], cf["nev"], cf["nex"]
+    w = G.wy(n, cf["nd"], cf["seed"])
+    H = w.full()
+    X0 = G.start_basis(n, nev + nex, cf["seed"])
+    Hs = []
+    for ell in range(cf["nprob"]):
+        if ell > 0:
+            G.perturb(H, cf["seed"], ell, cf["delta"] * HNORM)
+        Hs.append(gpu_lib.to_colmajor(H))
+    Xd = gpu_lib.to_colmajor(X0)
+    out = ctx.solve_sequence(lambda ell: Hs[ell], cf["nprob"], Xd, nev, nex, cf["tol"], deg_cap=cf["cap"],
+                             seed=cf["seed"])
+    assert out["status"] == 0
+    assert np.max(np.abs(out["lam"][0] - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
+    Hl = Hs[-1].cpu().numpy()
+    ev = np.linalg.eigvalsh(Hl)[:nev]
+    lam = out["lam"][-1]
+    assert np.max(np.abs(lam - ev) / np.abs(ev)) <= 1e-10
+    X = Xd.cpu().numpy()[:, :nev]
+    nrm = np.abs(np.linalg.eigvalsh(Hl)).max()
+    res = np.linalg.norm(Hl @ X - X * lam, axis=0) / nrm
+    assert res.max() <= cf["tol"] * 1.01
+    loops = [r["loops"] for r in out["reports"]]
+    assert all(l <= loops[0] for l in loops[1:])  # reuse of the previous eigenvectors pays
