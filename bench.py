@@ -1,0 +1,354 @@
+"""bench.py -- ChFSI on a synthetic correlated sequence shaped like the paper's DFT workloads.
+
+Metric (BASELINE.json): "Chebyshev-filter FP64 TFLOP/s & frac of peak; time per eigenproblem at
+1/2/4/8 GPU". A step is one eigenproblem of the c2 sequence solved by the whole hot path (Lanczos,
+filter loops, CholQR2, Rayleigh-Ritz, locking, degree optimisation): n = 13000 complex128,
+nev = 520, nex = 104, degree cap 36, tol 1e-10, H^(l+1) = H^(l) + 5e-4 * 40 * G_l.
+
+  value   = algorithmic filter flops (8 n^2 sum(deg), all filter calls of the K timed problems)
+            / device time of the K timed problems (inputs resident in HBM), TFLOP/s
+  e2e     = the same, each problem's H^(l) copied host(pinned) -> device inside the timed region and
+            the eigenvalues / residuals read back per problem
+  filter_kernel_tflops / frac_of_peak: the filter alone (its CUDA-event time inside the steps)
+  roofline: K1 (the filter kernel), FP64 tensor (DMMA) bound, peak = 37.07 TF measured on this pool
+            (profiles/r01_fp64_peaks.txt; MEASURED_PEAKS.json has no FP64 entry)
+
+`python bench.py --gpus N --steps K --warmup W`; N > 1 under torchrun (row-panel sharding, NCCL).
+`--impl reference` times the CPU oracle (oracle/, plain C) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Chebyshev-filter FP64 TFLOP/s & frac of peak; time per eigenproblem at 1/2/4/8 GPU"
+FP64_PEAK_TFLOPS = 37.07  # DMMA.8x8x4 register-only probe at 1965 MHz (tools/fp64_probe.cu)
+HBM_PEAK_GBS = None
+
+
+def load_peaks():
+    global HBM_PEAK_GBS
+    try:
+        HBM_PEAK_GBS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        HBM_PEAK_GBS = 6650.0  # B200_PROFILING.md fallback
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        time.sleep(0.1)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 8 and r[2].replace(".", "").isdigit()]
+        pw = [float(r[3]) for r in self.rows if len(r) >= 8 and r[3].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 8 for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": reasons}
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------------------------------------
+# sharding helpers (also exercised by tests/test_dist_cpu.py with gloo on CPU)
+def rank_rows(n: int, world: int, rank: int):
+    """1-D row panels: rank owns global rows [row0, row0 + nloc) (n divisible by world)."""
+    if n % world:
+        raise ValueError(f"n = {n} is not divisible by {world} ranks")
+    nloc = n // world
+    return rank * nloc, nloc
+
+
+def build_panels(cf, row0: int, nloc: int, nprob: int, alloc):
+    """This rank's column slab H^(l)[:, row0:row0+nloc] of problems l = 0..nprob-1 of the sequence
+    (H^(1) = Q Lambda Q^H, then H^(l+1) = H^(l) + delta*40*G_l), each written into alloc() -> an
+    (nloc x n) C-contiguous array / pinned tensor (i.e. a column-major n x nloc slab)."""
+    import gen as G
+    from gen.configs import HNORM
+
+    n = cf["n"]
+    wy = G.wy(n, cf["nd"], cf["seed"])
+    out = []
+    for ell in range(nprob):
+        buf = alloc()
+        hv = (buf.numpy() if hasattr(buf, "numpy") else buf).T  # F-ordered (n x nloc) view
+        if ell == 0:
+            wy.panel(row0, nloc, out=hv)
+        else:
+            prev = out[-1]
+            hv[...] = (prev.numpy() if hasattr(prev, "numpy") else prev).T
+            G.perturb(hv, cf["seed"], ell, cf["delta"] * HNORM, c0=row0)
+        out.append(buf)
+    return out
+
+
+def max_over_ranks(x: float, dist, device):
+    """The bench's timing reduction: max of a per-rank scalar over all ranks."""
+    if dist is None:
+        return x
+    import torch
+
+    t = torch.tensor([x], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def oracle_filter_sample(cf, ncols: int, deg: int):
+    """The oracle (plain C, OpenMP) filtering `ncols` columns of the c2 start block with H^(1) at a
+    uniform degree: a bounded sample of the filter work of the same workload. Returns (TFLOP/s,
+    seconds, threads)."""
+    import numpy as np
+
+    import gen as G
+    import oracle as O
+
+    n = cf["n"]
+    w = G.wy(n, cf["nd"], cf["seed"])
+    H = w.full()
+    Y0 = G.start_basis(n, ncols, cf["seed"])
+    lam = w.lam
+    l1, a, b = lam[0] - 0.05, lam[cf["nev"] + cf["nex"] - 1], 48.0
+    c, e = (a + b) / 2, (b - a) / 2
+    t0 = time.perf_counter()
+    Y, mv = O.chebyshev_filter(H, Y0, [deg] * ncols, l1, c, e)
+    dt = time.perf_counter() - t0
+    assert np.isfinite(Y).all()
+    return 8.0 * n * n * mv / dt / 1e12, dt, int(os.environ.get("OMP_NUM_THREADS", host_cores()))
+
+
+def run_reference(args, cf, rank, world):
+    if rank != 0:
+        return
+    K, W = args.steps, args.warmup
+    ncols, deg = 8, 8
+    vals = []
+    for i in range(W + K):
+        v, dt, thr = oracle_filter_sample(cf, ncols, deg)
+        if i >= W:
+            vals.append((v, dt))
+    value = sum(v for v, _ in vals) / len(vals)
+    ms = 1e3 * sum(dt for _, dt in vals) / len(vals)
+    sample = (f"oracle.chebyshev_filter (naive C, OpenMP) on {ncols} columns of the c2 start block, "
+              f"H^(1) n={cf['n']}, uniform degree {deg} ({8.0 * cf['n'] ** 2 * ncols * deg:.3g} flop per step)")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+           "steps": K, "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "c2 (filter-only sample)", "n": cf["n"], "nev": cf["nev"], "nex": cf["nex"]},
+           "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": thr, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="chfsi", choices=["chfsi", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    load_peaks()
+    from gen.configs import CONFIGS, DEG0, HNORM, LANCZOS_STEPS, MAX_LOOPS
+
+    cf = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cf, rank, world)
+        return
+
+    import numpy as np
+    import torch
+
+    import gen as G
+    import paper_1404_4161_b200 as chfsi
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        t = torch.zeros(1, device="cuda")
+        dist.all_reduce(t)  # materialise the NCCL communicator
+        pg = dist.distributed_c10d._get_default_group()
+        comm = pg._get_backend(torch.device("cuda"))._comm_ptr()
+    n, nev, nex = cf["n"], cf["nev"], cf["nex"]
+    k = nev + nex
+    row0, nloc = rank_rows(n, world, rank)
+    K, W = args.steps, args.warmup
+    nprob = W + K
+
+    # ---- inputs: this rank's column slab of every H^(l) (pinned host + HBM), start basis rows ----
+    t_gen = time.perf_counter()
+    host_H = build_panels(cf, row0, nloc, nprob,
+                          lambda: torch.empty((nloc, n), dtype=torch.complex128, pin_memory=True))
+    dev_H = []
+    for hp in host_H:
+        d = torch.empty((nloc, n), dtype=torch.complex128, device="cuda")
+        d.copy_(hp)
+        dev_H.append(d.t())
+    X0 = G.start_basis(n, k, cf["seed"], row0, nloc)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+
+    ctx = chfsi.Context(local_rank, nccl_comm=comm, rank=rank, nranks=world)
+    ctx.reserve(n, nloc, k)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def run_pass(e2e: bool):
+        Xd = chfsi.to_colmajor(X0)
+        stage = chfsi.colmajor(n, nloc) if e2e else None
+        ev = {}
+        sampler = ClockSampler(local_rank)
+        launches = {}
+
+        def get_h(ell):
+            if ell == W:
+                barrier()
+                launches["start"] = ctx.kernel_launches
+                sampler.start()
+                ev["start"] = torch.cuda.Event(enable_timing=True)
+                ev["start"].record(stream)
+            if e2e and ell >= W:
+                stage.t().copy_(host_H[ell], non_blocking=True)  # H2D inside the timed region
+                return stage
+            return dev_H[ell]
+
+        out = ctx.solve_sequence(get_h, nprob, Xd, nev, nex, cf["tol"], deg_cap=cf["cap"], deg0=DEG0,
+                                 max_loops=MAX_LOOPS, lanczos_steps=LANCZOS_STEPS, seed=cf["seed"])
+        if e2e:
+            xh = Xd.cpu()  # the final block read back (part of the last step)
+        ev["end"] = torch.cuda.Event(enable_timing=True)
+        ev["end"].record(stream)
+        barrier()
+        clocks = sampler.stop()
+        ms = max_over_ranks(ev["start"].elapsed_time(ev["end"]), dist, "cuda")
+        launches["n"] = ctx.kernel_launches - launches["start"]
+        return out, ms, clocks, launches["n"]
+
+    out, ms, clocks, nlaunch = run_pass(False)
+    reps = out["reports"][W:]
+    flops = sum(r["filter_flops"] for r in reps)
+    t_filter = max_over_ranks(sum(r["t_filter"] for r in reps), dist, "cuda")
+    value = flops / (ms * 1e-3) / 1e12
+    filt_tf = flops / t_filter / 1e12
+    e2e = None
+    if not args.no_e2e:
+        out2, ms2, _, _ = run_pass(True)
+        flops2 = sum(r["filter_flops"] for r in out2["reports"][W:])
+        e2e = {"value": flops2 / (ms2 * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms2 / K,
+               "h2d_bytes_per_step": 16 * n * nloc, "d2h_bytes_per_step": 16 * nev + (16 * nloc * k) // K,
+               "note": "each problem's H panel copied from pinned host memory inside the timed region; "
+                       "eigenvalues/residuals read back per problem, the final block once"}
+
+    # roofline of K1: FP64 DMMA-bound contraction; achieved from the filter calls' CUDA-event time
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": filt_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": filt_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "kernel": "K1 filter_step_kernel (DMMA.8x8x4, TMA)",
+                "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peaks.txt"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, thr = oracle_filter_sample(cf, 16, 16)
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
+               "sample": f"oracle.chebyshev_filter (naive C, OpenMP) on 16 columns of the c2 start block with "
+                         f"H^(1), degree 16: {8.0 * n * n * 256:.3g} flop in {dt:.1f} s"}
+
+    # correctness guard on the timed problems: all converged, residuals within tol (R8)
+    conv = all(r["converged"] == nev for r in reps)
+    res_max = float(np.max(out["resid"][W:]))
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: ChFSI sequence, one eigenproblem per step", "n": n,
+                       "nev": nev, "nex": nex, "deg_cap": cf["cap"], "tol": cf["tol"], "delta": cf["delta"],
+                       "problems": f"{W} warm-up + {K} timed of the correlated sequence",
+                       "parallelism": f"1-D row panels over {world} GPU(s)" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (H panel per problem >> 126 MB)"},
+            "time_per_eigenproblem_s": ms / K / 1e3,
+            "filter_kernel_tflops": filt_tf, "frac_of_peak": filt_tf / FP64_PEAK_TFLOPS,
+            "filter_share_of_step": t_filter / (ms * 1e-3),
+            "loops_per_problem": [r["loops"] for r in reps],
+            "matvecs_filter_per_problem": [r["matvecs_filter"] for r in reps],
+            "converged": conv, "max_resid_over_tol": res_max / cf["tol"],
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": nlaunch,
+            "input_generation_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -44,10 +44,20 @@ typedef enum {
 
 #define CHFSI_MAX_DEGREE 64
 
-/* Create a context on `device` using `cuda_stream` (a cudaStream_t, or NULL for a library-owned
- * stream). nccl_comm: an ncclComm_t spanning the `nranks` ranks (NULL when nranks == 1). */
+/* Create a context on `device` using `cuda_stream` (a cudaStream_t; NULL = the legacy default
+ * stream 0, ordered with the caller's default-stream work). nccl_comm: an ncclComm_t spanning the `nranks` ranks (NULL when nranks == 1). */
 chfsi_status chfsi_ctx_create(chfsi_ctx* out, int32_t device, void* cuda_stream, void* nccl_comm,
                               int32_t rank, int32_t nranks);
+/* Emulated ranks: `nranks` contexts in one process, on one device, share a local group whose
+ * collectives are device copies ordered by CUDA events and a host barrier (same semantics as the
+ * NCCL calls). Drive each rank from its own host thread, each context on its own stream. This runs
+ * the nranks > 1 data path (row panels, packed B operands, rank-chunked contraction) on one GPU. */
+typedef struct chfsi_local_group_s* chfsi_local_group;
+chfsi_status chfsi_local_group_create(chfsi_local_group* out, int32_t nranks);
+void chfsi_local_group_destroy(chfsi_local_group group);
+chfsi_status chfsi_ctx_create_local(chfsi_ctx* out, int32_t device, void* cuda_stream,
+                                    chfsi_local_group group, int32_t rank);
+
 /* Optional: preallocate workspace for problems up to n rows globally, nloc rows per rank and kmax
  * block columns, so no allocation happens inside a timed loop. */
 chfsi_status chfsi_ctx_reserve(chfsi_ctx ctx, int64_t n, int64_t nloc, int64_t kmax);

@@ -24,9 +24,9 @@ MAX_DEGREE = 64
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_NOCONV", 4: "ERR_QR", 5: "ERR_CUDA", 6: "ERR_NCCL",
           7: "ERR_NOMEM"}
 
-EXPORTS = ("chfsi_ctx_create", "chfsi_ctx_reserve", "chfsi_ctx_destroy", "chfsi_last_error",
-           "chfsi_kernel_launches", "chfsi_filter", "chfsi_lanczos_bounds", "chfsi_qr", "chfsi_rayleigh_ritz",
-           "chfsi_solve_sequence")
+EXPORTS = ("chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_ctx_reserve", "chfsi_ctx_destroy",
+           "chfsi_last_error", "chfsi_kernel_launches", "chfsi_local_group_create", "chfsi_local_group_destroy",
+           "chfsi_filter", "chfsi_lanczos_bounds", "chfsi_qr", "chfsi_rayleigh_ritz", "chfsi_solve_sequence")
 
 
 class ChfsiError(RuntimeError):
@@ -69,6 +69,10 @@ def lib():
         i64, u64, i32, dbl, vp = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
         pd, pi64, pi32 = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)
         L.chfsi_ctx_create.argtypes = [ctypes.POINTER(vp), i32, vp, vp, i32, i32]
+        L.chfsi_ctx_create_local.argtypes = [ctypes.POINTER(vp), i32, vp, vp, i32]
+        L.chfsi_local_group_create.argtypes = [ctypes.POINTER(vp), i32]
+        L.chfsi_local_group_destroy.argtypes = [vp]
+        L.chfsi_local_group_destroy.restype = None
         L.chfsi_ctx_reserve.argtypes = [vp, i64, i64, i64]
         L.chfsi_ctx_destroy.argtypes = [vp]
         L.chfsi_ctx_destroy.restype = None
@@ -82,7 +86,7 @@ def lib():
         L.chfsi_rayleigh_ritz.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, i64, dbl, pd, pd]
         L.chfsi_solve_sequence.argtypes = [vp, i64, i64, i64, i32, GET_H, vp, ctypes.POINTER(Opts), vp, i64, pd, pd,
                                            ctypes.POINTER(Report)]
-        for name in ("chfsi_ctx_create", "chfsi_ctx_reserve", "chfsi_filter", "chfsi_lanczos_bounds", "chfsi_qr",
+        for name in ("chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_local_group_create", "chfsi_ctx_reserve", "chfsi_filter", "chfsi_lanczos_bounds", "chfsi_qr",
                      "chfsi_rayleigh_ritz", "chfsi_solve_sequence"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
@@ -121,21 +125,45 @@ def _mat(t, rows=None, cols=None, name="matrix"):
     return ctypes.c_void_p(t.data_ptr()), ld
 
 
+class LocalGroup:
+    """P emulated ranks on one device (chfsi_local_group): drive each rank's Context from its own
+    thread, each on its own stream. Runs the nranks > 1 data path on a single GPU."""
+
+    def __init__(self, nranks: int):
+        h = ctypes.c_void_p()
+        st = lib().chfsi_local_group_create(ctypes.byref(h), nranks)
+        if st != 0:
+            raise ChfsiError(st, "chfsi_local_group_create failed")
+        self.h, self.nranks = h, nranks
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().chfsi_local_group_destroy(self.h)
+            self.h = None
+
+
 class Context:
     """A library context on one device (one per rank). Work runs on `stream` (default: torch's current
-    stream). For nranks > 1 pass `nccl_comm` (an ncclComm_t as int, e.g. from torch's ProcessGroupNCCL)."""
+    stream). For nranks > 1 pass `nccl_comm` (an ncclComm_t as int, e.g. from torch's ProcessGroupNCCL)
+    or a LocalGroup (emulated ranks on one device)."""
 
-    def __init__(self, device: int = 0, stream=None, nccl_comm: int | None = None, rank: int = 0, nranks: int = 1):
+    def __init__(self, device: int = 0, stream=None, nccl_comm: int | None = None, rank: int = 0, nranks: int = 1,
+                 local_group: LocalGroup | None = None):
         import torch
 
         L = lib()
         self.device = device
-        self.rank, self.nranks = rank, nranks
+        self.rank = rank
+        self.nranks = local_group.nranks if local_group else nranks
         torch.cuda.set_device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
         h = ctypes.c_void_p()
-        st = L.chfsi_ctx_create(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream),
-                                ctypes.c_void_p(nccl_comm or 0), rank, nranks)
+        if local_group is not None:
+            st = L.chfsi_ctx_create_local(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream),
+                                          local_group.h, rank)
+        else:
+            st = L.chfsi_ctx_create(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream),
+                                    ctypes.c_void_p(nccl_comm or 0), rank, nranks)
         if st != 0:
             raise ChfsiError(st, "chfsi_ctx_create failed (no B200 / CUDA device?)")
         self.h = h

@@ -274,11 +274,11 @@ using namespace chfsi;
 // ------------------------------------------------------------------------------------------------
 extern "C" {
 
-chfsi_status chfsi_ctx_create(chfsi_ctx* out, int32_t device, void* cuda_stream, void* nccl_comm, int32_t rank,
-                              int32_t nranks) {
+static chfsi_status ctx_create_impl(chfsi_ctx* out, int32_t device, void* cuda_stream, void* nccl_comm,
+                                    chfsi_local_group group, int32_t rank, int32_t nranks) {
   if (!out) return CHFSI_ERR_ARG;
   *out = nullptr;
-  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_comm)) return CHFSI_ERR_ARG;
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_comm && !group)) return CHFSI_ERR_ARG;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || device < 0 || device >= ndev) {
     cudaGetLastError();
@@ -294,15 +294,11 @@ chfsi_status chfsi_ctx_create(chfsi_ctx* out, int32_t device, void* cuda_stream,
   ctx->nranks = nranks;
   ctx->num_sms = prop.multiProcessorCount;
   ctx->nccl_comm = nccl_comm;
-  if (cuda_stream) {
-    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
-  } else {
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
-      delete ctx;
-      return CHFSI_ERR_CUDA;
-    }
-    ctx->own_stream = true;
-  }
+  ctx->local_group = group;
+  // NULL selects the legacy default stream (stream 0), so work is ordered with the caller's default-
+  // stream copies; pass an explicit stream for concurrency.
+  ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+  ctx->own_stream = false;
   if (cublasCreate(&ctx->cublas) != CUBLAS_STATUS_SUCCESS ||
       cublasSetStream(ctx->cublas, ctx->stream) != CUBLAS_STATUS_SUCCESS ||
       cusolverDnCreate(&ctx->cusolver) != CUSOLVER_STATUS_SUCCESS ||
@@ -317,6 +313,17 @@ chfsi_status chfsi_ctx_create(chfsi_ctx* out, int32_t device, void* cuda_stream,
   }
   *out = ctx;
   return CHFSI_OK;
+}
+
+chfsi_status chfsi_ctx_create(chfsi_ctx* out, int32_t device, void* cuda_stream, void* nccl_comm, int32_t rank,
+                              int32_t nranks) {
+  return ctx_create_impl(out, device, cuda_stream, nccl_comm, nullptr, rank, nranks);
+}
+
+chfsi_status chfsi_ctx_create_local(chfsi_ctx* out, int32_t device, void* cuda_stream, chfsi_local_group group,
+                                    int32_t rank) {
+  if (!group) return CHFSI_ERR_ARG;
+  return ctx_create_impl(out, device, cuda_stream, nullptr, group, rank, group->P);
 }
 
 chfsi_status chfsi_ctx_reserve(chfsi_ctx ctx, int64_t n, int64_t nloc, int64_t kmax) {

@@ -1,9 +1,16 @@
-// comm.cu -- communication layer over NCCL (NVLink 5 / NVSwitch on one B200 box). NCCL is loaded
-// with dlopen on first use, so single-GPU use of libchfsi.so has no NCCL dependency. The
-// communicator is the caller's (e.g. torch's ProcessGroupNCCL comm, or one built from an
-// ncclUniqueId broadcast over the torch process group); the library never creates or destroys it.
+// comm.cu -- communication layer.
+//  * NCCL (NVLink 5 / NVSwitch on one B200 box), loaded with dlopen on first use so single-GPU use of
+//    libchfsi.so has no NCCL dependency. The communicator is the caller's (e.g. torch's
+//    ProcessGroupNCCL comm); the library never creates or destroys it.
+//  * A local group: P ranks emulated on one device, one host thread per rank, each with its own
+//    stream. Collectives are device copies / a fixed-order reduction ordered by CUDA events and a
+//    host barrier -- the same semantics as the NCCL calls (in-place allgather, allreduce, broadcast),
+//    so the P > 1 data path (row panels, packed B operands, rank-chunked K loop) runs on a 1-GPU box.
+//    No kernel ever waits on another kernel; ordering is host barrier + cudaStreamWaitEvent.
 #include <dlfcn.h>
 #include <nccl.h>
+
+#include <vector>
 
 #include "ctx.cuh"
 
@@ -12,6 +19,9 @@ namespace chfsi {
 struct Comm {
   void* lib = nullptr;
   ncclComm_t comm = nullptr;
+  chfsi_local_group local = nullptr;
+  double* scratch = nullptr;  // local-group allreduce accumulator
+  size_t scratch_n = 0;
   decltype(&ncclAllGather) allgather = nullptr;
   decltype(&ncclAllReduce) allreduce = nullptr;
   decltype(&ncclBroadcast) bcast = nullptr;
@@ -21,6 +31,11 @@ struct Comm {
 chfsi_status comm_init(chfsi_ctx ctx) {
   if (ctx->nranks == 1) return CHFSI_OK;
   Comm* c = new Comm();
+  if (ctx->local_group) {
+    c->local = ctx->local_group;
+    ctx->comm = c;
+    return CHFSI_OK;
+  }
   const char* names[] = {"libnccl.so.2", "libnccl.so"};
   for (const char* nm : names) {
     c->lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
@@ -47,7 +62,8 @@ chfsi_status comm_init(chfsi_ctx ctx) {
 }
 
 void comm_destroy(chfsi_ctx ctx) {
-  delete ctx->comm;  // the library handle stays loaded; the communicator belongs to the caller
+  if (ctx->comm && ctx->comm->scratch) cudaFree(ctx->comm->scratch);
+  delete ctx->comm;  // the NCCL library handle stays loaded; the communicator belongs to the caller
   ctx->comm = nullptr;
 }
 
@@ -57,8 +73,53 @@ static chfsi_status nccl_check(chfsi_ctx ctx, ncclResult_t r, const char* what) 
   return CHFSI_ERR_NCCL;
 }
 
+// ---- local group primitives ----
+namespace {
+
+__global__ void sum_ranks_kernel(const double* const* src, int P, size_t count, double* dst) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    double s = 0;
+    for (int q = 0; q < P; ++q) s += src[q][i];  // fixed rank order: identical bits on every rank
+    dst[i] = s;
+  }
+}
+
+// publish `buf`, wait until every rank has published and its producer work is ordered before ours
+void lg_enter(chfsi_ctx ctx, const void* buf) {
+  chfsi_local_group g = ctx->comm->local;
+  g->bufs[ctx->rank] = buf;
+  cudaEventRecord(g->ready[ctx->rank], ctx->stream);
+  g->barrier();
+  for (int q = 0; q < g->P; ++q)
+    if (q != ctx->rank) cudaStreamWaitEvent(ctx->stream, g->ready[q], 0);
+}
+
+// every rank's reads of the published buffers are ordered before anyone's later writes
+void lg_exit(chfsi_ctx ctx) {
+  chfsi_local_group g = ctx->comm->local;
+  cudaEventRecord(g->done[ctx->rank], ctx->stream);
+  g->barrier();
+  for (int q = 0; q < g->P; ++q)
+    if (q != ctx->rank) cudaStreamWaitEvent(ctx->stream, g->done[q], 0);
+  g->barrier();  // nobody re-records its events before all waits above were issued
+}
+
+}  // namespace
+
 chfsi_status comm_allgather_inplace(chfsi_ctx ctx, double* buf, size_t count) {
   if (ctx->nranks == 1 || count == 0) return CHFSI_OK;
+  if (ctx->comm->local) {
+    chfsi_local_group g = ctx->comm->local;
+    lg_enter(ctx, buf);
+    for (int q = 0; q < g->P; ++q) {
+      if (q == ctx->rank) continue;
+      const double* src = static_cast<const double*>(g->bufs[q]) + count * q;
+      CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(buf + count * q, src, count * sizeof(double), cudaMemcpyDeviceToDevice,
+                                          ctx->stream));
+    }
+    lg_exit(ctx);
+    return CHFSI_OK;
+  }
   return nccl_check(ctx,
                     ctx->comm->allgather(buf + count * ctx->rank, buf, count, ncclDouble, ctx->comm->comm, ctx->stream),
                     "ncclAllGather");
@@ -66,14 +127,81 @@ chfsi_status comm_allgather_inplace(chfsi_ctx ctx, double* buf, size_t count) {
 
 chfsi_status comm_allreduce_sum(chfsi_ctx ctx, double* buf, size_t count) {
   if (ctx->nranks == 1 || count == 0) return CHFSI_OK;
+  if (ctx->comm->local) {
+    Comm* c = ctx->comm;
+    chfsi_local_group g = c->local;
+    if (c->scratch_n < count + (size_t)g->P) {
+      if (c->scratch) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(c->scratch);
+      }
+      CHFSI_CUDA_TRY(ctx, cudaMalloc(&c->scratch, sizeof(double) * (count + (size_t)g->P)));
+      c->scratch_n = count + (size_t)g->P;
+    }
+    lg_enter(ctx, buf);
+    const double** ptrs = reinterpret_cast<const double**>(c->scratch + count);
+    std::vector<const double*> hp(g->P);
+    for (int q = 0; q < g->P; ++q) hp[q] = static_cast<const double*>(g->bufs[q]);
+    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(ptrs, hp.data(), sizeof(double*) * g->P, cudaMemcpyHostToDevice, ctx->stream));
+    const unsigned blocks = (unsigned)std::min<size_t>((count + 255) / 256, 1024);
+    sum_ranks_kernel<<<blocks, 256, 0, ctx->stream>>>(ptrs, g->P, count, c->scratch);
+    CHFSI_CUDA_TRY(ctx, cudaGetLastError());
+    ctx->launches++;
+    lg_exit(ctx);
+    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(buf, c->scratch, count * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    // the pointer table is rewritten by the next call only after this stream's work: order it
+    CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return CHFSI_OK;
+  }
   return nccl_check(ctx, ctx->comm->allreduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm->comm, ctx->stream),
                     "ncclAllReduce");
 }
 
 chfsi_status comm_bcast(chfsi_ctx ctx, double* buf, size_t count, int root) {
   if (ctx->nranks == 1 || count == 0) return CHFSI_OK;
+  if (ctx->comm->local) {
+    chfsi_local_group g = ctx->comm->local;
+    lg_enter(ctx, buf);
+    if (ctx->rank != root)
+      CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(buf, g->bufs[root], count * sizeof(double), cudaMemcpyDeviceToDevice,
+                                          ctx->stream));
+    lg_exit(ctx);
+    return CHFSI_OK;
+  }
   return nccl_check(ctx, ctx->comm->bcast(buf, buf, count, ncclDouble, root, ctx->comm->comm, ctx->stream),
                     "ncclBroadcast");
 }
 
 }  // namespace chfsi
+
+extern "C" {
+
+chfsi_status chfsi_local_group_create(chfsi_local_group* out, int32_t nranks) {
+  if (!out || nranks < 1) return CHFSI_ERR_ARG;
+  chfsi_local_group g = new chfsi_local_group_s();
+  g->P = nranks;
+  g->bufs.assign(nranks, nullptr);
+  g->ready.assign(nranks, nullptr);
+  g->done.assign(nranks, nullptr);
+  for (int q = 0; q < nranks; ++q) {
+    if (cudaEventCreateWithFlags(&g->ready[q], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->done[q], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      chfsi_local_group_destroy(g);
+      return CHFSI_ERR_CUDA;
+    }
+  }
+  *out = g;
+  return CHFSI_OK;
+}
+
+void chfsi_local_group_destroy(chfsi_local_group g) {
+  if (!g) return;
+  for (auto e : g->ready)
+    if (e) cudaEventDestroy(e);
+  for (auto e : g->done)
+    if (e) cudaEventDestroy(e);
+  delete g;
+}
+
+}  // extern "C"

@@ -6,11 +6,35 @@
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
+#include <condition_variable>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "chfsi.h"
 #include "common.cuh"
+
+// Emulated ranks on one device (comm.cu): host barrier + per-rank events.
+struct chfsi_local_group_s {
+  int P = 1;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long generation = 0;
+  std::vector<const void*> bufs;
+  std::vector<cudaEvent_t> ready, done;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long gen = generation;
+    if (++arrived == P) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
 
 namespace chfsi {
 
@@ -31,6 +55,7 @@ struct chfsi_ctx_s {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   void* nccl_comm = nullptr;
+  chfsi_local_group local_group = nullptr;
   chfsi::Comm* comm = nullptr;
   cublasHandle_t cublas = nullptr;
   cusolverDnHandle_t cusolver = nullptr;

@@ -1,0 +1,17 @@
+#!/bin/bash
+# One gpurun call: GPU tests, the bench line, the ncu launch list of a short bench, one full ncu
+# capture of K1. Outputs land in gpurun_out/ (scratch); summaries are copied to profiles/ by hand.
+set -u
+TAG=${1:-r01}
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -q -x > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest_gpu.log
+python __graft_entry__.py smoke > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/${TAG}_smoke.log
+python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?" >> gpurun_out/${TAG}_bench.err
+SHORT="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+$SHORT > gpurun_out/${TAG}_short_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $SHORT > gpurun_out/${TAG}_ncu_launches.log 2>&1
+echo "ncu launches rc=$?" >> gpurun_out/${TAG}_ncu_launches.log
+PERF="python tools/filter_perf.py 13000 624 4 auto"
+$PERF > gpurun_out/${TAG}_perf_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:filter_step -s 4 -c 1 -o gpurun_out/${TAG}_k1 -f $PERF > gpurun_out/${TAG}_ncu_full.log 2>&1
+echo "ncu full rc=$?" >> gpurun_out/${TAG}_ncu_full.log
