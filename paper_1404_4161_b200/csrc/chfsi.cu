@@ -92,6 +92,18 @@ chfsi_status make_tmap_3d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64
 
 static inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+chfsi_status sk_workspace(chfsi_ctx ctx, const TileChoice& t, StepParams& p) {
+  const size_t tick_bytes = 4096;  // >= num_sms ints
+  const size_t need = tick_bytes + sizeof(double) * filter_partials_doubles(t, ctx->num_sms);
+  void* old = ctx->sk.ptr;
+  chfsi_status st = ensure(ctx, ctx->sk, need);
+  if (st) return st;
+  if (ctx->sk.ptr != old) CHFSI_CUDA_TRY(ctx, cudaMemsetAsync(ctx->sk.ptr, 0, tick_bytes, ctx->stream));
+  p.tickets = static_cast<int*>(ctx->sk.ptr);
+  p.partials = reinterpret_cast<double*>(static_cast<char*>(ctx->sk.ptr) + tick_bytes);
+  return CHFSI_OK;
+}
+
 // Common driver for one K1 launch over the active columns [col0, k) of the B operand.
 struct Operand {
   CUtensorMap tm;
@@ -155,6 +167,9 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
   sp.c = 0.0;
   sp.out = static_cast<double2*>(out);
   sp.ld_out = ldo;
+  schedule_filter_step(t, ctx->num_sms, sp);
+  st = sk_workspace(ctx, t, sp);
+  if (st) return st;
   CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, sp, ctx->stream));
   ctx->launches++;
   return CHFSI_OK;
@@ -248,6 +263,9 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       sp.ld_r_next = nloc;
     }
     sp.nonfinite = check_finite ? flag : nullptr;
+    schedule_filter_step(t, ctx->num_sms, sp);
+    st = sk_workspace(ctx, t, sp);
+    if (st) return st;
     CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, sp, ctx->stream));
     ctx->launches++;
     if (p > 1 && ka_next > 0) {
@@ -347,7 +365,7 @@ void chfsi_ctx_destroy(chfsi_ctx ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   comm_destroy(ctx);
-  DevBuf* bufs[] = {&ctx->L0, &ctx->L1, &ctx->R0, &ctx->R1, &ctx->flag, &ctx->w1, &ctx->w2, &ctx->w3, &ctx->w4,
+  DevBuf* bufs[] = {&ctx->L0, &ctx->L1, &ctx->R0, &ctx->R1, &ctx->flag, &ctx->sk, &ctx->w1, &ctx->w2, &ctx->w3, &ctx->w4,
                     &ctx->small1, &ctx->small2, &ctx->small3, &ctx->solver_ws, &ctx->devinfo, &ctx->lz,
                     &ctx->ya,    &ctx->xl,     &ctx->tb,     &ctx->idx};
   for (DevBuf* b : bufs)

@@ -66,6 +66,7 @@ struct chfsi_ctx_s {
   chfsi::DevBuf L0, L1;          // filter local state (nloc x k each)
   chfsi::DevBuf R0, R1;          // p > 1: packed full-height B operands
   chfsi::DevBuf flag;            // int nonfinite flag (+ small scalars)
+  chfsi::DevBuf sk;              // K1 stream-K workspace: tickets (zeroed) + partial accumulators
   chfsi::DevBuf w1, w2, w3, w4;  // general nloc x k / k x k scratch for QR / RR / solver
   chfsi::DevBuf small1, small2, small3;
   chfsi::DevBuf solver_ws;       // cuSOLVER workspace
@@ -79,6 +80,10 @@ struct chfsi_ctx_s {
 namespace chfsi {
 
 chfsi_status ensure(chfsi_ctx ctx, DevBuf& b, size_t bytes);
+// K1 stream-K workspace for tile variant `t`: fills p.partials / p.tickets
+struct TileChoice;
+struct StepParams;
+chfsi_status sk_workspace(chfsi_ctx ctx, const TileChoice& t, StepParams& p);
 void set_err(chfsi_ctx ctx, const std::string& msg);
 
 // TMA descriptors (FLOAT64, 128B swizzle, OOB -> zero fill)

@@ -18,21 +18,22 @@ cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ste
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int ncols = p.col_end - p.col0;
-  dim3 grid((ncols + BNC - 1) / BNC, (unsigned)((p.nrows + BM - 1) / BM));
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tmA, tmB, p);
+  kern<<<p.grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tmA, tmB, p);
   return cudaGetLastError();
 }
 
 struct Variant {
   int bm, bnc;
-  double eff;  // relative per-flop efficiency of the variant (measured)
+  double eff;   // relative per-flop efficiency of the variant (measured)
+  int threads;  // CTA size
+  int acc;      // accumulator doubles per thread
 };
 constexpr Variant kVariants[] = {
-    {128, 32, 1.00},  // 0
-    {64, 64, 1.00},   // 1
-    {128, 64, 1.00},  // 2
-    {64, 32, 0.90},   // 3
+    {128, 32, 0.944, 256, 32},  // 0: 8 warps, warp tile 32 x 16
+    {64, 64, 0.938, 256, 32},   // 1: 8 warps, warp tile 32 x 16
+    {128, 64, 0.983, 256, 64},  // 2: 8 warps, warp tile 32 x 32
+    {64, 32, 0.724, 128, 32},   // 3: 4 warps
+    {128, 64, 1.000, 512, 32},  // 4: 16 warps (4 per SMSP), warp tile 32 x 16
 };
 
 }  // namespace
@@ -42,22 +43,40 @@ TileChoice choose_filter_tile(int64_t nrows, int64_t ncols, int num_sms) {
   const char* fs = getenv("CHFSI_FILTER_VARIANT");
   const int forced = fs ? atoi(fs) : -1;
   const int nvar = (int)(sizeof(kVariants) / sizeof(kVariants[0]));
-  if (forced >= 0 && forced < nvar) return TileChoice{forced, kVariants[forced].bm, kVariants[forced].bnc};
-  // minimise (waves x per-tile work / efficiency): wave quantisation dominates narrow steps
+  if (forced >= 0 && forced < nvar)
+    return TileChoice{forced, kVariants[forced].bm, kVariants[forced].bnc, kVariants[forced].threads,
+                      kVariants[forced].acc};
+  // the persistent stream-K schedule removes wave quantisation: minimise padded work / efficiency
+  // (efficiencies: measured full-width rates relative to the best variant)
   int best = 0;
   double best_cost = 1e300;
-  for (int v = 0; v < (int)(sizeof(kVariants) / sizeof(kVariants[0])); ++v) {
-    const int64_t tiles = ((nrows + kVariants[v].bm - 1) / kVariants[v].bm) *
-                          ((ncols + kVariants[v].bnc - 1) / kVariants[v].bnc);
-    const int64_t waves = (tiles + num_sms - 1) / num_sms;
-    const double cost = (double)waves * kVariants[v].bm * kVariants[v].bnc / kVariants[v].eff;
+  for (int v = 0; v < nvar; ++v) {
+    const int64_t tm = (nrows + kVariants[v].bm - 1) / kVariants[v].bm;
+    const int64_t tn = (ncols + kVariants[v].bnc - 1) / kVariants[v].bnc;
+    const double cost = (double)tm * kVariants[v].bm * tn * kVariants[v].bnc / kVariants[v].eff;
     if (cost < best_cost * 0.999) {
       best_cost = cost;
       best = v;
     }
   }
-  return TileChoice{best, kVariants[best].bm, kVariants[best].bnc};
+  (void)num_sms;
+  return TileChoice{best, kVariants[best].bm, kVariants[best].bnc, kVariants[best].threads, kVariants[best].acc};
 }
+
+void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
+  const int64_t ncols = p.col_end - p.col0;
+  const int64_t tm = (p.nrows + t.bm - 1) / t.bm, tn = (ncols + t.bnc - 1) / t.bnc;
+  const int64_t tiles = tm * tn;
+  const int64_t iters = tiles * p.num_kt;
+  const int64_t grid = iters < num_sms ? iters : num_sms;
+  p.tiles_n = (int32_t)tn;
+  p.grid = (int32_t)grid;
+  p.dp_units = (int32_t)(tiles / grid);
+  p.tail_tile0 = (int32_t)(p.dp_units * grid);
+  p.tail_iters = (tiles - p.tail_tile0) * p.num_kt;
+}
+
+size_t filter_partials_doubles(const TileChoice& t, int num_sms) { return (size_t)2 * num_sms * t.acc * t.threads; }
 
 cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, const CUtensorMap& tmB,
                                const StepParams& p, cudaStream_t stream) {
@@ -70,6 +89,8 @@ cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, cons
       return launch_cfg<128, 64, 32, 32, 4>(tmA, tmB, p, stream);
     case 3:
       return launch_cfg<64, 32, 32, 16, 8>(tmA, tmB, p, stream);
+    case 4:
+      return launch_cfg<128, 64, 32, 16, 4>(tmA, tmB, p, stream);
     default:
       return cudaErrorInvalidValue;
   }

@@ -15,7 +15,7 @@ namespace chfsi {
 
 struct StepParams {
   int64_t nrows;        // output rows (nloc)
-  int32_t num_kt;       // k-tiles (32 real = 16 complex contraction entries each)
+  int32_t num_kt;       // k-tiles per output tile (32 real = 16 complex contraction entries each)
   int32_t kt_per_rank;  // k-tiles per rank chunk of the B operand (== num_kt when p == 1)
   int32_t a_rank_stride;  // real-K offset between rank chunks in A (2 * nloc_per_rank)
   int32_t col0;         // first active complex column s_i
@@ -23,6 +23,18 @@ struct StepParams {
   int32_t fin_end;      // columns [col0, fin_end) finish at this step and go to `out`
   int32_t b_col0;       // B-operand column coordinate of complex column col0
   int32_t flags;        // 1: read y_cur (c != 0), 2: read y_prev (b != 0)
+  // persistent schedule (host-computed, see schedule_filter_step): tiles are numbered n-fastest;
+  // CTA c owns the data-parallel tiles c, c + grid, ..., c + (dp_units - 1) grid, then the
+  // stream-K iterations [c*tail_iters/grid, (c+1)*tail_iters/grid) of the tail tiles
+  // tail_tile0.. (each tile = num_kt iterations); a split tile is finished by the last of its
+  // contributors to arrive (ticket), which sums the partial accumulators in k order.
+  int32_t tiles_n;      // N tiles
+  int32_t grid;         // CTAs
+  int32_t dp_units;     // full tiles per CTA
+  int32_t tail_tile0;   // first stream-K tile
+  int64_t tail_iters;   // (tiles - tail_tile0) * num_kt
+  double* partials;     // 2 slots per CTA
+  int* tickets;         // one per tail tile, zero between launches
   double a, b, c;       // Y_{i+1} = a (acc - c y_cur) - b y_prev
   const double2* y_cur;
   int64_t ld_cur;
@@ -62,22 +74,39 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
   return static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
 }
 
+// first iteration of CTA c in the stream-K tail (balanced integer split)
+__device__ __forceinline__ int64_t sk_start(int64_t c, int64_t iters, int64_t grid) { return (c * iters) / grid; }
+// CTA whose tail range contains iteration g
+__device__ __forceinline__ int64_t sk_owner(int64_t g, int64_t iters, int64_t grid) {
+  return ((g + 1) * grid - 1) / iters;
+}
+
+__device__ __forceinline__ double dneg(double x) {  // sign flip on the ALU pipe (no DADD)
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
+}
+
 template <int BM, int BNC, int WM, int WNC, int STAGES>
 __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES>::kThreads, 1)
     filter_step_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const StepParams p) {
   using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES>;
+  constexpr int kAcc = Cfg::kMT * Cfg::kNT * 2;  // accumulator doubles per thread
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align to 1024 B (128B-swizzle atoms) by pointer arithmetic on the shared array, so the compiler
+  // keeps the shared address space and emits LDS (an integer round-trip would give generic LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes);
   uint64_t* empty = full + STAGES;
+  __shared__ int s_ticket;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n_tile = blockIdx.x;  // n fastest: CTAs sharing an H row block run together (L2 reuse)
-  const int m_tile = blockIdx.y;
-  const int m0 = m_tile * BM;
-  const int bcol = p.b_col0 + n_tile * BNC;
+  const int64_t cta = blockIdx.x;
+  const int KT = p.num_kt;
+  const int64_t t_beg = sk_start(cta, p.tail_iters, p.grid);
+  const int64_t t_end = sk_start(cta + 1, p.tail_iters, p.grid);
+  const int64_t dp_iters = (int64_t)p.dp_units * KT;
+  const int64_t my_iters = dp_iters + (t_end - t_beg);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -88,32 +117,83 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES>::kThreads,
   }
   __syncthreads();
 
+  // CTA-local iteration j -> (tile, k-tile)
+  auto coords = [&](int64_t j, int& tile, int& kt) {
+    if (j < dp_iters) {
+      tile = (int)(cta + (j / KT) * p.grid);
+      kt = (int)(j % KT);
+    } else {
+      const int64_t g = t_beg + (j - dp_iters);
+      tile = p.tail_tile0 + (int)(g / KT);
+      kt = (int)(g % KT);
+    }
+  };
   // TMA producer = thread 0 (a dedicated producer warp would round the CTA to 12 warps of register
-  // allocation and cap consumers at 168 registers). Stage s of k-tile kt is refilled with k-tile
-  // kt + STAGES once every consumer warp has released it; thread 0 refills one iteration behind its
-  // own progress, so it blocks only if another warp is more than one k-tile behind.
-  auto produce = [&](int kt) {
-    const int s = kt % STAGES;
-    uint8_t* sa = smem + s * Cfg::kStageBytes;
+  // allocation and cap the consumers at 168 registers). Stage s is refilled once every consumer warp
+  // has released it; thread 0 refills one iteration behind its own progress, so it blocks only if
+  // another warp is more than one k-tile behind. The producer walks the CTA's iterations in order
+  // with an incremental cursor and runs across tile boundaries, so the next tile's first stages
+  // stream in during an epilogue.
+  // producer cursor in shared memory: only thread 0 touches it, and keeping it out of the register
+  // file leaves the consumers their full budget
+  __shared__ struct {
+    int64_t j;
+    int tile, kt, dp_left, stage;
+  } pc;
+  int64_t& pc_j = pc.j;
+  int& pc_tile = pc.tile;
+  int& pc_kt = pc.kt;
+  int& pc_dp_left = pc.dp_left;
+  int& pc_stage = pc.stage;
+  auto pc_init = [&]() {
+    if (pc_dp_left > 0) {
+      pc_tile = (int)cta;
+      pc_kt = 0;
+    } else {
+      pc_tile = p.tail_tile0 + (int)(t_beg / KT);
+      pc_kt = (int)(t_beg % KT);
+    }
+  };
+  auto produce = [&]() {  // load iteration pc_j into stage pc_stage, then advance the cursor
+    const int m0 = (pc_tile / p.tiles_n) * BM;
+    const int bcol = p.b_col0 + (pc_tile % p.tiles_n) * BNC;
+    uint8_t* sa = smem + pc_stage * Cfg::kStageBytes;
     uint8_t* sb = sa + Cfg::kABytes;
-    mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
-    const int q = kt / p.kt_per_rank;
-    const int t = kt - q * p.kt_per_rank;
+    mbar_arrive_expect_tx(&full[pc_stage], Cfg::kStageBytes);
+    const int q = pc_kt / p.kt_per_rank;
+    const int t = pc_kt - q * p.kt_per_rank;
     const int ka = q * p.a_rank_stride + t * kBK;
     const int kb = t * kBK;
 #pragma unroll
     for (int h = 0; h < kHalves; ++h) {
-      tma_load_2d(sa + h * BM * 128, &tmA, ka + h * kBKHalf, m0, &full[s]);
-      tma_load_3d(sb + h * BNC * 128, &tmB, kb + h * kBKHalf, bcol, q, &full[s]);
+      tma_load_2d(sa + h * BM * 128, &tmA, ka + h * kBKHalf, m0, &full[pc_stage]);
+      tma_load_3d(sb + h * BNC * 128, &tmB, kb + h * kBKHalf, bcol, q, &full[pc_stage]);
+    }
+    ++pc_j;
+    if (++pc_stage == STAGES) pc_stage = 0;
+    if (++pc_kt == KT) {
+      pc_kt = 0;
+      if (pc_dp_left > 0) {
+        if (--pc_dp_left > 0) {
+          pc_tile += p.grid;
+        } else {
+          pc_init();
+        }
+      } else {
+        ++pc_tile;
+      }
     }
   };
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    for (int kt = 0; kt < STAGES && kt < p.num_kt; ++kt) produce(kt);
+    pc_j = 0;
+    pc_stage = 0;
+    pc_dp_left = p.dp_units;
+    pc_init();
+    while (pc_j < STAGES && pc_j < my_iters) produce();
   }
 
-  // ===== consumers: DMMA main loop =====
   const int wm = warp % Cfg::kWarpsM;
   const int wn = warp / Cfg::kWarpsM;
   const int g = lane >> 2;   // MMA group (row of A / column of B within the 8-wide tile)
@@ -121,94 +201,155 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES>::kThreads,
   const bool odd = (g & 1);  // this lane feeds an imaginary-part (B'') column
   const int a_row0 = wm * WM + g;
   const int b_row0 = wn * WNC + (lane >> 3);
+  bool bad = false;
 
   double acc[Cfg::kMT][Cfg::kNT][2];
-#pragma unroll
-  for (int i = 0; i < Cfg::kMT; ++i)
-#pragma unroll
-    for (int j = 0; j < Cfg::kNT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  for (int kt = 0; kt < p.num_kt; ++kt) {
-    const int s = kt % STAGES;
-    mbar_wait(&full[s], (kt / STAGES) & 1);
-    const uint8_t* sa = smem + s * Cfg::kStageBytes;
-    const uint8_t* sb = sa + Cfg::kABytes;
+  // fused epilogue: three-term recurrence, degree masking, finished-column store
+  auto epilogue = [&](int tile) {
+    const int m0 = (tile / p.tiles_n) * BM;
+    const int col_base = p.col0 + (tile % p.tiles_n) * BNC + wn * WNC + qd;
 #pragma unroll
-    for (int h = 0; h < kHalves; ++h) {
-      const uint8_t* ah = sa + h * BM * 128;
-      const uint8_t* bh = sb + h * BNC * 128;
+    for (int i = 0; i < Cfg::kMT; ++i) {
+      const int64_t r = (int64_t)m0 + wm * WM + i * 8 + g;
+      if (r >= p.nrows) continue;
 #pragma unroll
-      for (int sub = 0; sub < 2; ++sub) {
-        // k-steps 2*sub, 2*sub+1 of this half: lane qd covers doubles 4*qd + 2*sub + {0,1}
-        const int chunk = 2 * qd + sub;
-        double2 av[Cfg::kMT], bv[Cfg::kNT];
-#pragma unroll
-        for (int i = 0; i < Cfg::kMT; ++i) {
-          const int r = a_row0 + i * 8;
-          av[i] = *reinterpret_cast<const double2*>(ah + swz(r, chunk));
+      for (int j = 0; j < Cfg::kNT; ++j) {
+        const int col = col_base + j * 4;
+        if (col >= p.col_end) continue;
+        double vr = acc[i][j][0], vi = acc[i][j][1];
+        if (p.flags & 1) {
+          const double2 yc = p.y_cur[(int64_t)col * p.ld_cur + r];
+          vr -= p.c * yc.x;
+          vi -= p.c * yc.y;
         }
-#pragma unroll
-        for (int j = 0; j < Cfg::kNT; ++j) {
-          const int r = b_row0 + j * 4;
-          const double2 y = *reinterpret_cast<const double2*>(bh + swz(r, chunk));
-          // B' (even g): (re, im) as stored; B'' (odd g): (im, -re)
-          bv[j].x = odd ? y.y : y.x;
-          bv[j].y = odd ? -y.x : y.y;
+        vr *= p.a;
+        vi *= p.a;
+        if (p.flags & 2) {
+          const double2 yp = p.y_prev[(int64_t)col * p.ld_prev + r];
+          vr -= p.b * yp.x;
+          vi -= p.b * yp.y;
         }
-#pragma unroll
-        for (int i = 0; i < Cfg::kMT; ++i)
-#pragma unroll
-          for (int j = 0; j < Cfg::kNT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], av[i].x, bv[j].x);
-#pragma unroll
-        for (int i = 0; i < Cfg::kMT; ++i)
-#pragma unroll
-          for (int j = 0; j < Cfg::kNT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], av[i].y, bv[j].y);
+        const double2 v = make_double2(vr, vi);
+        bad |= !(isfinite(vr) && isfinite(vi));
+        if (col < p.fin_end) {
+          p.out[(int64_t)col * p.ld_out + r] = v;
+        } else {
+          p.y_next[(int64_t)col * p.ld_next + r] = v;
+          if (p.r_next) p.r_next[(int64_t)(col - p.fin_end) * p.ld_r_next + r] = v;
+        }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (threadIdx.x == 0 && kt >= 1) {
-      const int kr = kt - 1 + STAGES;
-      if (kr < p.num_kt) {
-        mbar_wait(&empty[(kt - 1) % STAGES], ((kt - 1) / STAGES) & 1);
-        produce(kr);
-      }
-    }
-  }
+  };
 
-  // ===== fused epilogue: three-term recurrence, degree masking, finished-column store =====
-  const int col_base = p.col0 + n_tile * BNC + wn * WNC + qd;
-  bool bad = false;
+  int64_t j = 0;  // CTA-local iteration (global across tiles)
+  int stage = 0;   // j % STAGES
+  uint32_t phase = 0;  // (j / STAGES) & 1
+  while (j < my_iters) {
+    int tile, kbeg;
+    coords(j, tile, kbeg);
+    // this work unit: k-tiles [kbeg, kend) of `tile`
+    int kend = KT;
+    if (j >= dp_iters) {
+      const int64_t g0 = t_beg + (j - dp_iters);
+      const int64_t tile_end_g = (g0 / KT + 1) * KT;
+      kend = (int)(KT - (tile_end_g - (t_end < tile_end_g ? t_end : tile_end_g)));
+    }
 #pragma unroll
-  for (int i = 0; i < Cfg::kMT; ++i) {
-    const int64_t r = (int64_t)m0 + wm * WM + i * 8 + g;
-    if (r >= p.nrows) continue;
+    for (int i = 0; i < Cfg::kMT; ++i)
 #pragma unroll
-    for (int j = 0; j < Cfg::kNT; ++j) {
-      const int col = col_base + j * 4;
-      if (col >= p.col_end) continue;
-      double vr = acc[i][j][0], vi = acc[i][j][1];
-      if (p.flags & 1) {
-        const double2 yc = p.y_cur[(int64_t)col * p.ld_cur + r];
-        vr -= p.c * yc.x;
-        vi -= p.c * yc.y;
+      for (int jj = 0; jj < Cfg::kNT; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+
+    for (int kt = kbeg; kt < kend; ++kt, ++j) {
+      const int s = stage;
+      mbar_wait(&full[s], phase);
+      const uint8_t* sa = smem + s * Cfg::kStageBytes;
+      const uint8_t* sb = sa + Cfg::kABytes;
+#pragma unroll
+      for (int h = 0; h < kHalves; ++h) {
+        const uint8_t* ah = sa + h * BM * 128;
+        const uint8_t* bh = sb + h * BNC * 128;
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+          // k-steps 2*sub, 2*sub+1 of this half: lane qd covers doubles 4*qd + 2*sub + {0,1}
+          const int chunk = 2 * qd + sub;
+          double2 av[Cfg::kMT], bv[Cfg::kNT];
+#pragma unroll
+          for (int i = 0; i < Cfg::kMT; ++i) av[i] = *reinterpret_cast<const double2*>(ah + swz(a_row0 + i * 8, chunk));
+#pragma unroll
+          for (int jj = 0; jj < Cfg::kNT; ++jj) {
+            const double2 y = *reinterpret_cast<const double2*>(bh + swz(b_row0 + jj * 4, chunk));
+            // B' (even g): (re, im) as stored; B'' (odd g): (im, -re)
+            bv[jj].x = odd ? y.y : y.x;
+            bv[jj].y = odd ? dneg(y.x) : y.y;
+          }
+#pragma unroll
+          for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+            for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], av[i].x, bv[jj].x);
+#pragma unroll
+          for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+            for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], av[i].y, bv[jj].y);
+        }
       }
-      vr *= p.a;
-      vi *= p.a;
-      if (p.flags & 2) {
-        const double2 yp = p.y_prev[(int64_t)col * p.ld_prev + r];
-        vr -= p.b * yp.x;
-        vi -= p.b * yp.y;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      // refill the stage of iteration j - 1 (stage pc_stage, phase of j - 1) with iteration pc_j
+      if (threadIdx.x == 0 && j >= 1 && *(volatile int64_t*)&pc_j < my_iters) {
+        const uint32_t prev_phase = (s == 0) ? (phase ^ 1u) : phase;
+        mbar_wait(&empty[pc_stage], prev_phase);
+        produce();
       }
-      const double2 v = make_double2(vr, vi);
-      bad |= !(isfinite(vr) && isfinite(vi));
-      if (col < p.fin_end) {
-        p.out[(int64_t)col * p.ld_out + r] = v;
-      } else {
-        p.y_next[(int64_t)col * p.ld_next + r] = v;
-        if (p.r_next) p.r_next[(int64_t)(col - p.fin_end) * p.ld_r_next + r] = v;
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1u;
       }
     }
+
+    if (kbeg == 0 && kend == KT) {
+      epilogue(tile);
+      continue;
+    }
+    // ---- split tile: publish the partial accumulator; the last contributor finishes the tile ----
+    const int u = tile - p.tail_tile0;
+    const int64_t U0 = (int64_t)u * KT, U1 = U0 + KT;
+    const int my_slot = (t_beg / KT == u) ? 0 : 1;
+    double* mine = p.partials + ((cta * 2 + my_slot) * kAcc) * (int64_t)Cfg::kThreads;
+#pragma unroll
+    for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < Cfg::kNT; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) __stcg(mine + ((i * Cfg::kNT + jj) * 2 + e) * Cfg::kThreads + threadIdx.x, acc[i][jj][e]);
+    __threadfence();
+    __syncthreads();
+    const int64_t c_lo = sk_owner(U0, p.tail_iters, p.grid), c_hi = sk_owner(U1 - 1, p.tail_iters, p.grid);
+    int nseg = 0;
+    for (int64_t c = c_lo; c <= c_hi; ++c)
+      if (sk_start(c + 1, p.tail_iters, p.grid) > sk_start(c, p.tail_iters, p.grid)) ++nseg;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(&p.tickets[u], 1);
+    __syncthreads();
+    if (s_ticket != nseg - 1) continue;  // not the last contributor
+    __threadfence();
+#pragma unroll
+    for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < Cfg::kNT; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+    for (int64_t c = c_lo; c <= c_hi; ++c) {  // fixed k order: deterministic sum
+      const int64_t cs = sk_start(c, p.tail_iters, p.grid);
+      if (sk_start(c + 1, p.tail_iters, p.grid) <= cs) continue;
+      const int slot = (cs / KT == u) ? 0 : 1;
+      const double* src = p.partials + ((c * 2 + slot) * kAcc) * (int64_t)Cfg::kThreads;
+#pragma unroll
+      for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+        for (int jj = 0; jj < Cfg::kNT; ++jj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) acc[i][jj][e] += __ldcg(src + ((i * Cfg::kNT + jj) * 2 + e) * Cfg::kThreads + threadIdx.x);
+    }
+    epilogue(tile);
+    if (threadIdx.x == 0) p.tickets[u] = 0;  // ready for the next launch (stream ordered)
   }
   if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
 }
@@ -217,8 +358,14 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES>::kThreads,
 struct TileChoice {
   int id;
   int bm, bnc;
+  int threads;  // CTA size of the variant
+  int acc;      // accumulator doubles per thread (partial-slot size = acc * threads doubles)
 };
 TileChoice choose_filter_tile(int64_t nrows, int64_t ncols, int num_sms);
+// Fill the persistent-schedule fields of p (tiles_n .. tail_iters) for variant t on num_sms SMs.
+void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p);
+// workspace the schedule needs: partial slots (doubles) and tickets (ints)
+size_t filter_partials_doubles(const TileChoice& t, int num_sms);
 cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, const CUtensorMap& tmB,
                                const StepParams& p, cudaStream_t stream);
 
