@@ -135,6 +135,8 @@ typedef struct {
   double filter_flops; /* algorithmic: 8 n^2 sum(deg) over all filter calls */
   double t_lanczos, t_filter, t_qr, t_rr, t_resid, t_opt, t_total; /* seconds, CUDA events */
   double theta_min, theta_max, beta_up, normH;
+  double t_filter_kernel; /* seconds inside K1 launches of the filter (CUDA events per launch) */
+  int64_t filter_launches; /* K1 launches of the filter */
 } chfsi_report;
 
 /* Callback giving problem ell's column slab (device pointer and its leading dimension). */

@@ -47,7 +47,8 @@ class Report(ctypes.Structure):
                 ("filter_flops", ctypes.c_double), ("t_lanczos", ctypes.c_double), ("t_filter", ctypes.c_double),
                 ("t_qr", ctypes.c_double), ("t_rr", ctypes.c_double), ("t_resid", ctypes.c_double),
                 ("t_opt", ctypes.c_double), ("t_total", ctypes.c_double), ("theta_min", ctypes.c_double),
-                ("theta_max", ctypes.c_double), ("beta_up", ctypes.c_double), ("normH", ctypes.c_double)]
+                ("theta_max", ctypes.c_double), ("beta_up", ctypes.c_double), ("normH", ctypes.c_double),
+                ("t_filter_kernel", ctypes.c_double), ("filter_launches", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -209,6 +209,15 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
   }
   CUtensorMap tmA;
   int last_bm = -1;
+  // CUDA events around every K1 launch (read back after the final synchronisation)
+  if ((int)ctx->k1_events.size() < 2 * (mk + 1)) {
+    for (int q = (int)ctx->k1_events.size(); q < 2 * (mk + 1); ++q) {
+      cudaEvent_t ev;
+      CHFSI_CUDA_TRY(ctx, cudaEventCreate(&ev));
+      ctx->k1_events.push_back(ev);
+    }
+  }
+  int nev_used = 0;
   int64_t s = 0;  // active start s_i = #{j : deg[j] <= i}
   for (int i = 0; i < mk; ++i) {
     while (s < k && deg[s] <= i) ++s;
@@ -266,12 +275,22 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     schedule_filter_step(t, ctx->num_sms, sp);
     st = sk_workspace(ctx, t, sp);
     if (st) return st;
+    CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used], ctx->stream));
     CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, sp, ctx->stream));
+    CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used + 1], ctx->stream));
+    nev_used += 2;
     ctx->launches++;
     if (p > 1 && ka_next > 0) {
       st = comm_allgather_inplace(ctx, R[oth], (size_t)2 * nloc * ka_next);
       if (st) return st;
     }
+  }
+  CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int q = 0; q < nev_used; q += 2) {
+    float ms = 0;
+    CHFSI_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->k1_events[q], ctx->k1_events[q + 1]));
+    ctx->k1_seconds += ms * 1e-3;
+    ctx->k1_launches++;
   }
   if (check_finite) {
     int h = 0;
@@ -370,6 +389,7 @@ void chfsi_ctx_destroy(chfsi_ctx ctx) {
                     &ctx->ya,    &ctx->xl,     &ctx->tb,     &ctx->idx};
   for (DevBuf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
+  for (cudaEvent_t ev : ctx->k1_events) cudaEventDestroy(ev);
   if (ctx->cublas) cublasDestroy(ctx->cublas);
   if (ctx->cusolver) cusolverDnDestroy(ctx->cusolver);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);

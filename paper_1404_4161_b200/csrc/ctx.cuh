@@ -61,6 +61,10 @@ struct chfsi_ctx_s {
   cusolverDnHandle_t cusolver = nullptr;
   std::string err;
   int64_t launches = 0;
+  // K1 launch timing (CUDA events around every filter-step launch): accumulated seconds, launches
+  double k1_seconds = 0;
+  int64_t k1_launches = 0;
+  std::vector<cudaEvent_t> k1_events;
 
   // workspace
   chfsi::DevBuf L0, L1;          // filter local state (nloc x k each)

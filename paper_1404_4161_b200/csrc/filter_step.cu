@@ -23,17 +23,20 @@ cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ste
 }
 
 struct Variant {
-  int bm, bnc;
+  int bm, bnc, wnc;
   double eff;   // relative per-flop efficiency of the variant (measured)
   int threads;  // CTA size
   int acc;      // accumulator doubles per thread
 };
 constexpr Variant kVariants[] = {
-    {128, 32, 0.944, 256, 32},  // 0: 8 warps, warp tile 32 x 16
-    {64, 64, 0.938, 256, 32},   // 1: 8 warps, warp tile 32 x 16
-    {128, 64, 0.983, 256, 64},  // 2: 8 warps, warp tile 32 x 32
-    {64, 32, 0.724, 128, 32},   // 3: 4 warps
-    {128, 64, 1.000, 512, 32},  // 4: 16 warps (4 per SMSP), warp tile 32 x 16
+    {128, 32, 16, 0.930, 256, 32},  // 0: 8 warps, warp tile 32 x 16
+    {64, 64, 16, 0.920, 256, 32},   // 1: 8 warps, warp tile 32 x 16
+    {128, 64, 32, 0.940, 256, 64},  // 2: 8 warps, warp tile 32 x 32
+    {64, 32, 16, 0.700, 128, 32},   // 3: 4 warps
+    {128, 64, 16, 0.970, 512, 32},  // 4: 16 warps (4 per SMSP), warp tile 32 x 16
+    {128, 16, 16, 0.800, 256, 16},  // 5: 8 warps, warp tile 16 x 16 (narrow blocks)
+    {128, 32, 8, 0.960, 512, 16},   // 6: 16 warps, warp tile 32 x 8
+    {128, 48, 16, 1.000, 384, 32},  // 7: 12 warps, warp tile 32 x 16 (34.9 TF/s at n=13000, k=624)
 };
 
 }  // namespace
@@ -45,27 +48,39 @@ TileChoice choose_filter_tile(int64_t nrows, int64_t ncols, int num_sms) {
   const int nvar = (int)(sizeof(kVariants) / sizeof(kVariants[0]));
   if (forced >= 0 && forced < nvar)
     return TileChoice{forced, kVariants[forced].bm, kVariants[forced].bnc, kVariants[forced].threads,
-                      kVariants[forced].acc};
+                      kVariants[forced].acc, kVariants[forced].wnc};
   // the persistent stream-K schedule removes wave quantisation: minimise padded work / efficiency
   // (efficiencies: measured full-width rates relative to the best variant)
   int best = 0;
   double best_cost = 1e300;
   for (int v = 0; v < nvar; ++v) {
     const int64_t tm = (nrows + kVariants[v].bm - 1) / kVariants[v].bm;
-    const int64_t tn = (ncols + kVariants[v].bnc - 1) / kVariants[v].bnc;
-    const double cost = (double)tm * kVariants[v].bm * tn * kVariants[v].bnc / kVariants[v].eff;
+    // balanced N split in warp-tile units: every tile has `per` active warp columns; idle warps skip
+    // their MMAs but are not free (model: halfway between free and full cost), and fewer than two
+    // active warps per SM sub-partition lose latency hiding (profiles/r01_filter_variants)
+    const Variant& V = kVariants[v];
+    const int64_t units = (ncols + V.wnc - 1) / V.wnc;
+    const int64_t tn = (ncols + V.bnc - 1) / V.bnc;
+    const int64_t per = (units + tn - 1) / tn;
+    const int warps_m = V.threads / 32 / (V.bnc / V.wnc);
+    const double active_warps = (double)per * warps_m;
+    const double occ = active_warps >= 8 ? 1.0 : 0.6 + 0.05 * active_warps;
+    const double cols = 0.5 * (double)(tn * per * V.wnc) + 0.5 * (double)ncols;
+    const double cost = (double)tm * V.bm * cols / (V.eff * occ);
     if (cost < best_cost * 0.999) {
       best_cost = cost;
       best = v;
     }
   }
   (void)num_sms;
-  return TileChoice{best, kVariants[best].bm, kVariants[best].bnc, kVariants[best].threads, kVariants[best].acc};
+  return TileChoice{best, kVariants[best].bm, kVariants[best].bnc, kVariants[best].threads, kVariants[best].acc,
+                    kVariants[best].wnc};
 }
 
 void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
   const int64_t ncols = p.col_end - p.col0;
   const int64_t tm = (p.nrows + t.bm - 1) / t.bm, tn = (ncols + t.bnc - 1) / t.bnc;
+  p.units_n = (int32_t)((ncols + t.wnc - 1) / t.wnc);
   const int64_t tiles = tm * tn;
   const int64_t iters = tiles * p.num_kt;
   const int64_t grid = iters < num_sms ? iters : num_sms;
@@ -91,6 +106,12 @@ cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, cons
       return launch_cfg<64, 32, 32, 16, 8>(tmA, tmB, p, stream);
     case 4:
       return launch_cfg<128, 64, 32, 16, 4>(tmA, tmB, p, stream);
+    case 5:
+      return launch_cfg<128, 16, 16, 16, 6>(tmA, tmB, p, stream);
+    case 6:
+      return launch_cfg<128, 32, 32, 8, 5>(tmA, tmB, p, stream);
+    case 7:
+      return launch_cfg<128, 48, 32, 16, 4>(tmA, tmB, p, stream);
     default:
       return cudaErrorInvalidValue;
   }

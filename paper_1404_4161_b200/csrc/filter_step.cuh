@@ -29,6 +29,7 @@ struct StepParams {
   // tail_tile0.. (each tile = num_kt iterations); a split tile is finished by the last of its
   // contributors to arrive (ticket), which sums the partial accumulators in k order.
   int32_t tiles_n;      // N tiles
+  int32_t units_n;      // WNC-wide column units of the active block, split evenly over the N tiles
   int32_t grid;         // CTAs
   int32_t dp_units;     // full tiles per CTA
   int32_t tail_tile0;   // first stream-K tile
@@ -81,8 +82,21 @@ __device__ __forceinline__ int64_t sk_owner(int64_t g, int64_t iters, int64_t gr
   return ((g + 1) * grid - 1) / iters;
 }
 
-__device__ __forceinline__ double dneg(double x) {  // sign flip on the ALU pipe (no DADD)
-  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
+// balanced N split: N tile i covers column units [i*(U/T) + min(i, U%T), ...) of width U/T (+1 for
+// the first U%T tiles), so every tile has (nearly) the same number of active warps and the stream-K
+// split by iterations stays balanced; returns the first column (relative to col0) and the units
+__device__ __forceinline__ int tile_cols(int ntile, int tiles_n, int units, int wnc, int* n_units) {
+  const int base = units / tiles_n, extra = units % tiles_n;
+  *n_units = base + (ntile < extra ? 1 : 0);
+  return (ntile * base + (ntile < extra ? ntile : extra)) * wnc;
+}
+
+// conditional sign flip on the integer pipe: XOR of the high word with 0 or 0x80000000 (inline PTX so
+// the compiler cannot turn it into an FP64 DADD, which would compete with the DMMAs)
+__device__ __forceinline__ double xor_sign(double x, uint32_t mask) {
+  int hi = __double2hiint(x);
+  asm("xor.b32 %0, %0, %1;" : "+r"(hi) : "r"(mask));
+  return __hiloint2double(hi, __double2loint(x));
 }
 
 template <int BM, int BNC, int WM, int WNC, int STAGES>
@@ -156,7 +170,8 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES>::kThreads,
   };
   auto produce = [&]() {  // load iteration pc_j into stage pc_stage, then advance the cursor
     const int m0 = (pc_tile / p.tiles_n) * BM;
-    const int bcol = p.b_col0 + (pc_tile % p.tiles_n) * BNC;
+    int nu;
+    const int bcol = p.b_col0 + tile_cols(pc_tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
     uint8_t* sa = smem + pc_stage * Cfg::kStageBytes;
     uint8_t* sb = sa + Cfg::kABytes;
     mbar_arrive_expect_tx(&full[pc_stage], Cfg::kStageBytes);
@@ -199,6 +214,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES>::kThreads,
   const int g = lane >> 2;   // MMA group (row of A / column of B within the 8-wide tile)
   const int qd = lane & 3;   // thread in group (k index; output column pair)
   const bool odd = (g & 1);  // this lane feeds an imaginary-part (B'') column
+  const uint32_t sign_mask = odd ? 0x80000000u : 0u;
   const int a_row0 = wm * WM + g;
   const int b_row0 = wn * WNC + (lane >> 3);
   bool bad = false;
@@ -208,7 +224,10 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES>::kThreads,
   // fused epilogue: three-term recurrence, degree masking, finished-column store
   auto epilogue = [&](int tile) {
     const int m0 = (tile / p.tiles_n) * BM;
-    const int col_base = p.col0 + (tile % p.tiles_n) * BNC + wn * WNC + qd;
+    int nu;
+    const int c0 = tile_cols(tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
+    if (wn >= nu) return;  // this warp's columns belong to the next tile
+    const int col_base = p.col0 + c0 + wn * WNC + qd;
 #pragma unroll
     for (int i = 0; i < Cfg::kMT; ++i) {
       const int64_t r = (int64_t)m0 + wm * WM + i * 8 + g;
@@ -260,13 +279,18 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES>::kThreads,
 #pragma unroll
       for (int jj = 0; jj < Cfg::kNT; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
 
+    // a warp whose columns all lie past the active block (ragged last N tile) skips the MMAs: the
+    // DMMA pipe is shared per SM sub-partition, so the padding costs no tensor-core time
+    int nu;
+    tile_cols(tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
+    const bool warp_active = wn < nu;
     for (int kt = kbeg; kt < kend; ++kt, ++j) {
       const int s = stage;
       mbar_wait(&full[s], phase);
       const uint8_t* sa = smem + s * Cfg::kStageBytes;
       const uint8_t* sb = sa + Cfg::kABytes;
 #pragma unroll
-      for (int h = 0; h < kHalves; ++h) {
+      for (int h = 0; h < kHalves && warp_active; ++h) {
         const uint8_t* ah = sa + h * BM * 128;
         const uint8_t* bh = sb + h * BNC * 128;
 #pragma unroll
@@ -278,10 +302,11 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES>::kThreads,
           for (int i = 0; i < Cfg::kMT; ++i) av[i] = *reinterpret_cast<const double2*>(ah + swz(a_row0 + i * 8, chunk));
 #pragma unroll
           for (int jj = 0; jj < Cfg::kNT; ++jj) {
-            const double2 y = *reinterpret_cast<const double2*>(bh + swz(b_row0 + jj * 4, chunk));
-            // B' (even g): (re, im) as stored; B'' (odd g): (im, -re)
-            bv[jj].x = odd ? y.y : y.x;
-            bv[jj].y = odd ? dneg(y.x) : y.y;
+            // B' (even g): (re, im) as stored; B'' (odd g): (im, -re) -- two lane-offset LDS.64 do the
+            // swap, one integer XOR the sign (no select, no FP64 op)
+            const double* y = reinterpret_cast<const double*>(bh + swz(b_row0 + jj * 4, chunk));
+            bv[jj].x = y[odd ? 1 : 0];
+            bv[jj].y = xor_sign(y[odd ? 0 : 1], sign_mask);
           }
 #pragma unroll
           for (int i = 0; i < Cfg::kMT; ++i)
@@ -360,6 +385,7 @@ struct TileChoice {
   int bm, bnc;
   int threads;  // CTA size of the variant
   int acc;      // accumulator doubles per thread (partial-slot size = acc * threads doubles)
+  int wnc;      // complex columns per warp (column-unit width of the balanced N split)
 };
 TileChoice choose_filter_tile(int64_t nrows, int64_t ncols, int num_sms);
 // Fill the persistent-schedule fields of p (tiles_n .. tail_iters) for variant t on num_sms SMs.

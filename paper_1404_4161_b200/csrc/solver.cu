@@ -136,8 +136,12 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
     TRY(gather(Ya, perm, T, nloc));
     // Alg 1 l5: the Chebyshev filter (Alg 2)
     auto t3 = tm.begin();
+    const double k1s = ctx->k1_seconds;
+    const int64_t k1n = ctx->k1_launches;
     TRY(filter_impl(ctx, n, row0, nloc, Hp, ldh, T, nloc, ka, ms.data(), lam1, c, e, true));
     tm.end(T_FILTER, t3);
+    rep.t_filter_kernel += ctx->k1_seconds - k1s;
+    rep.filter_launches += ctx->k1_launches - k1n;
     int64_t mv = 0;
     for (int64_t j = 0; j < ka; ++j) mv += ms[j];
     rep.matvecs_filter += mv;

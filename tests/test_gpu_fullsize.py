@@ -1,0 +1,65 @@
+"""Parity at BASELINE.json's full c2 size (n = 13000, k = 624) in the launch configuration bench.py
+times: the filter on H^(1) checked column by column against the oracle's closed form (every column)
+and against the oracle's Alg 2 (a sample of columns), and the first eigenproblem of the c2 sequence
+checked against H^(1)'s exact spectrum, with naive-oracle residuals on a sample of eigenvectors."""
+import numpy as np
+import pytest
+
+import gen as G
+import oracle as O
+from gen.configs import CONFIGS, HNORM
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def c2():
+    cf = CONFIGS["c2"]
+    w = G.wy(cf["n"], cf["nd"], cf["seed"])
+    H = w.full()
+    return cf, w, H
+
+
+def test_filter_c2_full_width(gpu_lib, c2):
+    cf, w, H = c2
+    n, k = cf["n"], cf["nev"] + cf["nex"]
+    rng = np.random.default_rng(2)
+    deg = sorted(rng.integers(1, cf["cap"] + 1, k).tolist())
+    Y0 = G.start_basis(n, k, cf["seed"])
+    l1, a, b = w.lam[0] - 0.02, w.lam[k], 48.0
+    c, e = (a + b) / 2, (b - a) / 2
+    ctx = gpu_lib.Context(0)
+    Hd = gpu_lib.to_colmajor(H)
+    Yd = gpu_lib.to_colmajor(Y0)
+    assert ctx.filter(Hd, Yd, deg, l1, c, e) == sum(deg)
+    Y = Yd.cpu().numpy()
+    del Hd, Yd
+    ctx.close()
+    Yc = O.filter_wy_closed(w, Y0, deg, l1, c, e)  # every column, closed form (App. A)
+    rel = np.linalg.norm(Y - Yc, axis=0) / np.linalg.norm(Yc, axis=0)
+    assert rel.max() <= 1e-11, (rel.max(), int(np.argmax(rel)))
+    cols = [0, k // 2, k - 1]  # Alg 2 step by step, naive loops
+    Yo, _ = O.chebyshev_filter(H, Y0[:, cols], [deg[j] for j in cols], l1, c, e)
+    rel = np.linalg.norm(Y[:, cols] - Yo, axis=0) / np.linalg.norm(Yo, axis=0)
+    assert rel.max() <= 1e-11
+
+
+def test_solve_c2_first_problem(gpu_lib, c2):
+    cf, w, H = c2
+    n, nev, nex = cf["n"], cf["nev"], cf["nex"]
+    X0 = G.start_basis(n, nev + nex, cf["seed"])
+    ctx = gpu_lib.Context(0)
+    Hd = gpu_lib.to_colmajor(H)
+    Xd = gpu_lib.to_colmajor(X0)
+    out = ctx.solve_sequence(lambda ell: Hd, 1, Xd, nev, nex, cf["tol"], deg_cap=cf["cap"], seed=cf["seed"])
+    X = Xd.cpu().numpy()[:, :nev]
+    del Hd, Xd
+    ctx.close()
+    assert out["status"] == 0
+    lam = out["lam"][0]
+    # H^(1) has the exact spectrum Lambda: the nev smallest, to 1e-10 relative (J)
+    assert np.max(np.abs(lam - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
+    assert np.abs(X.conj().T @ X - np.eye(nev)).max() <= 1e-12
+    sample = [0, 1, nev // 2, nev - 2, nev - 1]
+    res = O.residuals(H, X[:, sample], lam[sample], HNORM)  # ||H x - lam x|| / ||H||_2, naive
+    assert res.max() <= cf["tol"]
