@@ -224,9 +224,11 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         t = torch.zeros(1, device="cuda")
-        dist.all_reduce(t)  # materialise the NCCL communicator
-        pg = dist.distributed_c10d._get_default_group()
-        comm = pg._get_backend(torch.device("cuda"))._comm_ptr()
+        dist.all_reduce(t)
+        # the library owns its NCCL communicator: rank 0's ncclUniqueId is broadcast over torch.distributed
+        obj = [chfsi.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = obj[0]
     n, nev, nex = cf["n"], cf["nev"], cf["nex"]
     k = nev + nex
     row0, nloc = rank_rows(n, world, rank)
@@ -246,7 +248,7 @@ def main():
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
 
-    ctx = chfsi.Context(local_rank, nccl_comm=comm, rank=rank, nranks=world)
+    ctx = chfsi.Context(local_rank, nccl_id=comm, rank=rank, nranks=world) if world > 1 else chfsi.Context(local_rank)
     ctx.reserve(n, nloc, k)
     stream = torch.cuda.current_stream()
 

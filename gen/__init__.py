@@ -41,6 +41,7 @@ def lib():
         L.gen_gue_panel.argtypes = [i64, u64, u64, i64, i64, ptr, i64]
         L.gen_perturb_panel.argtypes = [i64, u64, i32, dbl, i64, i64, ptr, i64]
         L.gen_start_basis.argtypes = [i64, i64, u64, i64, i64, ptr, i64]
+        L.gen_lower_factor.argtypes = [i64, u64, dbl, ptr, i64]
         _lib = L
     return _lib
 
@@ -123,3 +124,21 @@ def start_basis(n: int, k: int, seed: int, r0: int = 0, nrows: int | None = None
 
 def uniform(seed: int, strm: int, idx: int) -> float:
     return lib().gen_uniform(seed, strm, idx)
+
+
+def lower_factor(n: int, seed: int, scale: float = 0.5) -> np.ndarray:
+    M = np.empty((n, n), dtype=np.complex128, order="F")
+    lib().gen_lower_factor(n, seed, scale, _p(M), n)
+    return M
+
+
+def generalized_pair(wy: WY, seed: int, scale: float = 0.5):
+    """(A, B, M): B = M M^H (HPD, Cholesky factor M), A = M H^(1) M^H -- generalised eigenvalues = wy.lam,
+    generalised eigenvectors M^{-H} Q e_i. Products formed with numpy (input construction only)."""
+    M = lower_factor(wy.n, seed, scale)
+    H = wy.full()
+    B = np.asfortranarray(M @ M.conj().T)
+    A = M @ H @ M.conj().T
+    A = np.asfortranarray((A + A.conj().T) / 2)  # exact Hermitian storage (R13)
+    B = np.asfortranarray((B + B.conj().T) / 2)
+    return A, B, M

@@ -277,3 +277,25 @@ void gen_start_basis(int64_t n, int64_t k, uint64_t seed, int64_t r0, int64_t nr
     }
   }
 }
+
+void gen_lower_factor(int64_t n, uint64_t seed, double scale, double* M, int64_t ldm) {
+  uint64_t stream = GEN_STREAM(6, 0);
+  const double s = scale / sqrt(2.0 * (double)n);
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int64_t j = 0; j < n; ++j) {
+    double* col = M + 2 * j * ldm;
+    for (int64_t i = 0; i < n; ++i) {
+      if (i < j) {
+        col[2 * i] = col[2 * i + 1] = 0.0;
+      } else if (i == j) {
+        col[2 * i] = 1.0 + 0.5 * gen_uniform(seed, stream, (uint64_t)i * (uint64_t)n + (uint64_t)i);
+        col[2 * i + 1] = 0.0;
+      } else {
+        double x, y;
+        gen_normal2(seed, stream, (uint64_t)i * (uint64_t)n + (uint64_t)j, &x, &y);
+        col[2 * i] = s * x;
+        col[2 * i + 1] = s * y;
+      }
+    }
+  }
+}

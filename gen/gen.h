@@ -55,6 +55,12 @@ void gen_perturb_panel(int64_t n, uint64_t seed, int32_t ell, double scale, int6
 void gen_start_basis(int64_t n, int64_t k, uint64_t seed, int64_t r0, int64_t nrows,
                      double* Y, int64_t ldy);
 
+/* Lower-triangular factor with real positive diagonal for a generalised pair with a known spectrum
+ * (DESIGN.md 5): M[i,i] = 1 + 0.5 u_i, M[i,j] = scale (x + i y)/sqrt(2n) for i > j (stream (6,0)),
+ * zero above the diagonal. B = M M^H is Hermitian positive definite with Cholesky factor M, and
+ * A = M H^(1) M^H has the generalised eigenvalues Lambda. */
+void gen_lower_factor(int64_t n, uint64_t seed, double scale, double* M, int64_t ldm);
+
 #ifdef __cplusplus
 }
 #endif

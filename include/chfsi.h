@@ -48,6 +48,13 @@ typedef enum {
  * stream 0, ordered with the caller's default-stream work). nccl_comm: an ncclComm_t spanning the `nranks` ranks (NULL when nranks == 1). */
 chfsi_status chfsi_ctx_create(chfsi_ctx* out, int32_t device, void* cuda_stream, void* nccl_comm,
                               int32_t rank, int32_t nranks);
+/* A library-owned NCCL communicator (NVLink / NVSwitch): rank 0 calls chfsi_nccl_unique_id, the caller
+ * broadcasts the 128 bytes (e.g. over torch.distributed), then every rank calls chfsi_ctx_create_nccl.
+ * The communicator is created with ncclCommInitRank and destroyed with the context. */
+chfsi_status chfsi_nccl_unique_id(char id_out[128]);
+chfsi_status chfsi_ctx_create_nccl(chfsi_ctx* out, int32_t device, void* cuda_stream, const char id[128],
+                                   int32_t rank, int32_t nranks);
+
 /* Emulated ranks: `nranks` contexts in one process, on one device, share a local group whose
  * collectives are device copies ordered by CUDA events and a host barrier (same semantics as the
  * NCCL calls). Drive each rank from its own host thread, each context on its own stream. This runs
@@ -87,6 +94,14 @@ chfsi_status chfsi_filter(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, 
                           int64_t ldh, void* Y, int64_t ldy, int64_t k, const int32_t* deg,
                           double lambda1, double c, double e, int64_t* matvecs);
 
+/* Real-symmetric variant of chfsi_filter (SPEC supports both fields): the
+ * same Alg 2 recurrence on real data -- Hp (n x nloc, double, the rank's column slab of the symmetric H),
+ * Y (nloc x k, double) -- with a plain real FP64 DMMA GEMM (2 n nloc k_a flop per step instead of 8).
+ * Arguments, layout and errors as chfsi_filter. */
+chfsi_status chfsi_filter_real(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const double* Hp,
+                               int64_t ldh, double* Y, int64_t ldy, int64_t k, const int32_t* deg,
+                               double lambda1, double c, double e, int64_t* matvecs);
+
 /* Lanczos spectral bounds -- Alg 1 line 3, reading R17: `steps` iterations
  * with full reorthogonalisation from the normalised counter-based start vector of DESIGN.md R22
  * (seed, stream (4 << 16) | restart); a breakdown restarts with the next stream, at most 3 times.
@@ -118,6 +133,22 @@ chfsi_status chfsi_rayleigh_ritz(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t
                                  const void* Hp, int64_t ldh, void* Q, int64_t ldq, int64_t k,
                                  double normH, double* ritz, double* resid);
 
+/* Reduction of the generalised problem A c = lambda B c to standard form -- P:541-545 ("H = L^{-1} A
+ * L^{-T} where B = L L^T", complex Hermitian: L^{-1} A L^{-H}; the FLAPW problems of P:330-347):
+ *   B  device n x n (ldb >= n), Hermitian positive definite; out: its Cholesky factor L in the lower
+ *      triangle (B = L L^H, real positive diagonal); the strict upper triangle is left unspecified.
+ *   A  device n x n (lda >= n), Hermitian; out: H = L^{-1} A L^{-H}, stored full and exactly
+ *      Hermitian ((H + H^H)/2, R13) -- the input of chfsi_solve_sequence / chfsi_filter.
+ * Single rank only (nranks == 1). Errors: CHFSI_ERR_ARG (dims, nranks > 1, B not positive definite:
+ * the failing pivot is named in chfsi_last_error), CHFSI_ERR_CUDA. */
+chfsi_status chfsi_reduce_generalized(chfsi_ctx ctx, int64_t n, void* A, int64_t lda, void* B,
+                                      int64_t ldb);
+/* Back-transformation of eigenvectors of H to generalised eigenvectors: X <- L^{-H} X (c = L^{-H} y),
+ * L from chfsi_reduce_generalized (lower triangle of the returned B). X device n x k (ldx >= n). The
+ * result is B-orthonormal when X is orthonormal. Single rank only. */
+chfsi_status chfsi_back_transform(chfsi_ctx ctx, int64_t n, const void* L, int64_t ldl, void* X,
+                                  int64_t ldx, int64_t k);
+
 typedef struct {
   int32_t nev, nex;      /* wanted eigenpairs and extra buffer columns, k = nev + nex <= n */
   int32_t deg0;          /* starting degree of each problem's first loop (R12; default 8) */
@@ -127,6 +158,11 @@ typedef struct {
   double tol;            /* residual tolerance, relative to ||H||_est (R8), e.g. 1e-10 */
   uint64_t seed;         /* Lanczos start-vector seed; problem ell uses seed + ell */
   int32_t random_start;  /* 1: ignore X on input and draw a counter-based start block (R22) */
+  /* ablations: */
+  int32_t no_reuse;      /* 1: every problem starts from its own random block (R22, seed + ell) instead
+                            of the previous problem's eigenvectors -- Fig 2b's "random vectors" arm */
+  int32_t fixed_degree;  /* > 0: every vector is filtered with this degree in every loop (no Single
+                            Optimisation) -- Fig 5's "-OPT" arm; 0: optimised degrees */
 } chfsi_opts;
 
 typedef struct {
@@ -156,6 +192,25 @@ chfsi_status chfsi_solve_sequence(chfsi_ctx ctx, int64_t n, int64_t row0, int64_
                                   int32_t nprob, chfsi_get_h get_h, void* user,
                                   const chfsi_opts* opts, void* X, int64_t ldx, double* lambda,
                                   double* resid, chfsi_report* reports);
+
+/* Independent sequences: the N_k k-point sequences of one SCF cycle are
+ * independent eigenproblem sequences. chfsi_solve_batch solves `count` of them
+ * concurrently on one device with `workers` library contexts, each on its own CUDA stream and host
+ * thread, taking sequences in order. Each sequence is described as for chfsi_solve_sequence (single
+ * rank: row0 = 0, nloc = n); its status is returned in `status`. The call returns the worst status. */
+typedef struct {
+  int32_t nprob;
+  chfsi_get_h get_h;
+  void* user;
+  void* X;          /* device n x (nev+nex) */
+  int64_t ldx;
+  double* lambda;   /* host nprob * nev */
+  double* resid;    /* host nprob * nev, nullable */
+  chfsi_report* reports; /* host [nprob], nullable */
+  chfsi_status status;   /* out */
+} chfsi_sequence;
+chfsi_status chfsi_solve_batch(int32_t device, int32_t workers, int64_t n, const chfsi_opts* opts,
+                               chfsi_sequence* seqs, int32_t count);
 
 #ifdef __cplusplus
 }

@@ -70,6 +70,11 @@ def lib():
         L.ora_chfsi_solve.argtypes = [i64, ptr, i64, ctypes.POINTER(Opts), ptr, i64, i32, ptr, ptr, ptr, ptr,
                                       ctypes.POINTER(Report)]
         L.ora_chfsi_solve.restype = i32
+        L.ora_cholesky.argtypes = [i64, ptr, i64, ptr, i64]
+        L.ora_cholesky.restype = i32
+        L.ora_trsm_lower.argtypes = [i64, i64, ptr, i64, ptr, i64, i32]
+        L.ora_reduce_generalized.argtypes = [i64, ptr, i64, ptr, i64, ptr, i64, ptr, i64]
+        L.ora_reduce_generalized.restype = i32
         L.ora_count_below.argtypes = [i64, ptr, i64, dbl]
         L.ora_count_below.restype = i64
         _lib = L
@@ -230,3 +235,33 @@ def chfsi_solve(H, X0, nev, nex, tol, cap, deg0=8, max_loops=50, lanczos_steps=2
 def count_below(H, sigma_):
     H = _cf(H)
     return lib().ora_count_below(H.shape[0], _p(H), H.shape[0], sigma_)
+
+
+def cholesky(B):
+    B = _cf(B)
+    n = B.shape[0]
+    L = np.empty((n, n), dtype=np.complex128, order="F")
+    st = lib().ora_cholesky(n, _p(B), n, _p(L), n)
+    if st:
+        raise ValueError(f"not positive definite at pivot {st - 1}")
+    return L
+
+
+def trsm_lower(L, X, adjoint=False):
+    L = _cf(L)
+    X = _cf(X).copy(order="F")
+    lib().ora_trsm_lower(L.shape[0], X.shape[1], _p(L), L.shape[0], _p(X), X.shape[0], 1 if adjoint else 0)
+    return X
+
+
+def reduce_generalized(A, B):
+    """(H, L): B = L L^H, H = L^{-1} A L^{-H}."""
+    A = _cf(A)
+    B = _cf(B)
+    n = A.shape[0]
+    H = np.empty((n, n), dtype=np.complex128, order="F")
+    L = np.empty((n, n), dtype=np.complex128, order="F")
+    st = lib().ora_reduce_generalized(n, _p(A), n, _p(B), n, _p(H), n, _p(L), n)
+    if st:
+        raise ValueError(f"B not positive definite at pivot {st - 1}")
+    return H, L

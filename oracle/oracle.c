@@ -887,3 +887,96 @@ int64_t ora_count_below(int64_t n, const double* H, int64_t ldh, double sigma) {
   free(A);
   return neg;
 }
+
+/* ------------------------------------------------------------------------------------------------ */
+/* Cholesky, column by column (left-looking): L[j,j] = sqrt(B[j,j] - sum_p |L[j,p]|^2),
+ * L[i,j] = (B[i,j] - sum_p L[i,p] conj(L[j,p])) / L[j,j] for i > j. */
+int32_t ora_cholesky(int64_t n, const double* B, int64_t ldb, double* L, int64_t ldl) {
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < n; ++i) L[2 * (j * ldl + i)] = L[2 * (j * ldl + i) + 1] = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    double d = B[2 * (j * ldb + j)];
+    for (int64_t p = 0; p < j; ++p) {
+      double lr = L[2 * (p * ldl + j)], li = L[2 * (p * ldl + j) + 1];
+      d -= lr * lr + li * li;
+    }
+    if (!(d > 0.0)) return (int32_t)(j + 1);
+    d = sqrt(d);
+    L[2 * (j * ldl + j)] = d;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = j + 1; i < n; ++i) {
+      double sr = B[2 * (j * ldb + i)], si = B[2 * (j * ldb + i) + 1];
+      for (int64_t p = 0; p < j; ++p) {
+        double ar = L[2 * (p * ldl + i)], ai = L[2 * (p * ldl + i) + 1]; /* L[i,p] */
+        double br = L[2 * (p * ldl + j)], bi = -L[2 * (p * ldl + j) + 1]; /* conj(L[j,p]) */
+        sr -= ar * br - ai * bi;
+        si -= ar * bi + ai * br;
+      }
+      L[2 * (j * ldl + i)] = sr / d;
+      L[2 * (j * ldl + i) + 1] = si / d;
+    }
+  }
+  return 0;
+}
+
+void ora_trsm_lower(int64_t n, int64_t k, const double* L, int64_t ldl, double* X, int64_t ldx,
+                    int32_t adjoint) {
+#pragma omp parallel for schedule(static)
+  for (int64_t c = 0; c < k; ++c) {
+    double* x = X + 2 * c * ldx;
+    if (!adjoint) { /* forward: x_i = (x_i - sum_{p<i} L[i,p] x_p) / L[i,i] */
+      for (int64_t i = 0; i < n; ++i) {
+        double sr = x[2 * i], si = x[2 * i + 1];
+        for (int64_t p = 0; p < i; ++p) {
+          double lr = L[2 * (p * ldl + i)], li = L[2 * (p * ldl + i) + 1];
+          sr -= lr * x[2 * p] - li * x[2 * p + 1];
+          si -= lr * x[2 * p + 1] + li * x[2 * p];
+        }
+        double dr = L[2 * (i * ldl + i)], di = L[2 * (i * ldl + i) + 1];
+        double den = dr * dr + di * di;
+        x[2 * i] = (sr * dr + si * di) / den;
+        x[2 * i + 1] = (si * dr - sr * di) / den;
+      }
+    } else { /* backward with L^H: x_i = (x_i - sum_{p>i} conj(L[p,i]) x_p) / conj(L[i,i]) */
+      for (int64_t i = n - 1; i >= 0; --i) {
+        double sr = x[2 * i], si = x[2 * i + 1];
+        for (int64_t p = i + 1; p < n; ++p) {
+          double lr = L[2 * (i * ldl + p)], li = -L[2 * (i * ldl + p) + 1];
+          sr -= lr * x[2 * p] - li * x[2 * p + 1];
+          si -= lr * x[2 * p + 1] + li * x[2 * p];
+        }
+        double dr = L[2 * (i * ldl + i)], di = -L[2 * (i * ldl + i) + 1];
+        double den = dr * dr + di * di;
+        x[2 * i] = (sr * dr + si * di) / den;
+        x[2 * i + 1] = (si * dr - sr * di) / den;
+      }
+    }
+  }
+}
+
+int32_t ora_reduce_generalized(int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb,
+                               double* H, int64_t ldh, double* L, int64_t ldl) {
+  int32_t st = ora_cholesky(n, B, ldb, L, ldl);
+  if (st) return st;
+  double* W = (double*)malloc(sizeof(double) * 2 * (size_t)n * (size_t)n);
+  for (int64_t j = 0; j < n; ++j) memcpy(W + 2 * j * n, A + 2 * j * lda, sizeof(double) * 2 * n);
+  ora_trsm_lower(n, n, L, ldl, W, n, 0); /* W = L^{-1} A */
+  for (int64_t j = 0; j < n; ++j)        /* H = W^H (= A L^{-H} for Hermitian A) */
+    for (int64_t i = 0; i < n; ++i) {
+      H[2 * (j * ldh + i)] = W[2 * (i * n + j)];
+      H[2 * (j * ldh + i) + 1] = -W[2 * (i * n + j) + 1];
+    }
+  ora_trsm_lower(n, n, L, ldl, H, ldh, 0); /* H = L^{-1} A L^{-H} */
+  for (int64_t j = 0; j < n; ++j)          /* hermitise */
+    for (int64_t i = 0; i <= j; ++i) {
+      double ur = 0.5 * (H[2 * (j * ldh + i)] + H[2 * (i * ldh + j)]);
+      double ui = 0.5 * (H[2 * (j * ldh + i) + 1] - H[2 * (i * ldh + j) + 1]);
+      if (i == j) ui = 0.0;
+      H[2 * (j * ldh + i)] = ur;
+      H[2 * (j * ldh + i) + 1] = ui;
+      H[2 * (i * ldh + j)] = ur;
+      H[2 * (i * ldh + j) + 1] = -ui;
+    }
+  free(W);
+  return 0;
+}

@@ -109,6 +109,17 @@ int32_t ora_chfsi_solve(int64_t n, const double* H, int64_t ldh, const ora_opts*
                         int64_t ldx, int32_t have_prev, double* lambda1, double* lambdak,
                         double* lam, double* resid, ora_report* rep);
 
+/* ---- generalised front / back end (H = L^{-1} A L^{-H}, B = L L^H) --------------------- */
+/* Cholesky B = L L^H (L lower, real positive diagonal; upper part of L set to 0). Returns 0, or j+1 if
+ * pivot j is not positive. */
+int32_t ora_cholesky(int64_t n, const double* B, int64_t ldb, double* L, int64_t ldl);
+/* X (n x k) <- L^{-1} X (adjoint = 0) or L^{-H} X (adjoint = 1), forward / backward substitution. */
+void ora_trsm_lower(int64_t n, int64_t k, const double* L, int64_t ldl, double* X, int64_t ldx,
+                    int32_t adjoint);
+/* H = L^{-1} A L^{-H} (hermitised) and L = chol(B). Returns the Cholesky status. */
+int32_t ora_reduce_generalized(int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb,
+                               double* H, int64_t ldh, double* L, int64_t ldl);
+
 /* Number of eigenvalues of H strictly below sigma: inertia of H - sigma I by an LDL^H factorisation
  * with Bunch-Kaufman-free diagonal pivoting on a copy (Sylvester's law of inertia). */
 int64_t ora_count_below(int64_t n, const double* H, int64_t ldh, double sigma);

@@ -24,9 +24,10 @@ MAX_DEGREE = 64
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_NOCONV", 4: "ERR_QR", 5: "ERR_CUDA", 6: "ERR_NCCL",
           7: "ERR_NOMEM"}
 
-EXPORTS = ("chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_ctx_reserve", "chfsi_ctx_destroy",
+EXPORTS = ("chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_ctx_create_nccl", "chfsi_nccl_unique_id", "chfsi_ctx_reserve", "chfsi_ctx_destroy",
            "chfsi_last_error", "chfsi_kernel_launches", "chfsi_local_group_create", "chfsi_local_group_destroy",
-           "chfsi_filter", "chfsi_lanczos_bounds", "chfsi_qr", "chfsi_rayleigh_ritz", "chfsi_solve_sequence")
+           "chfsi_filter", "chfsi_filter_real", "chfsi_lanczos_bounds", "chfsi_qr", "chfsi_rayleigh_ritz", "chfsi_solve_sequence",
+           "chfsi_reduce_generalized", "chfsi_back_transform", "chfsi_solve_batch")
 
 
 class ChfsiError(RuntimeError):
@@ -38,7 +39,8 @@ class ChfsiError(RuntimeError):
 class Opts(ctypes.Structure):
     _fields_ = [("nev", ctypes.c_int32), ("nex", ctypes.c_int32), ("deg0", ctypes.c_int32),
                 ("deg_cap", ctypes.c_int32), ("max_loops", ctypes.c_int32), ("lanczos_steps", ctypes.c_int32),
-                ("tol", ctypes.c_double), ("seed", ctypes.c_uint64), ("random_start", ctypes.c_int32)]
+                ("tol", ctypes.c_double), ("seed", ctypes.c_uint64), ("random_start", ctypes.c_int32),
+                ("no_reuse", ctypes.c_int32), ("fixed_degree", ctypes.c_int32)]
 
 
 class Report(ctypes.Structure):
@@ -54,8 +56,17 @@ class Report(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class Sequence(ctypes.Structure):
+    pass
+
+
 GET_H = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p),
                          ctypes.POINTER(ctypes.c_int64))
+
+Sequence._fields_ = [("nprob", ctypes.c_int32), ("get_h", GET_H), ("user", ctypes.c_void_p), ("X", ctypes.c_void_p),
+                     ("ldx", ctypes.c_int64), ("lambda_", ctypes.POINTER(ctypes.c_double)),
+                     ("resid", ctypes.POINTER(ctypes.c_double)), ("reports", ctypes.POINTER(Report)),
+                     ("status", ctypes.c_int)]
 
 _lib = None
 
@@ -71,6 +82,10 @@ def lib():
         pd, pi64, pi32 = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)
         L.chfsi_ctx_create.argtypes = [ctypes.POINTER(vp), i32, vp, vp, i32, i32]
         L.chfsi_ctx_create_local.argtypes = [ctypes.POINTER(vp), i32, vp, vp, i32]
+        L.chfsi_ctx_create_nccl.argtypes = [ctypes.POINTER(vp), i32, vp, ctypes.c_char_p, i32, i32]
+        L.chfsi_ctx_create_nccl.restype = ctypes.c_int
+        L.chfsi_nccl_unique_id.argtypes = [ctypes.c_char_p]
+        L.chfsi_nccl_unique_id.restype = ctypes.c_int
         L.chfsi_local_group_create.argtypes = [ctypes.POINTER(vp), i32]
         L.chfsi_local_group_destroy.argtypes = [vp]
         L.chfsi_local_group_destroy.restype = None
@@ -82,12 +97,17 @@ def lib():
         L.chfsi_kernel_launches.argtypes = [vp]
         L.chfsi_kernel_launches.restype = i64
         L.chfsi_filter.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, i64, pi32, dbl, dbl, dbl, pi64]
+        L.chfsi_filter_real.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, i64, pi32, dbl, dbl, dbl, pi64]
+        L.chfsi_filter_real.restype = ctypes.c_int
         L.chfsi_lanczos_bounds.argtypes = [vp, i64, i64, i64, vp, i64, i32, u64, pd, pd, pd]
         L.chfsi_qr.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, pi32]
         L.chfsi_rayleigh_ritz.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, i64, dbl, pd, pd]
         L.chfsi_solve_sequence.argtypes = [vp, i64, i64, i64, i32, GET_H, vp, ctypes.POINTER(Opts), vp, i64, pd, pd,
                                            ctypes.POINTER(Report)]
-        for name in ("chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_local_group_create", "chfsi_ctx_reserve", "chfsi_filter", "chfsi_lanczos_bounds", "chfsi_qr",
+        L.chfsi_reduce_generalized.argtypes = [vp, i64, vp, i64, vp, i64]
+        L.chfsi_back_transform.argtypes = [vp, i64, vp, i64, vp, i64, i64]
+        L.chfsi_solve_batch.argtypes = [i32, i32, i64, ctypes.POINTER(Opts), ctypes.POINTER(Sequence), i32]
+        for name in ("chfsi_solve_batch", "chfsi_reduce_generalized", "chfsi_back_transform", "chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_local_group_create", "chfsi_ctx_reserve", "chfsi_filter", "chfsi_lanczos_bounds", "chfsi_qr",
                      "chfsi_rayleigh_ritz", "chfsi_solve_sequence"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
@@ -102,22 +122,24 @@ def colmajor(rows: int, cols: int, device="cuda", dtype=None):
     return torch.empty((cols, rows), dtype=dtype, device=device).t()
 
 
-def to_colmajor(a, device="cuda"):
-    """Copy a numpy / torch (rows x cols) array into a column-major complex128 device tensor."""
+def to_colmajor(a, device="cuda", real=False):
+    """Copy a numpy / torch (rows x cols) array into a column-major complex128 (real: float64) device tensor."""
     import torch
 
     t = torch.as_tensor(np.asarray(a) if not isinstance(a, torch.Tensor) else a)
-    out = colmajor(t.shape[0], t.shape[1], device=device)
-    out.copy_(t.to(torch.complex128))
+    dt = torch.float64 if real else torch.complex128
+    out = colmajor(t.shape[0], t.shape[1], device=device, dtype=dt)
+    out.copy_(t.real.to(dt) if (real and t.is_complex()) else t.to(dt))
     return out
 
 
-def _mat(t, rows=None, cols=None, name="matrix"):
-    """(pointer, ld) of a column-major complex128 CUDA tensor."""
+def _mat(t, rows=None, cols=None, name="matrix", real=False):
+    """(pointer, ld) of a column-major complex128 (real=True: float64) CUDA tensor."""
     import torch
 
-    if not isinstance(t, torch.Tensor) or t.dtype != torch.complex128 or not t.is_cuda or t.dim() != 2:
-        raise TypeError(f"{name}: need a 2-D complex128 CUDA tensor")
+    want = torch.float64 if real else torch.complex128
+    if not isinstance(t, torch.Tensor) or t.dtype != want or not t.is_cuda or t.dim() != 2:
+        raise TypeError(f"{name}: need a 2-D {want} CUDA tensor")
     if rows is not None and t.shape[0] != rows or cols is not None and t.shape[1] != cols:
         raise ValueError(f"{name}: shape {tuple(t.shape)} != ({rows}, {cols})")
     if t.shape[1] > 1 and t.stride(0) != 1 or t.shape[1] <= 1 and t.shape[0] > 1 and t.stride(0) != 1:
@@ -143,13 +165,23 @@ class LocalGroup:
             self.h = None
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for Context(nccl_id=...) (rank 0 creates it; broadcast it to all ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    st = lib().chfsi_nccl_unique_id(buf)
+    if st != 0:
+        raise ChfsiError(st, "chfsi_nccl_unique_id failed (NCCL unavailable?)")
+    return buf.raw
+
+
 class Context:
     """A library context on one device (one per rank). Work runs on `stream` (default: torch's current
-    stream). For nranks > 1 pass `nccl_comm` (an ncclComm_t as int, e.g. from torch's ProcessGroupNCCL)
-    or a LocalGroup (emulated ranks on one device)."""
+    stream). For nranks > 1 pass `nccl_id` (bytes from nccl_unique_id(), broadcast to all ranks: the
+    library creates its own NCCL communicator), or `nccl_comm` (an existing ncclComm_t as int), or a
+    LocalGroup (emulated ranks on one device)."""
 
     def __init__(self, device: int = 0, stream=None, nccl_comm: int | None = None, rank: int = 0, nranks: int = 1,
-                 local_group: LocalGroup | None = None):
+                 local_group: LocalGroup | None = None, nccl_id: bytes | None = None):
         import torch
 
         L = lib()
@@ -162,6 +194,9 @@ class Context:
         if local_group is not None:
             st = L.chfsi_ctx_create_local(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream),
                                           local_group.h, rank)
+        elif nccl_id is not None:
+            st = L.chfsi_ctx_create_nccl(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream),
+                                         ctypes.c_char_p(bytes(nccl_id)), rank, nranks)
         else:
             st = L.chfsi_ctx_create(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream),
                                     ctypes.c_void_p(nccl_comm or 0), rank, nranks)
@@ -204,6 +239,18 @@ class Context:
         self._check(lib().chfsi_filter(self.h, n, row0, nloc, hp, ldh, yp, ldy, k, d, lambda1, c, e, ctypes.byref(mv)))
         return mv.value
 
+    def filter_real(self, Hp, Y, deg, lambda1, c, e, n=None, row0=0):
+        """Real-symmetric Alg 2 (chfsi_filter_real): float64 column-major Hp (n x nloc) and Y (nloc x k)."""
+        nloc, k = Y.shape
+        n = n or Hp.shape[0]
+        hp, ldh = _mat(Hp, n, nloc, "Hp", real=True)
+        yp, ldy = _mat(Y, nloc, k, "Y", real=True)
+        d = (ctypes.c_int32 * max(k, 1))(*[int(x) for x in deg])
+        mv = ctypes.c_int64()
+        self._check(lib().chfsi_filter_real(self.h, n, row0, nloc, hp, ldh, yp, ldy, k, d, lambda1, c, e,
+                                            ctypes.byref(mv)))
+        return mv.value
+
     # -- Alg 1 l3 ----------------------------------------------------------------------------------
     def lanczos_bounds(self, Hp, steps=25, seed=0, n=None, row0=0):
         n = n or Hp.shape[0]
@@ -237,9 +284,24 @@ class Context:
             res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if res is not None else None))
         return ritz, res
 
+    # -- generalised front / back end ------------------------------------------------
+    def reduce_generalized(self, A, B):
+        """In place: B <- L (lower Cholesky factor), A <- H = L^{-1} A L^{-H}."""
+        n = A.shape[0]
+        ap, lda = _mat(A, n, n, "A")
+        bp, ldb = _mat(B, n, n, "B")
+        self._check(lib().chfsi_reduce_generalized(self.h, n, ap, lda, bp, ldb))
+
+    def back_transform(self, L, X):
+        """In place: X <- L^{-H} X (generalised eigenvectors)."""
+        n, k = X.shape
+        lp, ldl = _mat(L, n, n, "L")
+        xp, ldx = _mat(X, n, k, "X")
+        self._check(lib().chfsi_back_transform(self.h, n, lp, ldl, xp, ldx, k))
+
     # -- Alg 1 over a sequence ----------------------------------------------------------------------
     def solve_sequence(self, get_h, nprob, X, nev, nex, tol, deg_cap=40, deg0=8, max_loops=50, lanczos_steps=25,
-                       seed=0, random_start=False, n=None, row0=0):
+                       seed=0, random_start=False, n=None, row0=0, no_reuse=False, fixed_degree=0):
         """get_h(ell) -> column-major CUDA tensor Hp (n x nloc) of problem ell (kept alive by the caller
         until the next call). Returns dict(status, lam (nprob x nev), resid, reports)."""
         nloc, k = X.shape
@@ -261,7 +323,8 @@ class Context:
                 return 1
 
         cbf = GET_H(cb)
-        opts = Opts(nev, nex, deg0, deg_cap, max_loops, lanczos_steps, tol, seed, 1 if random_start else 0)
+        opts = Opts(nev, nex, deg0, deg_cap, max_loops, lanczos_steps, tol, seed, 1 if random_start else 0,
+                    1 if no_reuse else 0, int(fixed_degree))
         lam = np.zeros(nprob * nev)
         res = np.zeros(nprob * nev)
         reps = (Report * nprob)()
@@ -273,6 +336,51 @@ class Context:
         self._check(st)
         return dict(status=st, lam=lam.reshape(nprob, nev), resid=res.reshape(nprob, nev),
                     reports=[r.as_dict() for r in reps])
+
+
+def solve_batch(device, workers, sequences, nev, nex, tol, deg_cap=40, deg0=8, max_loops=50, lanczos_steps=25,
+                seed=0):
+    """Independent sequences (k-points) concurrently on one device (chfsi_solve_batch).
+    sequences: list of (get_h(ell) -> column-major Hp tensor, nprob, X tensor). Returns a list of
+    dict(status, lam, resid, reports)."""
+    import torch
+
+    torch.cuda.synchronize(device)
+    count = len(sequences)
+    arr = (Sequence * count)()
+    keep = []
+    outs = []
+    for i, (get_h, nprob, X) in enumerate(sequences):
+        n, k = X.shape
+        xp, ldx = _mat(X, n, k, "X")
+        tensors = {}
+
+        def cb(user, ell, hp_out, ldh_out, get_h=get_h, tensors=tensors, n=n):
+            try:
+                t = get_h(int(ell))
+                p, ld = _mat(t, n, n, "Hp")
+                tensors[int(ell)] = t
+                hp_out[0] = p.value
+                ldh_out[0] = ld
+                return 0
+            except Exception:
+                return 1
+
+        cbf = GET_H(cb)
+        lam = np.zeros(nprob * nev)
+        res = np.zeros(nprob * nev)
+        reps = (Report * nprob)()
+        keep += [cbf, lam, res, reps, tensors]
+        arr[i] = Sequence(nprob, cbf, None, xp.value, ldx, lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                          res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), reps, 0)
+        outs.append((lam, res, reps, nprob))
+    n = sequences[0][2].shape[0]
+    opts = Opts(nev, nex, deg0, deg_cap, max_loops, lanczos_steps, tol, seed, 0, 0, 0)
+    st = lib().chfsi_solve_batch(device, workers, n, ctypes.byref(opts), arr, count)
+    if st not in (0, 3):
+        raise ChfsiError(st, "chfsi_solve_batch failed")
+    return [dict(status=arr[i].status, lam=lam.reshape(nprob, nev), resid=res.reshape(nprob, nev),
+                 reports=[r.as_dict() for r in reps]) for i, (lam, res, reps, nprob) in enumerate(outs)]
 
 
 def filter_flops(n: int, deg) -> float:

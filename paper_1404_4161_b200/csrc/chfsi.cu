@@ -114,14 +114,15 @@ struct Operand {
 //  p == 1: B = local state buffer (nloc x kcols, ld), column coordinate = absolute column.
 //  p > 1 : B = packed [rank][ka][nloc] buffer, column coordinate = column - col0.
 static chfsi_status b_operand(chfsi_ctx ctx, Operand* op, const void* buf, int64_t n_or_nloc, int64_t ld,
-                              int64_t kcols, int64_t col0, int nranks, int box_cols) {
+                              int64_t kcols, int64_t col0, int nranks, int box_cols, int elem = 2) {
   if (nranks == 1) {
     op->b_col0 = (int32_t)col0;
-    return make_tmap_3d(ctx, &op->tm, buf, 2 * n_or_nloc, kcols, 1, 2 * ld, 2 * ld * kcols, box_cols);
+    return make_tmap_3d(ctx, &op->tm, buf, elem * n_or_nloc, kcols, 1, elem * ld, elem * ld * kcols, box_cols);
   }
   op->b_col0 = 0;
   const int64_t ka = kcols - col0;
-  return make_tmap_3d(ctx, &op->tm, buf, 2 * n_or_nloc, ka, nranks, 2 * n_or_nloc, 2 * n_or_nloc * ka, box_cols);
+  return make_tmap_3d(ctx, &op->tm, buf, elem * n_or_nloc, ka, nranks, elem * n_or_nloc, elem * n_or_nloc * ka,
+                      box_cols);
 }
 
 chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
@@ -177,7 +178,7 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
 
 chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
                          void* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c, double e,
-                         bool check_finite) {
+                         bool check_finite, int elem) {
   (void)row0;
   if (k == 0) return CHFSI_OK;
   const int p = ctx->nranks;
@@ -187,24 +188,26 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
   sigma[0] = e / (lambda1 - c);
   for (int i = 1; i < mk; ++i) sigma[i] = 1.0 / (2.0 / sigma[0] - sigma[i - 1]);
 
+  // elem = 2: complex128 (real embedding in K1), elem = 1: real symmetric (NEXT-3); sizes in doubles
+  const size_t eb = 8 * (size_t)elem;  // bytes per element
   const int64_t ldl = round_up(nloc, 2);
-  chfsi_status st = ensure(ctx, ctx->L0, sizeof(double) * 2 * (size_t)ldl * k);
-  if (!st) st = ensure(ctx, ctx->L1, sizeof(double) * 2 * (size_t)ldl * k);
+  chfsi_status st = ensure(ctx, ctx->L0, sizeof(double) * elem * (size_t)ldl * k);
+  if (!st) st = ensure(ctx, ctx->L1, sizeof(double) * elem * (size_t)ldl * k);
   if (!st) st = ensure(ctx, ctx->flag, 64);
-  if (p > 1 && !st) st = ensure(ctx, ctx->R0, sizeof(double) * 2 * (size_t)n * k);
-  if (p > 1 && !st) st = ensure(ctx, ctx->R1, sizeof(double) * 2 * (size_t)n * k);
+  if (p > 1 && !st) st = ensure(ctx, ctx->R0, sizeof(double) * elem * (size_t)n * k);
+  if (p > 1 && !st) st = ensure(ctx, ctx->R1, sizeof(double) * elem * (size_t)n * k);
   if (st) return st;
   double2* L[2] = {static_cast<double2*>(ctx->L0.ptr), static_cast<double2*>(ctx->L1.ptr)};
   double* R[2] = {static_cast<double*>(ctx->R0.ptr), static_cast<double*>(ctx->R1.ptr)};
   int* flag = static_cast<int*>(ctx->flag.ptr);
   if (check_finite) CHFSI_CUDA_TRY(ctx, cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
   // Y_0 -> L0 (the caller's Y is the output and must never be the B operand)
-  CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(L[0], 16 * ldl, Y, 16 * ldy, 16 * nloc, k, cudaMemcpyDeviceToDevice,
+  CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(L[0], eb * ldl, Y, eb * ldy, eb * nloc, k, cudaMemcpyDeviceToDevice,
                                         ctx->stream));
   if (p > 1) {
-    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(R[0] + (size_t)2 * nloc * k * ctx->rank, 16 * nloc, Y, 16 * ldy, 16 * nloc,
-                                          k, cudaMemcpyDeviceToDevice, ctx->stream));
-    st = comm_allgather_inplace(ctx, R[0], (size_t)2 * nloc * k);
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(R[0] + (size_t)elem * nloc * k * ctx->rank, eb * nloc, Y, eb * ldy,
+                                          eb * nloc, k, cudaMemcpyDeviceToDevice, ctx->stream));
+    st = comm_allgather_inplace(ctx, R[0], (size_t)elem * nloc * k);
     if (st) return st;
   }
   CUtensorMap tmA;
@@ -225,25 +228,25 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     int64_t s_next = s;
     while (s_next < k && deg[s_next] <= i + 1) ++s_next;
     const int64_t ka = k - s;
-    TileChoice t = choose_filter_tile(nloc, ka, ctx->num_sms);
+    TileChoice t = elem == 2 ? choose_filter_tile(nloc, ka, ctx->num_sms) : choose_filter_tile_real(nloc, ka, ctx->num_sms);
     if (t.bm != last_bm) {
-      st = make_tmap_2d(ctx, &tmA, Hp, 2 * n, nloc, 2 * ldh, t.bm);
+      st = make_tmap_2d(ctx, &tmA, Hp, elem * n, nloc, elem * ldh, t.bm);
       if (st) return st;
       last_bm = t.bm;
     }
     const int cur = i & 1, oth = cur ^ 1;
     Operand op;
     if (p == 1)
-      st = b_operand(ctx, &op, L[cur], n, ldl, k, s, 1, t.bnc);
+      st = b_operand(ctx, &op, L[cur], n, ldl, k, s, 1, t.bnc, elem);
     else
-      st = b_operand(ctx, &op, R[cur], nloc, nloc, k, s, p, t.bnc);
+      st = b_operand(ctx, &op, R[cur], nloc, nloc, k, s, p, t.bnc, elem);
     if (st) return st;
     StepParams sp{};
     sp.nrows = nloc;
-    const int64_t kr = p == 1 ? 2 * n : 2 * nloc;
+    const int64_t kr = p == 1 ? elem * n : elem * nloc;
     sp.kt_per_rank = (int32_t)((kr + kBK - 1) / kBK);
     sp.num_kt = sp.kt_per_rank * p;
-    sp.a_rank_stride = (int32_t)(2 * nloc);
+    sp.a_rank_stride = (int32_t)(elem * nloc);
     sp.col0 = (int32_t)s;
     sp.col_end = (int32_t)k;
     sp.fin_end = (int32_t)s_next;
@@ -268,7 +271,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     sp.ld_out = ldy;
     const int64_t ka_next = k - s_next;
     if (p > 1 && ka_next > 0) {
-      sp.r_next = reinterpret_cast<double2*>(R[oth] + (size_t)2 * nloc * ka_next * ctx->rank);
+      sp.r_next = reinterpret_cast<double2*>(R[oth] + (size_t)elem * nloc * ka_next * ctx->rank);
       sp.ld_r_next = nloc;
     }
     sp.nonfinite = check_finite ? flag : nullptr;
@@ -281,7 +284,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     nev_used += 2;
     ctx->launches++;
     if (p > 1 && ka_next > 0) {
-      st = comm_allgather_inplace(ctx, R[oth], (size_t)2 * nloc * ka_next);
+      st = comm_allgather_inplace(ctx, R[oth], (size_t)elem * nloc * ka_next);
       if (st) return st;
     }
   }
@@ -312,10 +315,12 @@ using namespace chfsi;
 extern "C" {
 
 static chfsi_status ctx_create_impl(chfsi_ctx* out, int32_t device, void* cuda_stream, void* nccl_comm,
-                                    chfsi_local_group group, int32_t rank, int32_t nranks) {
+                                    chfsi_local_group group, int32_t rank, int32_t nranks,
+                                    const char* nccl_id = nullptr) {
   if (!out) return CHFSI_ERR_ARG;
   *out = nullptr;
-  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_comm && !group)) return CHFSI_ERR_ARG;
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_comm && !group && !nccl_id))
+    return CHFSI_ERR_ARG;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || device < 0 || device >= ndev) {
     cudaGetLastError();
@@ -332,6 +337,10 @@ static chfsi_status ctx_create_impl(chfsi_ctx* out, int32_t device, void* cuda_s
   ctx->num_sms = prop.multiProcessorCount;
   ctx->nccl_comm = nccl_comm;
   ctx->local_group = group;
+  if (nccl_id) {
+    memcpy(ctx->nccl_id, nccl_id, sizeof(ctx->nccl_id));
+    ctx->nccl_id_valid = true;
+  }
   // NULL selects the legacy default stream (stream 0), so work is ordered with the caller's default-
   // stream copies; pass an explicit stream for concurrency.
   ctx->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -355,6 +364,12 @@ static chfsi_status ctx_create_impl(chfsi_ctx* out, int32_t device, void* cuda_s
 chfsi_status chfsi_ctx_create(chfsi_ctx* out, int32_t device, void* cuda_stream, void* nccl_comm, int32_t rank,
                               int32_t nranks) {
   return ctx_create_impl(out, device, cuda_stream, nccl_comm, nullptr, rank, nranks);
+}
+
+chfsi_status chfsi_ctx_create_nccl(chfsi_ctx* out, int32_t device, void* cuda_stream, const char id[128],
+                                   int32_t rank, int32_t nranks) {
+  if (!id) return CHFSI_ERR_ARG;
+  return ctx_create_impl(out, device, cuda_stream, nullptr, nullptr, rank, nranks, id);
 }
 
 chfsi_status chfsi_ctx_create_local(chfsi_ctx* out, int32_t device, void* cuda_stream, chfsi_local_group group,
@@ -400,9 +415,9 @@ const char* chfsi_last_error(chfsi_ctx ctx) { return ctx ? ctx->err.c_str() : "n
 
 int64_t chfsi_kernel_launches(chfsi_ctx ctx) { return ctx ? ctx->launches : 0; }
 
-chfsi_status chfsi_filter(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
-                          void* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c, double e,
-                          int64_t* matvecs) {
+static chfsi_status filter_entry(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
+                                 void* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c,
+                                 double e, int64_t* matvecs, int elem) {
   if (!ctx) return CHFSI_ERR_ARG;
   ctx->err.clear();
   if (n < 1 || nloc < 1 || nloc > n || row0 < 0 || row0 + nloc > n || ldh < n || ldy < nloc || k < 0 ||
@@ -431,9 +446,21 @@ chfsi_status chfsi_filter(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, 
     mv += deg[j];
   }
   if (cudaSetDevice(ctx->device) != cudaSuccess) return CHFSI_ERR_CUDA;
-  chfsi_status st = filter_impl(ctx, n, row0, nloc, Hp, ldh, Y, ldy, k, deg, lambda1, c, e, true);
+  chfsi_status st = filter_impl(ctx, n, row0, nloc, Hp, ldh, Y, ldy, k, deg, lambda1, c, e, true, elem);
   if (st == CHFSI_OK && matvecs) *matvecs = mv;
   return st;
+}
+
+chfsi_status chfsi_filter(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
+                          void* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c, double e,
+                          int64_t* matvecs) {
+  return filter_entry(ctx, n, row0, nloc, Hp, ldh, Y, ldy, k, deg, lambda1, c, e, matvecs, 2);
+}
+
+chfsi_status chfsi_filter_real(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const double* Hp, int64_t ldh,
+                               double* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c,
+                               double e, int64_t* matvecs) {
+  return filter_entry(ctx, n, row0, nloc, Hp, ldh, Y, ldy, k, deg, lambda1, c, e, matvecs, 1);
 }
 
 }  // extern "C"

@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstring>
 #include <vector>
 
 #include "ctx.cuh"
@@ -19,6 +20,7 @@ namespace chfsi {
 struct Comm {
   void* lib = nullptr;
   ncclComm_t comm = nullptr;
+  bool owns_comm = false;  // created by chfsi_ctx_create_nccl
   chfsi_local_group local = nullptr;
   double* scratch = nullptr;  // local-group allreduce accumulator
   size_t scratch_n = 0;
@@ -28,6 +30,19 @@ struct Comm {
   decltype(&ncclGetErrorString) errstr = nullptr;
 };
 
+static void* nccl_lib() {
+  static void* lib = nullptr;
+  if (!lib) {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+      if (!lib) lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (lib) break;
+    }
+  }
+  return lib;
+}
+
 chfsi_status comm_init(chfsi_ctx ctx) {
   if (ctx->nranks == 1) return CHFSI_OK;
   Comm* c = new Comm();
@@ -36,12 +51,7 @@ chfsi_status comm_init(chfsi_ctx ctx) {
     ctx->comm = c;
     return CHFSI_OK;
   }
-  const char* names[] = {"libnccl.so.2", "libnccl.so"};
-  for (const char* nm : names) {
-    c->lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
-    if (!c->lib) c->lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
-    if (c->lib) break;
-  }
+  c->lib = nccl_lib();
   if (!c->lib) {
     set_err(ctx, "NCCL (libnccl.so.2) not found");
     delete c;
@@ -56,13 +66,31 @@ chfsi_status comm_init(chfsi_ctx ctx) {
     delete c;
     return CHFSI_ERR_NCCL;
   }
-  c->comm = static_cast<ncclComm_t>(ctx->nccl_comm);
+  if (ctx->nccl_id_valid) {  // library-owned communicator
+    auto init = reinterpret_cast<decltype(&ncclCommInitRank)>(dlsym(c->lib, "ncclCommInitRank"));
+    ncclUniqueId id;
+    static_assert(sizeof(id) == sizeof(ctx->nccl_id), "ncclUniqueId size");
+    memcpy(&id, ctx->nccl_id, sizeof(id));
+    ncclResult_t r = init ? init(&c->comm, ctx->nranks, id, ctx->rank) : ncclInternalError;
+    if (r != ncclSuccess) {
+      set_err(ctx, std::string("ncclCommInitRank: ") + c->errstr(r));
+      delete c;
+      return CHFSI_ERR_NCCL;
+    }
+    c->owns_comm = true;
+  } else {
+    c->comm = static_cast<ncclComm_t>(ctx->nccl_comm);
+  }
   ctx->comm = c;
   return CHFSI_OK;
 }
 
 void comm_destroy(chfsi_ctx ctx) {
   if (ctx->comm && ctx->comm->scratch) cudaFree(ctx->comm->scratch);
+  if (ctx->comm && ctx->comm->owns_comm && ctx->comm->comm) {
+    auto destroy = reinterpret_cast<decltype(&ncclCommDestroy)>(dlsym(ctx->comm->lib, "ncclCommDestroy"));
+    if (destroy) destroy(ctx->comm->comm);
+  }
   delete ctx->comm;  // the NCCL library handle stays loaded; the communicator belongs to the caller
   ctx->comm = nullptr;
 }
@@ -175,6 +203,17 @@ chfsi_status comm_bcast(chfsi_ctx ctx, double* buf, size_t count, int root) {
 }  // namespace chfsi
 
 extern "C" {
+
+chfsi_status chfsi_nccl_unique_id(char id_out[128]) {
+  if (!id_out) return CHFSI_ERR_ARG;
+  void* lib = chfsi::nccl_lib();
+  auto get = lib ? reinterpret_cast<decltype(&ncclGetUniqueId)>(dlsym(lib, "ncclGetUniqueId")) : nullptr;
+  if (!get) return CHFSI_ERR_NCCL;
+  ncclUniqueId id;
+  if (get(&id) != ncclSuccess) return CHFSI_ERR_NCCL;
+  memcpy(id_out, &id, sizeof(id));
+  return CHFSI_OK;
+}
 
 chfsi_status chfsi_local_group_create(chfsi_local_group* out, int32_t nranks) {
   if (!out || nranks < 1) return CHFSI_ERR_ARG;

@@ -55,6 +55,8 @@ struct chfsi_ctx_s {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   void* nccl_comm = nullptr;
+  char nccl_id[128] = {0};     // ncclUniqueId for a library-owned communicator
+  bool nccl_id_valid = false;
   chfsi_local_group local_group = nullptr;
   chfsi::Comm* comm = nullptr;
   cublasHandle_t cublas = nullptr;
@@ -109,7 +111,7 @@ chfsi_status comm_bcast(chfsi_ctx ctx, double* buf, size_t count, int root);
 // internal (no status marshalling) versions of the public entry points, used by the solver
 chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
                          void* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c, double e,
-                         bool check_finite);
+                         bool check_finite, int elem = 2);
 // HQ: out (nloc x k) = H Q for Q (nloc x k, this rank's rows). Uses the K1 kernel, plain epilogue.
 chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
                        const void* Q, int64_t ldq, int64_t k, void* out, int64_t ldo);

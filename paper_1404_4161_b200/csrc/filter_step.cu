@@ -7,11 +7,11 @@ namespace chfsi {
 
 namespace {
 
-template <int BM, int BNC, int WM, int WNC, int STAGES>
+template <int BM, int BNC, int WM, int WNC, int STAGES, bool CPLX = true>
 cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, const StepParams& p,
                        cudaStream_t stream) {
-  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES>;
-  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES>;
+  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>;
+  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, CPLX>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
@@ -33,7 +33,7 @@ constexpr Variant kVariants[] = {
     {64, 64, 16, 0.920, 256, 32},   // 1: 8 warps, warp tile 32 x 16
     {128, 64, 32, 0.940, 256, 64},  // 2: 8 warps, warp tile 32 x 32
     {64, 32, 16, 0.700, 128, 32},   // 3: 4 warps
-    {128, 64, 16, 0.970, 512, 32},  // 4: 16 warps (4 per SMSP), warp tile 32 x 16
+    {128, 64, 16, 0.950, 512, 32},  // 4: 16 warps (4 per SMSP), warp tile 32 x 16
     {128, 16, 16, 0.800, 256, 16},  // 5: 8 warps, warp tile 16 x 16 (narrow blocks)
     {128, 32, 8, 0.960, 512, 16},   // 6: 16 warps, warp tile 32 x 8
     {128, 48, 16, 1.000, 384, 32},  // 7: 12 warps, warp tile 32 x 16 (34.9 TF/s at n=13000, k=624)
@@ -56,7 +56,7 @@ TileChoice choose_filter_tile(int64_t nrows, int64_t ncols, int num_sms) {
   for (int v = 0; v < nvar; ++v) {
     const int64_t tm = (nrows + kVariants[v].bm - 1) / kVariants[v].bm;
     // balanced N split in warp-tile units: every tile has `per` active warp columns; idle warps skip
-    // their MMAs but are not free (model: halfway between free and full cost), and fewer than two
+    // their MMAs but are not free (model: 30 % of full cost), and fewer than two
     // active warps per SM sub-partition lose latency hiding (profiles/r01_filter_variants)
     const Variant& V = kVariants[v];
     const int64_t units = (ncols + V.wnc - 1) / V.wnc;
@@ -65,7 +65,7 @@ TileChoice choose_filter_tile(int64_t nrows, int64_t ncols, int num_sms) {
     const int warps_m = V.threads / 32 / (V.bnc / V.wnc);
     const double active_warps = (double)per * warps_m;
     const double occ = active_warps >= 8 ? 1.0 : 0.6 + 0.05 * active_warps;
-    const double cols = 0.5 * (double)(tn * per * V.wnc) + 0.5 * (double)ncols;
+    const double cols = 0.3 * (double)(tn * per * V.wnc) + 0.7 * (double)ncols;
     const double cost = (double)tm * V.bm * cols / (V.eff * occ);
     if (cost < best_cost * 0.999) {
       best_cost = cost;
@@ -75,6 +75,34 @@ TileChoice choose_filter_tile(int64_t nrows, int64_t ncols, int num_sms) {
   (void)num_sms;
   return TileChoice{best, kVariants[best].bm, kVariants[best].bnc, kVariants[best].threads, kVariants[best].acc,
                     kVariants[best].wnc};
+}
+
+TileChoice choose_filter_tile_real(int64_t nrows, int64_t ncols, int num_sms) {
+  (void)num_sms;
+  struct RV {
+    int id, bm, bnc, wnc, threads, acc;
+    double eff;
+  };
+  static const RV rv[] = {{100, 128, 96, 32, 384, 32, 1.0}, {101, 128, 64, 32, 256, 32, 0.97},
+                          {102, 128, 32, 16, 256, 16, 0.93}};
+  const char* fs = getenv("CHFSI_FILTER_VARIANT_REAL");
+  const int forced = fs ? atoi(fs) : -1;
+  int best = 0;
+  double best_cost = 1e300;
+  for (int v = 0; v < 3; ++v) {
+    if (forced >= 0 && rv[v].id != forced) continue;
+    const int64_t tm = (nrows + rv[v].bm - 1) / rv[v].bm;
+    const int64_t units = (ncols + rv[v].wnc - 1) / rv[v].wnc;
+    const int64_t tn = (ncols + rv[v].bnc - 1) / rv[v].bnc;
+    const int64_t per = (units + tn - 1) / tn;
+    const double cols = 0.3 * (double)(tn * per * rv[v].wnc) + 0.7 * (double)ncols;
+    const double cost = (double)tm * rv[v].bm * cols / rv[v].eff;
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = v;
+    }
+  }
+  return TileChoice{rv[best].id, rv[best].bm, rv[best].bnc, rv[best].threads, rv[best].acc, rv[best].wnc};
 }
 
 void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
@@ -112,6 +140,13 @@ cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, cons
       return launch_cfg<128, 32, 32, 8, 5>(tmA, tmB, p, stream);
     case 7:
       return launch_cfg<128, 48, 32, 16, 4>(tmA, tmB, p, stream);
+    // real symmetric (columns are real columns)
+    case 100:
+      return launch_cfg<128, 96, 32, 32, 3, false>(tmA, tmB, p, stream);
+    case 101:
+      return launch_cfg<128, 64, 32, 32, 4, false>(tmA, tmB, p, stream);
+    case 102:
+      return launch_cfg<128, 32, 32, 16, 5, false>(tmA, tmB, p, stream);
     default:
       return cudaErrorInvalidValue;
   }

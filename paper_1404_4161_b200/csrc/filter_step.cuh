@@ -54,19 +54,21 @@ constexpr int kBKHalf = 16;            // doubles per 128-byte swizzle row
 constexpr int kHalves = 2;             // two swizzle rows per stage -> 32 real K per stage
 constexpr int kBK = kBKHalf * kHalves;  // real K per stage
 
-template <int BM, int BNC, int WM, int WNC, int STAGES>
+// CPLX: complex Hermitian (BNC, WNC count complex columns; real embedding with B'' in registers) or
+// real symmetric (BNC, WNC count real columns, a plain real GEMM).
+template <int BM, int BNC, int WM, int WNC, int STAGES, bool CPLX = true>
 struct FilterCfg {
   static constexpr int kWarpsM = BM / WM;
   static constexpr int kWarpsN = BNC / WNC;
   static constexpr int kConsumerWarps = kWarpsM * kWarpsN;
   static constexpr int kThreads = kConsumerWarps * 32;  // thread 0 doubles as the TMA producer
   static constexpr int kMT = WM / 8;   // 8-row MMA tiles per warp
-  static constexpr int kNT = WNC / 4;  // 8-real-column (4 complex) MMA tiles per warp
+  static constexpr int kNT = CPLX ? WNC / 4 : WNC / 8;  // 8-real-column MMA tiles per warp
   static constexpr int kABytes = kHalves * BM * 128;
   static constexpr int kBBytes = kHalves * BNC * 128;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kSmemBytes = STAGES * kStageBytes + 2 * STAGES * 8 + 1024;  // + barriers + align
-  static_assert(WM % 8 == 0 && WNC % 4 == 0 && BM % WM == 0 && BNC % WNC == 0, "tile shape");
+  static_assert(WM % 8 == 0 && WNC % (CPLX ? 4 : 8) == 0 && BM % WM == 0 && BNC % WNC == 0, "tile shape");
   static_assert(BM <= 256 && BNC <= 256, "TMA box limit");
 };
 
@@ -99,11 +101,11 @@ __device__ __forceinline__ double xor_sign(double x, uint32_t mask) {
   return __hiloint2double(hi, __double2loint(x));
 }
 
-template <int BM, int BNC, int WM, int WNC, int STAGES>
-__global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES>::kThreads, 1)
+template <int BM, int BNC, int WM, int WNC, int STAGES, bool CPLX = true>
+__global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>::kThreads, 1)
     filter_step_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const StepParams p) {
-  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES>;
+  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>;
   constexpr int kAcc = Cfg::kMT * Cfg::kNT * 2;  // accumulator doubles per thread
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align to 1024 B (128B-swizzle atoms) by pointer arithmetic on the shared array, so the compiler
@@ -216,24 +218,46 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES>::kThreads,
   const bool odd = (g & 1);  // this lane feeds an imaginary-part (B'') column
   const uint32_t sign_mask = odd ? 0x80000000u : 0u;
   const int a_row0 = wm * WM + g;
-  const int b_row0 = wn * WNC + (lane >> 3);
+  // B smem row of this lane's first MMA column: complex -> complex column (lane >> 3), the lane pair
+  // (2c, 2c+1) building (B', B''); real -> real column g
+  const int b_row0 = CPLX ? wn * WNC + (lane >> 3) : wn * WNC + g;
   bool bad = false;
 
   double acc[Cfg::kMT][Cfg::kNT][2];
 
   // fused epilogue: three-term recurrence, degree masking, finished-column store
+  auto store_val = [&](int col, int64_t r, double v) {  // real: one value of column col
+    const double* yc = reinterpret_cast<const double*>(p.y_cur);
+    const double* yp = reinterpret_cast<const double*>(p.y_prev);
+    if (p.flags & 1) v -= p.c * yc[(int64_t)col * p.ld_cur + r];
+    v *= p.a;
+    if (p.flags & 2) v -= p.b * yp[(int64_t)col * p.ld_prev + r];
+    bad |= !isfinite(v);
+    if (col < p.fin_end) {
+      reinterpret_cast<double*>(p.out)[(int64_t)col * p.ld_out + r] = v;
+    } else {
+      reinterpret_cast<double*>(p.y_next)[(int64_t)col * p.ld_next + r] = v;
+      if (p.r_next) reinterpret_cast<double*>(p.r_next)[(int64_t)(col - p.fin_end) * p.ld_r_next + r] = v;
+    }
+  };
   auto epilogue = [&](int tile) {
     const int m0 = (tile / p.tiles_n) * BM;
     int nu;
     const int c0 = tile_cols(tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
     if (wn >= nu) return;  // this warp's columns belong to the next tile
-    const int col_base = p.col0 + c0 + wn * WNC + qd;
+    const int col_base = p.col0 + c0 + wn * WNC + (CPLX ? qd : 2 * qd);
 #pragma unroll
     for (int i = 0; i < Cfg::kMT; ++i) {
       const int64_t r = (int64_t)m0 + wm * WM + i * 8 + g;
       if (r >= p.nrows) continue;
 #pragma unroll
       for (int j = 0; j < Cfg::kNT; ++j) {
+        if constexpr (!CPLX) {
+          const int col = col_base + j * 8;
+          if (col < p.col_end) store_val(col, r, acc[i][j][0]);
+          if (col + 1 < p.col_end) store_val(col + 1, r, acc[i][j][1]);
+          continue;
+        }
         const int col = col_base + j * 4;
         if (col >= p.col_end) continue;
         double vr = acc[i][j][0], vi = acc[i][j][1];
@@ -302,11 +326,15 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES>::kThreads,
           for (int i = 0; i < Cfg::kMT; ++i) av[i] = *reinterpret_cast<const double2*>(ah + swz(a_row0 + i * 8, chunk));
 #pragma unroll
           for (int jj = 0; jj < Cfg::kNT; ++jj) {
-            // B' (even g): (re, im) as stored; B'' (odd g): (im, -re) -- two lane-offset LDS.64 do the
-            // swap, one integer XOR the sign (no select, no FP64 op)
-            const double* y = reinterpret_cast<const double*>(bh + swz(b_row0 + jj * 4, chunk));
-            bv[jj].x = y[odd ? 1 : 0];
-            bv[jj].y = xor_sign(y[odd ? 0 : 1], sign_mask);
+            if constexpr (CPLX) {
+              // B' (even g): (re, im) as stored; B'' (odd g): (im, -re) -- two lane-offset LDS.64 do the
+              // swap, one integer XOR the sign (no select, no FP64 op)
+              const double* y = reinterpret_cast<const double*>(bh + swz(b_row0 + jj * 4, chunk));
+              bv[jj].x = y[odd ? 1 : 0];
+              bv[jj].y = xor_sign(y[odd ? 0 : 1], sign_mask);
+            } else {
+              bv[jj] = *reinterpret_cast<const double2*>(bh + swz(b_row0 + jj * 8, chunk));
+            }
           }
 #pragma unroll
           for (int i = 0; i < Cfg::kMT; ++i)
@@ -394,5 +422,7 @@ void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p);
 size_t filter_partials_doubles(const TileChoice& t, int num_sms);
 cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, const CUtensorMap& tmB,
                                const StepParams& p, cudaStream_t stream);
+// real-symmetric variants (ids >= 100)
+TileChoice choose_filter_tile_real(int64_t nrows, int64_t ncols, int num_sms);
 
 }  // namespace chfsi

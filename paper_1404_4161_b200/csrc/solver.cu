@@ -3,8 +3,10 @@
 // O(n k^2) step runs on the device (filter K1, H Q K1, CholQR2, Rayleigh-Ritz, residuals); the
 // host only keeps O(k) bookkeeping (Ritz values, residuals, degrees, lock decisions).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <numeric>
+#include <thread>
 #include <vector>
 
 #include "ctx.cuh"
@@ -122,7 +124,7 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
     lam1 = lam1_io;
     alpha = lamk_io;
   }
-  std::vector<int32_t> m(k, o.deg0), ms(k);
+  std::vector<int32_t> m(k, o.fixed_degree > 0 ? o.fixed_degree : o.deg0), ms(k);
   int64_t nl = 0;
   chfsi_status status = CHFSI_ERR_NOCONV;
   while (rep.loops < o.max_loops) {
@@ -195,6 +197,11 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
       break;
     }
     // Alg 1 l11 (R21, R5, R9): degrees for the next filter
+    if (o.fixed_degree > 0) {  // ablation: no Single Optimisation
+      for (int64_t j = 0; j < na; ++j) m[j] = o.fixed_degree;
+      tm.end(T_OPT, t6);
+      continue;
+    }
     const double c2 = 0.5 * (alpha + beta), e2 = 0.5 * (beta - alpha);
     const int64_t want2 = nev - nl;
     int32_t mmax = 1;
@@ -270,7 +277,8 @@ extern "C" chfsi_status chfsi_solve_sequence(chfsi_ctx ctx, int64_t n, int64_t r
   const chfsi_opts& o = *opts;
   const int64_t k = (int64_t)o.nev + o.nex;
   if (o.nev < 1 || o.nex < 0 || k > n || !(o.tol > 0) || o.deg0 < 1 || o.deg0 > o.deg_cap ||
-      o.deg_cap > CHFSI_MAX_DEGREE || o.max_loops < 1 || o.lanczos_steps < 1 ||
+      o.deg_cap > CHFSI_MAX_DEGREE || o.max_loops < 1 || o.lanczos_steps < 1 || o.fixed_degree < 0 ||
+      o.fixed_degree > CHFSI_MAX_DEGREE ||
       (ctx->nranks > 1 && (nloc * ctx->nranks != n || row0 != nloc * ctx->rank))) {
     set_err(ctx, "chfsi_solve_sequence: bad options (need 0 < nev, nev + nex <= n, tol > 0, 1 <= deg0 <= cap <= 64)");
     return CHFSI_ERR_ARG;
@@ -290,8 +298,13 @@ extern "C" chfsi_status chfsi_solve_sequence(chfsi_ctx ctx, int64_t n, int64_t r
       set_err(ctx, "chfsi_solve_sequence: get_h failed for problem " + std::to_string(ell));
       return CHFSI_ERR_ARG;
     }
+    if (o.no_reuse && ell > 0) {  // ablation: a fresh random block instead of the hand-off
+      CHFSI_CUDA_TRY(ctx, launch_random_block(nloc, k, row0, o.seed + (uint64_t)ell, 3ull << 16, 1, Xd, ldx,
+                                              ctx->stream));
+      ctx->launches++;
+    }
     chfsi_report rep{};
-    chfsi_status st = solve_one(ctx, n, row0, nloc, Hp, ldh, o, Xd, ldx, ell > 0, lam1, lamk,
+    chfsi_status st = solve_one(ctx, n, row0, nloc, Hp, ldh, o, Xd, ldx, ell > 0 && !o.no_reuse, lam1, lamk,
                                 lambda + (size_t)ell * o.nev, resid ? resid + (size_t)ell * o.nev : nullptr, rep,
                                 o.seed + (uint64_t)ell);
     if (reports) reports[ell] = rep;
@@ -303,4 +316,40 @@ extern "C" chfsi_status chfsi_solve_sequence(chfsi_ctx ctx, int64_t n, int64_t r
   }
   if (worst == CHFSI_ERR_NOCONV) set_err(ctx, "ChFSI: at least one problem hit max_loops");
   return worst;
+}
+
+extern "C" chfsi_status chfsi_solve_batch(int32_t device, int32_t workers, int64_t n, const chfsi_opts* opts,
+                                          chfsi_sequence* seqs, int32_t count) {
+  if (!opts || !seqs || count < 0 || workers < 1 || n < 1) return CHFSI_ERR_ARG;
+  if (count == 0) return CHFSI_OK;
+  workers = std::min(workers, count);
+  std::vector<chfsi_ctx> ctxs(workers, nullptr);
+  std::vector<cudaStream_t> streams(workers, nullptr);
+  chfsi_status st = CHFSI_OK;
+  if (cudaSetDevice(device) != cudaSuccess) return CHFSI_ERR_CUDA;
+  for (int w = 0; w < workers && !st; ++w) {
+    if (cudaStreamCreateWithFlags(&streams[w], cudaStreamNonBlocking) != cudaSuccess) st = CHFSI_ERR_CUDA;
+    if (!st) st = chfsi_ctx_create(&ctxs[w], device, streams[w], nullptr, 0, 1);
+  }
+  if (!st) {
+    std::atomic<int> next{0};
+    std::vector<std::thread> th;
+    for (int w = 0; w < workers; ++w)
+      th.emplace_back([&, w] {
+        cudaSetDevice(device);
+        for (int s = next++; s < count; s = next++) {
+          chfsi_sequence& q = seqs[s];
+          q.status = chfsi_solve_sequence(ctxs[w], n, 0, n, q.nprob, q.get_h, q.user, opts, q.X, q.ldx, q.lambda,
+                                          q.resid, q.reports);
+        }
+      });
+    for (auto& t : th) t.join();
+    for (int s = 0; s < count; ++s)
+      if (seqs[s].status != CHFSI_OK && (st == CHFSI_OK || st == CHFSI_ERR_NOCONV)) st = seqs[s].status;
+  }
+  for (int w = 0; w < workers; ++w) {
+    if (ctxs[w]) chfsi_ctx_destroy(ctxs[w]);
+    if (streams[w]) cudaStreamDestroy(streams[w]);
+  }
+  return st;
 }

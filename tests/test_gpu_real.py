@@ -1,0 +1,101 @@
+"""NEXT-3: the real-symmetric filter (chfsi_filter_real) against the oracle (Alg 2 in complex
+arithmetic on real data computes the real recurrence exactly: every imaginary part is 0) and against
+the diagonal closed form; all real tile variants, ragged shapes, and the emulated multi-rank path."""
+import os
+
+import numpy as np
+import pytest
+
+import gen as G
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=["100", "101", "102"])
+def rvariant(request):
+    os.environ["CHFSI_FILTER_VARIANT_REAL"] = request.param
+    yield request.param
+    os.environ.pop("CHFSI_FILTER_VARIANT_REAL", None)
+
+
+def real_sym(n, seed):
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((n, n)) / np.sqrt(2 * n)
+    return np.asfortranarray(A + A.T)  # spectrum ~ [-2, 2]
+
+
+@pytest.mark.parametrize("n,k", [(300, 37), (517, 100), (129, 5)])
+def test_filter_real_vs_oracle(gpu_lib, rvariant, n, k):
+    H = real_sym(n, n)
+    rng = np.random.default_rng(k)
+    deg = sorted(rng.integers(1, 25, k).tolist())
+    Y0 = np.asfortranarray(rng.standard_normal((n, k)))
+    l1, a, b = -2.3, -1.0, 2.3
+    c, e = (a + b) / 2, (b - a) / 2
+    ctx = gpu_lib.Context(0)
+    Yd = gpu_lib.to_colmajor(Y0, real=True)
+    assert ctx.filter_real(gpu_lib.to_colmajor(H, real=True), Yd, deg, l1, c, e) == sum(deg)
+    Y = Yd.cpu().numpy()
+    ctx.close()
+    Yo, _ = O.chebyshev_filter(H.astype(complex), Y0.astype(complex), deg, l1, c, e)
+    assert np.abs(Yo.imag).max() == 0.0
+    rel = np.linalg.norm(Y - Yo.real, axis=0) / np.linalg.norm(Yo.real, axis=0)
+    assert rel.max() <= 1e-11
+
+
+def test_filter_real_diag_closed_form(gpu_lib):
+    rng = np.random.default_rng(3)
+    n = 211
+    d = np.sort(rng.uniform(-2.0, 40.0, n))
+    deg = sorted(rng.integers(1, 41, 29).tolist())
+    Y0 = rng.standard_normal((n, 29))
+    l1, a, b = -2.3, -1.2, 40.5
+    c, e = (a + b) / 2, (b - a) / 2
+    ctx = gpu_lib.Context(0)
+    Yd = gpu_lib.to_colmajor(Y0, real=True)
+    ctx.filter_real(gpu_lib.to_colmajor(np.diag(d), real=True), Yd, deg, l1, c, e)
+    Y = Yd.cpu().numpy()
+    ctx.close()
+    Yc = O.filter_diag_closed(d, Y0.astype(complex), deg, l1, c, e).real
+    assert (np.linalg.norm(Y - Yc, axis=0) / np.linalg.norm(Yc, axis=0)).max() <= 1e-13
+
+
+def test_filter_real_multirank(gpu_lib):
+    import threading
+
+    import torch
+
+    n, P, k = 640, 4, 21
+    H = real_sym(n, 11)
+    rng = np.random.default_rng(5)
+    deg = sorted(rng.integers(1, 15, k).tolist())
+    Y0 = rng.standard_normal((n, k))
+    l1, c, e = -2.3, 0.65, 1.65
+    nloc = n // P
+    g = gpu_lib.LocalGroup(P)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    ctxs = [gpu_lib.Context(0, stream=streams[r], local_group=g, rank=r) for r in range(P)]
+    Hs = [gpu_lib.to_colmajor(np.asfortranarray(H[:, r * nloc:(r + 1) * nloc]), real=True) for r in range(P)]
+    Ys = [gpu_lib.to_colmajor(Y0[r * nloc:(r + 1) * nloc], real=True) for r in range(P)]
+    torch.cuda.synchronize()
+    errs = []
+
+    def work(r):
+        try:
+            with torch.cuda.stream(streams[r]):
+                ctxs[r].filter_real(Hs[r], Ys[r], deg, l1, c, e, n=n, row0=r * nloc)
+                streams[r].synchronize()
+        except Exception as ex:
+            errs.append(ex)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    torch.cuda.synchronize()
+    [cx.close() for cx in ctxs]
+    g.close()
+    assert not errs, errs
+    Y = np.concatenate([y.cpu().numpy() for y in Ys], axis=0)
+    Yo, _ = O.chebyshev_filter(H.astype(complex), Y0.astype(complex), deg, l1, c, e)
+    assert (np.linalg.norm(Y - Yo.real, axis=0) / np.linalg.norm(Yo.real, axis=0)).max() <= 1e-11

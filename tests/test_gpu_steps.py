@@ -215,3 +215,54 @@ def test_solve_c1_sequence(gpu_lib, ctx):
     assert res.max() <= cf["tol"] * 1.01
     loops = [r["loops"] for r in out["reports"]]
     assert all(l <= loops[0] for l in loops[1:])  # reuse of the previous eigenvectors pays
+
+
+def test_ablation_options(gpu_lib, ctx):
+    """NEXT-2 ablations: no_reuse restarts every problem from a random block; fixed_degree filters every
+    vector with one degree (no Single Optimisation). Both still converge to the exact spectrum."""
+    n, nd, nev, nex, delta, seed = 320, 272, 16, 8, 1e-3, 77
+    w = G.wy(n, nd, seed)
+    H = w.full()
+    Hs = []
+    for ell in range(3):
+        if ell > 0:
+            G.perturb(H, seed, ell, delta * HNORM)
+        Hs.append(gpu_lib.to_colmajor(H))
+    X0 = G.start_basis(n, nev + nex, seed)
+    outs = {}
+    for label, kw in (("base", {}), ("random", dict(no_reuse=True)), ("fixed", dict(fixed_degree=12))):
+        Xd = gpu_lib.to_colmajor(X0)
+        outs[label] = ctx.solve_sequence(lambda ell: Hs[ell], 3, Xd, nev, nex, 1e-10, deg_cap=30, seed=seed,
+                                         max_loops=200, **kw)
+        assert outs[label]["status"] == 0
+        ev = np.linalg.eigvalsh(Hs[-1].cpu().numpy())[:nev]
+        assert np.max(np.abs(outs[label]["lam"][-1] - ev) / np.abs(ev)) <= 1e-10
+    # reuse pays: the random-start arm needs more filter work on the later problems
+    base, rnd = outs["base"]["reports"], outs["random"]["reports"]
+    assert sum(r["matvecs_filter"] for r in rnd[1:]) > sum(r["matvecs_filter"] for r in base[1:])
+    # fixed degree: every filter call uses degree 12 for every vector
+    for r in outs["fixed"]["reports"]:
+        assert r["matvecs_filter"] % 12 == 0
+
+
+def test_solve_batch_independent_sequences(gpu_lib, ctx):
+    """NEXT-4: independent k-point sequences solved concurrently (chfsi_solve_batch, 2 workers on one
+    device) give the same results as solving each sequence alone."""
+    n, nd, nev, nex = 384, 340, 12, 6
+    seqs, serial = [], []
+    for s in range(3):
+        w = G.wy(n, nd, 100 + s)
+        H = w.full()
+        Hs = [gpu_lib.to_colmajor(H)]
+        G.perturb(H, 100 + s, 1, 1e-3 * HNORM)
+        Hs.append(gpu_lib.to_colmajor(H))
+        X0 = G.start_basis(n, nev + nex, 100 + s)
+        Xd = gpu_lib.to_colmajor(X0)
+        serial.append(ctx.solve_sequence(lambda ell, Hs=Hs: Hs[ell], 2, Xd, nev, nex, 1e-10, deg_cap=24, seed=7))
+        seqs.append((lambda ell, Hs=Hs: Hs[ell], 2, gpu_lib.to_colmajor(X0)))
+        np.testing.assert_allclose(serial[-1]["lam"][0], w.lam[:nev], rtol=1e-10)
+    outs = gpu_lib.solve_batch(0, 2, seqs, nev, nex, 1e-10, deg_cap=24, seed=7)
+    for o, s in zip(outs, serial):
+        assert o["status"] == 0
+        np.testing.assert_allclose(o["lam"], s["lam"], rtol=1e-13)
+        assert [r["loops"] for r in o["reports"]] == [r["loops"] for r in s["reports"]]

@@ -9,26 +9,31 @@ def main():
     ks = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "624").split(",")]
     m = int(sys.argv[3]) if len(sys.argv) > 3 else 4
     variants = (sys.argv[4] if len(sys.argv) > 4 else "0,1,2,3,auto").split(",")
+    real = len(sys.argv) > 5 and sys.argv[5] == "real"
+    dt = torch.float64 if real else torch.complex128
+    env = "CHFSI_FILTER_VARIANT_REAL" if real else "CHFSI_FILTER_VARIANT"
     torch.manual_seed(0)
-    H = chfsi.colmajor(n, n)
-    H.copy_(torch.randn(n, n, dtype=torch.complex128, device="cuda") / (2 * n) ** 0.5)
+    H = chfsi.colmajor(n, n, dtype=dt)
+    H.copy_(torch.randn(n, n, dtype=dt, device="cuda") / (2 * n) ** 0.5)
     ctx = chfsi.Context(0)
+    filt = ctx.filter_real if real else ctx.filter
     for k in ks:
-        Y0 = chfsi.colmajor(n, k); Y0.copy_(torch.randn(n, k, dtype=torch.complex128, device="cuda"))
-        Y = chfsi.colmajor(n, k)
+        Y0 = chfsi.colmajor(n, k, dtype=dt); Y0.copy_(torch.randn(n, k, dtype=dt, device="cuda"))
+        Y = chfsi.colmajor(n, k, dtype=dt)
         deg = [m] * k
         for v in variants:
-            if v == "auto": os.environ.pop("CHFSI_FILTER_VARIANT", None)
-            else: os.environ["CHFSI_FILTER_VARIANT"] = v
-            Y.copy_(Y0); ctx.filter(H, Y, deg, -2.2, 0.6, 1.6)
+            if v == "auto": os.environ.pop(env, None)
+            else: os.environ[env] = v
+            Y.copy_(Y0); filt(H, Y, deg, -2.2, 0.6, 1.6)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
             best = 1e30
             for _ in range(3):
                 Y.copy_(Y0)
-                e0.record(); ctx.filter(H, Y, deg, -2.2, 0.6, 1.6); e1.record(); torch.cuda.synchronize()
+                e0.record(); filt(H, Y, deg, -2.2, 0.6, 1.6); e1.record(); torch.cuda.synchronize()
                 best = min(best, e0.elapsed_time(e1))
-            fl = 8.0 * n * n * k * m
-            print(json.dumps({"n": n, "k": k, "m": m, "variant": v, "ms": best, "tflops": fl / best / 1e9}), flush=True)
+            fl = (2.0 if real else 8.0) * n * n * k * m
+            print(json.dumps({"n": n, "k": k, "m": m, "variant": v, "real": real, "ms": best,
+                              "tflops": fl / best / 1e9}), flush=True)
 
 main()
