@@ -193,6 +193,15 @@ chfsi_status chfsi_solve_sequence(chfsi_ctx ctx, int64_t n, int64_t row0, int64_
                                   const chfsi_opts* opts, void* X, int64_t ldx, double* lambda,
                                   double* resid, chfsi_report* reports);
 
+/* Real-symmetric ChFSI on a sequence: chfsi_solve_sequence for real
+ * symmetric H (double, get_h returns the real column slab) and a real block X (double). Same options,
+ * outputs and errors; the filter runs chfsi_filter_real's kernel, the supporting steps their real
+ * (DGEMM / DPOTRF / DSYEVD / DGEQRF) counterparts; report filter_flops counts 2 n^2 sum(deg). */
+chfsi_status chfsi_solve_sequence_real(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc,
+                                       int32_t nprob, chfsi_get_h get_h, void* user,
+                                       const chfsi_opts* opts, double* X, int64_t ldx, double* lambda,
+                                       double* resid, chfsi_report* reports);
+
 /* Independent sequences: the N_k k-point sequences of one SCF cycle are
  * independent eigenproblem sequences. chfsi_solve_batch solves `count` of them
  * concurrently on one device with `workers` library contexts, each on its own CUDA stream and host

@@ -27,7 +27,7 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_NOCONV", 4: "ERR_QR
 EXPORTS = ("chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_ctx_create_nccl", "chfsi_nccl_unique_id", "chfsi_ctx_reserve", "chfsi_ctx_destroy",
            "chfsi_last_error", "chfsi_kernel_launches", "chfsi_local_group_create", "chfsi_local_group_destroy",
            "chfsi_filter", "chfsi_filter_real", "chfsi_lanczos_bounds", "chfsi_qr", "chfsi_rayleigh_ritz", "chfsi_solve_sequence",
-           "chfsi_reduce_generalized", "chfsi_back_transform", "chfsi_solve_batch")
+           "chfsi_reduce_generalized", "chfsi_back_transform", "chfsi_solve_batch", "chfsi_solve_sequence_real")
 
 
 class ChfsiError(RuntimeError):
@@ -106,6 +106,8 @@ def lib():
                                            ctypes.POINTER(Report)]
         L.chfsi_reduce_generalized.argtypes = [vp, i64, vp, i64, vp, i64]
         L.chfsi_back_transform.argtypes = [vp, i64, vp, i64, vp, i64, i64]
+        L.chfsi_solve_sequence_real.argtypes = L.chfsi_solve_sequence.argtypes
+        L.chfsi_solve_sequence_real.restype = ctypes.c_int
         L.chfsi_solve_batch.argtypes = [i32, i32, i64, ctypes.POINTER(Opts), ctypes.POINTER(Sequence), i32]
         for name in ("chfsi_solve_batch", "chfsi_reduce_generalized", "chfsi_back_transform", "chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_local_group_create", "chfsi_ctx_reserve", "chfsi_filter", "chfsi_lanczos_bounds", "chfsi_qr",
                      "chfsi_rayleigh_ritz", "chfsi_solve_sequence"):
@@ -301,19 +303,20 @@ class Context:
 
     # -- Alg 1 over a sequence ----------------------------------------------------------------------
     def solve_sequence(self, get_h, nprob, X, nev, nex, tol, deg_cap=40, deg0=8, max_loops=50, lanczos_steps=25,
-                       seed=0, random_start=False, n=None, row0=0, no_reuse=False, fixed_degree=0):
+                       seed=0, random_start=False, n=None, row0=0, no_reuse=False, fixed_degree=0, real=False):
         """get_h(ell) -> column-major CUDA tensor Hp (n x nloc) of problem ell (kept alive by the caller
-        until the next call). Returns dict(status, lam (nprob x nev), resid, reports)."""
+        until the next call). real=True: real symmetric H and X (float64; chfsi_solve_sequence_real).
+        Returns dict(status, lam (nprob x nev), resid, reports)."""
         nloc, k = X.shape
         assert k == nev + nex
         n = n or nloc
-        xp, ldx = _mat(X, nloc, k, "X")
+        xp, ldx = _mat(X, nloc, k, "X", real=real)
         keep = {}
 
         def cb(user, ell, hp_out, ldh_out):
             try:
                 t = get_h(int(ell))
-                p, ld = _mat(t, n, nloc, "Hp")
+                p, ld = _mat(t, n, nloc, "Hp", real=real)
                 keep["h"] = t
                 hp_out[0] = p.value
                 ldh_out[0] = ld
@@ -328,7 +331,8 @@ class Context:
         lam = np.zeros(nprob * nev)
         res = np.zeros(nprob * nev)
         reps = (Report * nprob)()
-        st = lib().chfsi_solve_sequence(self.h, n, row0, nloc, nprob, cbf, None, ctypes.byref(opts), xp, ldx,
+        fn = lib().chfsi_solve_sequence_real if real else lib().chfsi_solve_sequence
+        st = fn(self.h, n, row0, nloc, nprob, cbf, None, ctypes.byref(opts), xp, ldx,
                                         lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                         res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), reps)
         if "exc" in keep:

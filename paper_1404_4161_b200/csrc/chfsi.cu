@@ -119,45 +119,64 @@ static chfsi_status b_operand(chfsi_ctx ctx, Operand* op, const void* buf, int64
     op->b_col0 = (int32_t)col0;
     return make_tmap_3d(ctx, &op->tm, buf, elem * n_or_nloc, kcols, 1, elem * ld, elem * ld * kcols, box_cols);
   }
+  // packed [rank][ka][ld] (ld = nloc, rounded up to an even count for real data: TMA strides are
+  // multiples of 16 bytes)
   op->b_col0 = 0;
   const int64_t ka = kcols - col0;
-  return make_tmap_3d(ctx, &op->tm, buf, elem * n_or_nloc, ka, nranks, elem * n_or_nloc, elem * n_or_nloc * ka,
-                      box_cols);
+  return make_tmap_3d(ctx, &op->tm, buf, elem * n_or_nloc, ka, nranks, elem * ld, elem * ld * ka, box_cols);
+}
+
+// The A operand (H panel) through TMA needs a 16-byte row stride: real data with an odd ldh is first
+// copied into a workspace with an even leading dimension.
+static chfsi_status a_operand(chfsi_ctx ctx, const void** Hp, int64_t* ldh, int64_t n, int64_t nloc, int elem) {
+  if ((elem * *ldh * 8) % 16 == 0) return CHFSI_OK;
+  const int64_t ld2 = round_up(n, 2);
+  chfsi_status st = ensure(ctx, ctx->hpad, sizeof(double) * elem * (size_t)ld2 * nloc);
+  if (st) return st;
+  CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(ctx->hpad.ptr, 8 * elem * ld2, *Hp, 8 * elem * *ldh, 8 * elem * n, nloc,
+                                        cudaMemcpyDeviceToDevice, ctx->stream));
+  *Hp = ctx->hpad.ptr;
+  *ldh = ld2;
+  return CHFSI_OK;
 }
 
 chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
-                       const void* Q, int64_t ldq, int64_t k, void* out, int64_t ldo) {
+                       const void* Q, int64_t ldq, int64_t k, void* out, int64_t ldo, int elem) {
   (void)row0;
   if (k == 0) return CHFSI_OK;
   const int p = ctx->nranks;
-  TileChoice t = choose_filter_tile(nloc, k, ctx->num_sms);
+  const size_t eb = 8 * (size_t)elem;
+  TileChoice t = elem == 2 ? choose_filter_tile(nloc, k, ctx->num_sms) : choose_filter_tile_real(nloc, k, ctx->num_sms);
   CUtensorMap tmA;
-  chfsi_status st = make_tmap_2d(ctx, &tmA, Hp, 2 * n, nloc, 2 * ldh, t.bm);
+  chfsi_status st = a_operand(ctx, &Hp, &ldh, n, nloc, elem);
+  if (st) return st;
+  st = make_tmap_2d(ctx, &tmA, Hp, elem * n, nloc, elem * ldh, t.bm);
   if (st) return st;
   Operand op;
   const void* bsrc = Q;
   int64_t bld = ldq;
+  const int64_t ldp = elem == 1 ? round_up(nloc, 2) : nloc;  // packed column stride
   if (p > 1) {
-    // gather the full-height Q into R0 = [rank][k][nloc]
-    st = ensure(ctx, ctx->R0, sizeof(double) * 2 * (size_t)n * (size_t)k);
+    // gather the full-height Q into R0 = [rank][k][ldp]
+    st = ensure(ctx, ctx->R0, sizeof(double) * elem * (size_t)ldp * p * (size_t)k);
     if (st) return st;
     double* R = static_cast<double*>(ctx->R0.ptr);
-    double* mine = R + (size_t)2 * nloc * k * ctx->rank;
-    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(mine, 16 * nloc, Q, 16 * ldq, 16 * nloc, k, cudaMemcpyDeviceToDevice,
+    double* mine = R + (size_t)elem * ldp * k * ctx->rank;
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(mine, eb * ldp, Q, eb * ldq, eb * nloc, k, cudaMemcpyDeviceToDevice,
                                           ctx->stream));
-    st = comm_allgather_inplace(ctx, R, (size_t)2 * nloc * k);
+    st = comm_allgather_inplace(ctx, R, (size_t)elem * ldp * k);
     if (st) return st;
     bsrc = R;
-    bld = nloc;
+    bld = ldp;
   }
-  st = b_operand(ctx, &op, bsrc, p == 1 ? n : nloc, bld, k, 0, p, t.bnc);
+  st = b_operand(ctx, &op, bsrc, p == 1 ? n : nloc, bld, k, 0, p, t.bnc, elem);
   if (st) return st;
   StepParams sp{};
   sp.nrows = nloc;
-  const int64_t kr = p == 1 ? 2 * n : 2 * nloc;
+  const int64_t kr = p == 1 ? elem * n : elem * nloc;
   sp.kt_per_rank = (int32_t)((kr + kBK - 1) / kBK);
   sp.num_kt = sp.kt_per_rank * p;
-  sp.a_rank_stride = (int32_t)(2 * nloc);
+  sp.a_rank_stride = (int32_t)(elem * nloc);
   sp.col0 = 0;
   sp.col_end = (int32_t)k;
   sp.fin_end = (int32_t)k;
@@ -194,8 +213,10 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
   chfsi_status st = ensure(ctx, ctx->L0, sizeof(double) * elem * (size_t)ldl * k);
   if (!st) st = ensure(ctx, ctx->L1, sizeof(double) * elem * (size_t)ldl * k);
   if (!st) st = ensure(ctx, ctx->flag, 64);
-  if (p > 1 && !st) st = ensure(ctx, ctx->R0, sizeof(double) * elem * (size_t)n * k);
-  if (p > 1 && !st) st = ensure(ctx, ctx->R1, sizeof(double) * elem * (size_t)n * k);
+  const int64_t ldp = elem == 1 ? round_up(nloc, 2) : nloc;  // packed column stride of R0 / R1
+  if (p > 1 && !st) st = ensure(ctx, ctx->R0, sizeof(double) * elem * (size_t)ldp * p * k);
+  if (p > 1 && !st) st = ensure(ctx, ctx->R1, sizeof(double) * elem * (size_t)ldp * p * k);
+  if (!st) st = a_operand(ctx, &Hp, &ldh, n, nloc, elem);
   if (st) return st;
   double2* L[2] = {static_cast<double2*>(ctx->L0.ptr), static_cast<double2*>(ctx->L1.ptr)};
   double* R[2] = {static_cast<double*>(ctx->R0.ptr), static_cast<double*>(ctx->R1.ptr)};
@@ -205,9 +226,9 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
   CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(L[0], eb * ldl, Y, eb * ldy, eb * nloc, k, cudaMemcpyDeviceToDevice,
                                         ctx->stream));
   if (p > 1) {
-    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(R[0] + (size_t)elem * nloc * k * ctx->rank, eb * nloc, Y, eb * ldy,
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(R[0] + (size_t)elem * ldp * k * ctx->rank, eb * ldp, Y, eb * ldy,
                                           eb * nloc, k, cudaMemcpyDeviceToDevice, ctx->stream));
-    st = comm_allgather_inplace(ctx, R[0], (size_t)elem * nloc * k);
+    st = comm_allgather_inplace(ctx, R[0], (size_t)elem * ldp * k);
     if (st) return st;
   }
   CUtensorMap tmA;
@@ -239,7 +260,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     if (p == 1)
       st = b_operand(ctx, &op, L[cur], n, ldl, k, s, 1, t.bnc, elem);
     else
-      st = b_operand(ctx, &op, R[cur], nloc, nloc, k, s, p, t.bnc, elem);
+      st = b_operand(ctx, &op, R[cur], nloc, ldp, k, s, p, t.bnc, elem);
     if (st) return st;
     StepParams sp{};
     sp.nrows = nloc;
@@ -271,8 +292,8 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     sp.ld_out = ldy;
     const int64_t ka_next = k - s_next;
     if (p > 1 && ka_next > 0) {
-      sp.r_next = reinterpret_cast<double2*>(R[oth] + (size_t)elem * nloc * ka_next * ctx->rank);
-      sp.ld_r_next = nloc;
+      sp.r_next = reinterpret_cast<double2*>(R[oth] + (size_t)elem * ldp * ka_next * ctx->rank);
+      sp.ld_r_next = ldp;
     }
     sp.nonfinite = check_finite ? flag : nullptr;
     schedule_filter_step(t, ctx->num_sms, sp);
@@ -284,7 +305,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     nev_used += 2;
     ctx->launches++;
     if (p > 1 && ka_next > 0) {
-      st = comm_allgather_inplace(ctx, R[oth], (size_t)elem * nloc * ka_next);
+      st = comm_allgather_inplace(ctx, R[oth], (size_t)elem * ldp * ka_next);
       if (st) return st;
     }
   }
@@ -399,7 +420,7 @@ void chfsi_ctx_destroy(chfsi_ctx ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   comm_destroy(ctx);
-  DevBuf* bufs[] = {&ctx->L0, &ctx->L1, &ctx->R0, &ctx->R1, &ctx->flag, &ctx->sk, &ctx->w1, &ctx->w2, &ctx->w3, &ctx->w4,
+  DevBuf* bufs[] = {&ctx->L0, &ctx->L1, &ctx->R0, &ctx->R1, &ctx->flag, &ctx->sk, &ctx->hpad, &ctx->w1, &ctx->w2, &ctx->w3, &ctx->w4,
                     &ctx->small1, &ctx->small2, &ctx->small3, &ctx->solver_ws, &ctx->devinfo, &ctx->lz,
                     &ctx->ya,    &ctx->xl,     &ctx->tb,     &ctx->idx};
   for (DevBuf* b : bufs)

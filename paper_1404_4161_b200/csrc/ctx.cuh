@@ -73,6 +73,7 @@ struct chfsi_ctx_s {
   chfsi::DevBuf R0, R1;          // p > 1: packed full-height B operands
   chfsi::DevBuf flag;            // int nonfinite flag (+ small scalars)
   chfsi::DevBuf sk;              // K1 stream-K workspace: tickets (zeroed) + partial accumulators
+  chfsi::DevBuf hpad;            // real H panel re-strided to an even leading dimension (TMA)
   chfsi::DevBuf w1, w2, w3, w4;  // general nloc x k / k x k scratch for QR / RR / solver
   chfsi::DevBuf small1, small2, small3;
   chfsi::DevBuf solver_ws;       // cuSOLVER workspace
@@ -114,6 +115,6 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
                          bool check_finite, int elem = 2);
 // HQ: out (nloc x k) = H Q for Q (nloc x k, this rank's rows). Uses the K1 kernel, plain epilogue.
 chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
-                       const void* Q, int64_t ldq, int64_t k, void* out, int64_t ldo);
+                       const void* Q, int64_t ldq, int64_t k, void* out, int64_t ldo, int elem = 2);
 
 }  // namespace chfsi

@@ -220,4 +220,158 @@ cudaError_t launch_orth_err(int64_t k, const double2* G, int64_t ldg, double* ou
   return cudaGetLastError();
 }
 
+// ================================================================================================
+// real-symmetric counterparts
+namespace {
+
+__global__ void hemv_real_kernel(int64_t n, int64_t nloc, const double* __restrict__ Hp, int64_t ldh,
+                                 const double* __restrict__ v, double* __restrict__ w) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= nloc) return;
+  const double* h = Hp + r * ldh;
+  double s0 = 0, s1 = 0;
+  int64_t q = lane;
+  for (; q + 32 < n; q += 64) {
+    s0 += __ldcs(h + q) * __ldg(v + q);
+    s1 += __ldcs(h + q + 32) * __ldg(v + q + 32);
+  }
+  if (q < n) s0 += __ldcs(h + q) * __ldg(v + q);
+  const double s = warp_sum(s0 + s1);
+  if (lane == 0) w[r] = s;
+}
+
+__global__ void colnorm2_real_kernel(int64_t rows, const double* __restrict__ X, int64_t ldx, double* out) {
+  const double* x = X + (int64_t)blockIdx.x * ldx;
+  double s = 0;
+  for (int64_t r = threadIdx.x; r < rows; r += kRedThreads) s += x[r] * x[r];
+  s = block_sum<kRedThreads>(s);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+__global__ void resid2_real_kernel(int64_t rows, const double* __restrict__ HY, int64_t ld1,
+                                   const double* __restrict__ Y, int64_t ld2, const double* __restrict__ mu,
+                                   double* out) {
+  const double* hy = HY + (int64_t)blockIdx.x * ld1;
+  const double* y = Y + (int64_t)blockIdx.x * ld2;
+  const double m = mu[blockIdx.x];
+  double s = 0;
+  for (int64_t r = threadIdx.x; r < rows; r += kRedThreads) {
+    const double d = hy[r] - m * y[r];
+    s += d * d;
+  }
+  s = block_sum<kRedThreads>(s);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+__global__ void symmetrize_kernel(int64_t k, double* G, int64_t ldg) {
+  const int64_t j = blockIdx.y;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= j || j >= k) return;
+  const double u = 0.5 * (G[j * ldg + i] + G[i * ldg + j]);
+  G[j * ldg + i] = u;
+  G[i * ldg + j] = u;
+}
+
+__global__ void col_gather_real_kernel(int64_t rows, const double* __restrict__ src, int64_t lds,
+                                       const int* __restrict__ idx, double* __restrict__ dst, int64_t ldd) {
+  const int64_t j = blockIdx.y;
+  const double* s = src + (int64_t)idx[j] * lds;
+  double* d = dst + j * ldd;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+    d[r] = s[r];
+}
+
+__global__ void col_sign_kernel(int64_t rows, double* Q, int64_t ldq, const double* R, int64_t ldr) {
+  const int64_t j = blockIdx.y;
+  const double sgn = R[j * ldr + j] < 0 ? -1.0 : 1.0;
+  double* q = Q + j * ldq;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+    q[r] *= sgn;
+}
+
+__global__ void random_block_real_kernel(int64_t rows, int64_t row0, uint64_t seed, uint64_t stream_base,
+                                         uint64_t stream_stride, double* X, int64_t ldx) {
+  const int64_t j = blockIdx.y;
+  const uint64_t strm = stream_base | (stream_stride * (uint64_t)j);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = (uint64_t)(row0 + r);
+    const uint64_t h0 = splitmix64(seed ^ (strm << 40) ^ (2 * g));
+    const double u0 = (double)(h0 >> 11) * (1.0 / 9007199254740992.0);
+    X[j * ldx + r] = __dadd_rn(__dmul_rn(2.0, u0), -1.0);
+  }
+}
+
+__global__ void scale_real_kernel(int64_t rows, double* x, double s) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+    x[r] *= s;
+}
+
+__global__ void orth_err_real_kernel(int64_t k, const double* G, int64_t ldg, unsigned long long* out) {
+  const int64_t j = blockIdx.y;
+  double m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(G[j * ldg + i] - (i == j ? 1.0 : 0.0)));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __double_as_longlong(m));
+}
+
+}  // namespace
+
+cudaError_t launch_hemv(int64_t n, int64_t nloc, const double* Hp, int64_t ldh, const double* v, double* w,
+                        cudaStream_t st) {
+  const int warps = 8;
+  hemv_real_kernel<<<(unsigned)((nloc + warps - 1) / warps), warps * 32, 0, st>>>(n, nloc, Hp, ldh, v, w);
+  return cudaGetLastError();
+}
+cudaError_t launch_colnorm2(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* out, cudaStream_t st) {
+  if (cols <= 0) return cudaSuccess;
+  colnorm2_real_kernel<<<(unsigned)cols, kRedThreads, 0, st>>>(rows, X, ldx, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_resid2(int64_t rows, int64_t cols, const double* HY, int64_t ld1, const double* Y, int64_t ld2,
+                          const double* mu, double* out, cudaStream_t st) {
+  if (cols <= 0) return cudaSuccess;
+  resid2_real_kernel<<<(unsigned)cols, kRedThreads, 0, st>>>(rows, HY, ld1, Y, ld2, mu, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_hermitize(int64_t k, double* G, int64_t ldg, cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((k + 127) / 128), (unsigned)k);
+  symmetrize_kernel<<<grid, 128, 0, st>>>(k, G, ldg);
+  return cudaGetLastError();
+}
+cudaError_t launch_col_gather(int64_t rows, int64_t cols, const double* src, int64_t lds, const int* idx, double* dst,
+                              int64_t ldd, cudaStream_t st) {
+  if (cols <= 0 || rows <= 0) return cudaSuccess;
+  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), (unsigned)cols);
+  col_gather_real_kernel<<<grid, 256, 0, st>>>(rows, src, lds, idx, dst, ldd);
+  return cudaGetLastError();
+}
+cudaError_t launch_col_phase(int64_t rows, int64_t cols, double* Q, int64_t ldq, const double* R, int64_t ldr,
+                             cudaStream_t st) {
+  if (cols <= 0 || rows <= 0) return cudaSuccess;
+  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), (unsigned)cols);
+  col_sign_kernel<<<grid, 256, 0, st>>>(rows, Q, ldq, R, ldr);
+  return cudaGetLastError();
+}
+cudaError_t launch_random_block(int64_t rows, int64_t cols, int64_t row0, uint64_t seed, uint64_t stream_base,
+                                uint64_t stream_stride, double* X, int64_t ldx, cudaStream_t st) {
+  if (cols <= 0 || rows <= 0) return cudaSuccess;
+  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), (unsigned)cols);
+  random_block_real_kernel<<<grid, 256, 0, st>>>(rows, row0, seed, stream_base, stream_stride, X, ldx);
+  return cudaGetLastError();
+}
+cudaError_t launch_scale(int64_t rows, double* x, double s, cudaStream_t st) {
+  scale_real_kernel<<<grid1(rows, 256), 256, 0, st>>>(rows, x, s);
+  return cudaGetLastError();
+}
+cudaError_t launch_orth_err(int64_t k, const double* G, int64_t ldg, double* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((k + 255) / 256), (unsigned)k);
+  orth_err_real_kernel<<<grid, 256, 0, st>>>(k, G, ldg, reinterpret_cast<unsigned long long*>(out));
+  return cudaGetLastError();
+}
+
 }  // namespace chfsi

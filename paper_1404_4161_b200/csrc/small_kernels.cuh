@@ -33,4 +33,22 @@ cudaError_t launch_scale(int64_t rows, double2* x, double s, cudaStream_t st);
 // G[i,j] for i<k: make identity minus G, return max |entry| into out[0] via atomicMax on the bit pattern
 cudaError_t launch_orth_err(int64_t k, const double2* G, int64_t ldg, double* out, cudaStream_t st);
 
+// ---- real-symmetric (NEXT-3) counterparts, same semantics on double data ----
+cudaError_t launch_hemv(int64_t n, int64_t nloc, const double* Hp, int64_t ldh, const double* v, double* w,
+                        cudaStream_t st);
+cudaError_t launch_colnorm2(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* out, cudaStream_t st);
+cudaError_t launch_resid2(int64_t rows, int64_t cols, const double* HY, int64_t ld1, const double* Y, int64_t ld2,
+                          const double* mu, double* out, cudaStream_t st);
+cudaError_t launch_hermitize(int64_t k, double* G, int64_t ldg, cudaStream_t st);
+cudaError_t launch_col_gather(int64_t rows, int64_t cols, const double* src, int64_t lds, const int* idx, double* dst,
+                              int64_t ldd, cudaStream_t st);
+// Q[:, j] *= sign(R[j, j])
+cudaError_t launch_col_phase(int64_t rows, int64_t cols, double* Q, int64_t ldq, const double* R, int64_t ldr,
+                             cudaStream_t st);
+// X[r, j] = 2u_{2g} - 1 (the real part of the complex R22 formula)
+cudaError_t launch_random_block(int64_t rows, int64_t cols, int64_t row0, uint64_t seed, uint64_t stream_base,
+                                uint64_t stream_stride, double* X, int64_t ldx, cudaStream_t st);
+cudaError_t launch_scale(int64_t rows, double* x, double s, cudaStream_t st);
+cudaError_t launch_orth_err(int64_t k, const double* G, int64_t ldg, double* out, cudaStream_t st);
+
 }  // namespace chfsi

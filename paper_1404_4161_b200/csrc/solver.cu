@@ -7,6 +7,7 @@
 #include <cmath>
 #include <numeric>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "ctx.cuh"
@@ -67,8 +68,10 @@ enum { T_LANCZOS = 0, T_FILTER, T_QR, T_RR, T_RESID, T_OPT, T_TOTAL };
 }  // namespace
 
 // One eigenproblem. X (nloc x k) in: start block / hand-off; out: hand-off [locked asc | active].
+// E: double2 (complex Hermitian, scalar cuDoubleComplex) or double (real symmetric, NEXT-3)
+template <typename E>
 static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
-                              const chfsi_opts& o, double2* X, int64_t ldx, bool have_prev, double& lam1_io,
+                              const chfsi_opts& o, E* X, int64_t ldx, bool have_prev, double& lam1_io,
                               double& lamk_io, double* lam_out, double* res_out, chfsi_report& rep, uint64_t seed) {
   const int64_t nev = o.nev, k = (int64_t)o.nev + o.nex;
   rep = chfsi_report{};
@@ -79,12 +82,15 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
   TRY(ensure(ctx, ctx->xl, blk));
   TRY(ensure(ctx, ctx->tb, blk));
   TRY(ensure(ctx, ctx->idx, sizeof(int) * (size_t)k));
-  double2* Ya = static_cast<double2*>(ctx->ya.ptr);
-  double2* XL = static_cast<double2*>(ctx->xl.ptr);
-  double2* T = static_cast<double2*>(ctx->tb.ptr);
+  using Scal = typename std::conditional<std::is_same<E, double>::value, double, cuDoubleComplex>::type;
+  constexpr int elem = sizeof(E) / sizeof(double);
+  constexpr size_t eb = sizeof(E);
+  E* Ya = static_cast<E*>(ctx->ya.ptr);
+  E* XL = static_cast<E*>(ctx->xl.ptr);
+  E* T = static_cast<E*>(ctx->tb.ptr);
   int* didx = static_cast<int*>(ctx->idx.ptr);
   std::vector<int> hidx(k);
-  auto gather = [&](const double2* src, const std::vector<int>& cols, double2* dst, int64_t ldd) -> chfsi_status {
+  auto gather = [&](const E* src, const std::vector<int>& cols, E* dst, int64_t ldd) -> chfsi_status {
     if (cols.empty()) return CHFSI_OK;
     CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(didx, cols.data(), sizeof(int) * cols.size(), cudaMemcpyHostToDevice,
                                         ctx->stream));
@@ -96,7 +102,7 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
   // Alg 1 l3: Lanczos upper bound beta (R17) and ||H||_est (R8)
   double tmin, tmax, beta;
   auto t0 = tm.begin();
-  TRY(lanczos_impl(ctx, n, row0, nloc, Hp, ldh, o.lanczos_steps, seed, &tmin, &tmax, &beta));
+  TRY(lanczos_t<Scal>(ctx, n, row0, nloc, Hp, ldh, o.lanczos_steps, seed, &tmin, &tmax, &beta));
   tm.end(T_LANCZOS, t0);
   const double normH = std::max(std::fabs(tmin), std::fabs(tmax));
   rep.theta_min = tmin;
@@ -105,17 +111,17 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
   rep.normH = normH;
   rep.matvecs_total += o.lanczos_steps;
 
-  CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(Ya, 16 * nloc, X, 16 * ldx, 16 * nloc, k, cudaMemcpyDeviceToDevice, ctx->stream));
+  CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(Ya, eb * nloc, X, eb * ldx, eb * nloc, k, cudaMemcpyDeviceToDevice, ctx->stream));
   std::vector<double> mu(k), res(k), lamL, resL;
   double lam1, alpha;
   if (!have_prev) {  // R11: start block -> QR -> RR seeds (lambda_1, alpha)
     int32_t fb = 0;
     auto t1 = tm.begin();
-    TRY(qr_impl(ctx, n, nloc, nullptr, nloc, 0, Ya, nloc, k, &fb));
+    TRY(qr_t<Scal>(ctx, n, nloc, nullptr, nloc, 0, Ya, nloc, k, &fb));
     tm.end(T_QR, t1);
     rep.qr_fallbacks += fb;
     auto t2 = tm.begin();
-    TRY(rr_impl(ctx, n, row0, nloc, Hp, ldh, Ya, nloc, k, normH, mu.data(), nullptr));
+    TRY(rr_t<Scal>(ctx, n, row0, nloc, Hp, ldh, Ya, nloc, k, normH, mu.data(), nullptr));
     tm.end(T_RR, t2);
     rep.matvecs_total += k;
     lam1 = mu[0];
@@ -140,7 +146,7 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
     auto t3 = tm.begin();
     const double k1s = ctx->k1_seconds;
     const int64_t k1n = ctx->k1_launches;
-    TRY(filter_impl(ctx, n, row0, nloc, Hp, ldh, T, nloc, ka, ms.data(), lam1, c, e, true));
+    TRY(filter_impl(ctx, n, row0, nloc, Hp, ldh, T, nloc, ka, ms.data(), lam1, c, e, true, elem));
     tm.end(T_FILTER, t3);
     rep.t_filter_kernel += ctx->k1_seconds - k1s;
     rep.filter_launches += ctx->k1_launches - k1n;
@@ -148,16 +154,16 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
     for (int64_t j = 0; j < ka; ++j) mv += ms[j];
     rep.matvecs_filter += mv;
     rep.matvecs_total += mv;
-    rep.filter_flops += 8.0 * (double)n * (double)n * (double)mv;
+    rep.filter_flops += (elem == 2 ? 8.0 : 2.0) * (double)n * (double)n * (double)mv;
     // Alg 1 l6: orthonormalise [locked | filtered] (R14, R15)
     int32_t fb = 0;
     auto t4 = tm.begin();
-    TRY(qr_impl(ctx, n, nloc, XL, nloc, nl, T, nloc, ka, &fb));
+    TRY(qr_t<Scal>(ctx, n, nloc, XL, nloc, nl, T, nloc, ka, &fb));
     tm.end(T_QR, t4);
     rep.qr_fallbacks += fb;
     // Alg 1 l7-9 (+ residuals, R8): Rayleigh-Ritz on the active block (R16)
     auto t5 = tm.begin();
-    TRY(rr_impl(ctx, n, row0, nloc, Hp, ldh, T, nloc, ka, normH, mu.data(), res.data()));
+    TRY(rr_t<Scal>(ctx, n, row0, nloc, Hp, ldh, T, nloc, ka, normH, mu.data(), res.data()));
     tm.end(T_RR, t5);
     rep.matvecs_total += ka;
     rep.loops++;
@@ -230,11 +236,11 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
   std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return lamL[a] < lamL[b]; });
   if (nl > 0) {
     TRY(gather(XL, ord, T, nloc));
-    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(X, 16 * ldx, T, 16 * nloc, 16 * nloc, nl, cudaMemcpyDeviceToDevice,
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(X, eb * ldx, T, eb * nloc, eb * nloc, nl, cudaMemcpyDeviceToDevice,
                                           ctx->stream));
   }
   if (k - nl > 0)
-    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(X + (size_t)nl * ldx, 16 * ldx, Ya, 16 * nloc, 16 * nloc, k - nl,
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(X + (size_t)nl * ldx, eb * ldx, Ya, eb * nloc, eb * nloc, k - nl,
                                           cudaMemcpyDeviceToDevice, ctx->stream));
   for (int64_t j = 0; j < nev; ++j) {
     if (j < nl) {
@@ -264,9 +270,10 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
 
 using namespace chfsi;
 
-extern "C" chfsi_status chfsi_solve_sequence(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, int32_t nprob,
-                                             chfsi_get_h get_h, void* user, const chfsi_opts* opts, void* X,
-                                             int64_t ldx, double* lambda, double* resid, chfsi_report* reports) {
+template <typename E>
+static chfsi_status solve_sequence_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, int32_t nprob,
+                                     chfsi_get_h get_h, void* user, const chfsi_opts* opts, void* X, int64_t ldx,
+                                     double* lambda, double* resid, chfsi_report* reports) {
   if (!ctx) return CHFSI_ERR_ARG;
   ctx->err.clear();
   if (!opts || !get_h || !X || !lambda || nprob < 0 || n < 1 || nloc < 1 || row0 < 0 || row0 + nloc > n ||
@@ -284,7 +291,7 @@ extern "C" chfsi_status chfsi_solve_sequence(chfsi_ctx ctx, int64_t n, int64_t r
     return CHFSI_ERR_ARG;
   }
   cudaSetDevice(ctx->device);
-  double2* Xd = static_cast<double2*>(X);
+  E* Xd = static_cast<E*>(X);
   if (o.random_start) {  // R22 block: column j uses stream (3 << 16) | j
     CHFSI_CUDA_TRY(ctx, launch_random_block(nloc, k, row0, o.seed, 3ull << 16, 1, Xd, ldx, ctx->stream));
     ctx->launches++;
@@ -304,7 +311,7 @@ extern "C" chfsi_status chfsi_solve_sequence(chfsi_ctx ctx, int64_t n, int64_t r
       ctx->launches++;
     }
     chfsi_report rep{};
-    chfsi_status st = solve_one(ctx, n, row0, nloc, Hp, ldh, o, Xd, ldx, ell > 0 && !o.no_reuse, lam1, lamk,
+    chfsi_status st = solve_one<E>(ctx, n, row0, nloc, Hp, ldh, o, Xd, ldx, ell > 0 && !o.no_reuse, lam1, lamk,
                                 lambda + (size_t)ell * o.nev, resid ? resid + (size_t)ell * o.nev : nullptr, rep,
                                 o.seed + (uint64_t)ell);
     if (reports) reports[ell] = rep;
@@ -316,6 +323,19 @@ extern "C" chfsi_status chfsi_solve_sequence(chfsi_ctx ctx, int64_t n, int64_t r
   }
   if (worst == CHFSI_ERR_NOCONV) set_err(ctx, "ChFSI: at least one problem hit max_loops");
   return worst;
+}
+
+extern "C" chfsi_status chfsi_solve_sequence(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, int32_t nprob,
+                                             chfsi_get_h get_h, void* user, const chfsi_opts* opts, void* X,
+                                             int64_t ldx, double* lambda, double* resid, chfsi_report* reports) {
+  return solve_sequence_t<double2>(ctx, n, row0, nloc, nprob, get_h, user, opts, X, ldx, lambda, resid, reports);
+}
+
+extern "C" chfsi_status chfsi_solve_sequence_real(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc,
+                                                  int32_t nprob, chfsi_get_h get_h, void* user,
+                                                  const chfsi_opts* opts, double* X, int64_t ldx, double* lambda,
+                                                  double* resid, chfsi_report* reports) {
+  return solve_sequence_t<double>(ctx, n, row0, nloc, nprob, get_h, user, opts, X, ldx, lambda, resid, reports);
 }
 
 extern "C" chfsi_status chfsi_solve_batch(int32_t device, int32_t workers, int64_t n, const chfsi_opts* opts,

@@ -37,22 +37,124 @@ namespace chfsi {
     if (_st != CHFSI_OK) return _st; \
   } while (0)
 
-static const cuDoubleComplex kOne = {1.0, 0.0}, kZero = {0.0, 0.0}, kMinusOne = {-1.0, 0.0};
+// Scalar traits: complex Hermitian (cuDoubleComplex, the north-star path) or real symmetric (double,
+// SURVEY 8(f) NEXT-3). D is the element type of the library's small kernels.
+template <typename T>
+struct Sc;
+template <>
+struct Sc<cuDoubleComplex> {
+  using T = cuDoubleComplex;
+  using D = double2;
+  static constexpr int elem = 2;
+  static constexpr cublasOperation_t opH = CUBLAS_OP_C;
+  static T one() { return {1.0, 0.0}; }
+  static T zero() { return {0.0, 0.0}; }
+  static T mone() { return {-1.0, 0.0}; }
+  static cublasStatus_t gemm(cublasHandle_t h, cublasOperation_t a, cublasOperation_t b, int m, int n, int k,
+                             const T* al, const T* A, int lda, const T* B, int ldb, const T* be, T* C, int ldc) {
+    return cublasZgemm(h, a, b, m, n, k, al, A, lda, B, ldb, be, C, ldc);
+  }
+  static cublasStatus_t gemv(cublasHandle_t h, cublasOperation_t a, int m, int n, const T* al, const T* A, int lda,
+                             const T* x, const T* be, T* y) {
+    return cublasZgemv(h, a, m, n, al, A, lda, x, 1, be, y, 1);
+  }
+  static cublasStatus_t trsm_ru(cublasHandle_t h, int m, int n, const T* R, int ldr, T* Y, int ldy) {
+    const T o = one();
+    return cublasZtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, m, n, &o, R, ldr,
+                       Y, ldy);
+  }
+  static cusolverStatus_t potrf_bs(cusolverDnHandle_t h, int n, T* A, int lda, int* lw) {
+    return cusolverDnZpotrf_bufferSize(h, CUBLAS_FILL_MODE_UPPER, n, A, lda, lw);
+  }
+  static cusolverStatus_t potrf(cusolverDnHandle_t h, int n, T* A, int lda, T* w, int lw, int* info) {
+    return cusolverDnZpotrf(h, CUBLAS_FILL_MODE_UPPER, n, A, lda, w, lw, info);
+  }
+  static cusolverStatus_t heevd_bs(cusolverDnHandle_t h, int n, T* A, int lda, double* W, int* lw) {
+    return cusolverDnZheevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n, A, lda, W, lw);
+  }
+  static cusolverStatus_t heevd(cusolverDnHandle_t h, int n, T* A, int lda, double* W, T* w, int lw, int* info) {
+    return cusolverDnZheevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n, A, lda, W, w, lw, info);
+  }
+  static cusolverStatus_t geqrf_bs(cusolverDnHandle_t h, int m, int n, T* A, int lda, int* lw) {
+    return cusolverDnZgeqrf_bufferSize(h, m, n, A, lda, lw);
+  }
+  static cusolverStatus_t geqrf(cusolverDnHandle_t h, int m, int n, T* A, int lda, T* tau, T* w, int lw, int* info) {
+    return cusolverDnZgeqrf(h, m, n, A, lda, tau, w, lw, info);
+  }
+  static cusolverStatus_t orgqr_bs(cusolverDnHandle_t h, int m, int n, T* A, int lda, const T* tau, int* lw) {
+    return cusolverDnZungqr_bufferSize(h, m, n, n, A, lda, tau, lw);
+  }
+  static cusolverStatus_t orgqr(cusolverDnHandle_t h, int m, int n, T* A, int lda, const T* tau, T* w, int lw,
+                                int* info) {
+    return cusolverDnZungqr(h, m, n, n, A, lda, tau, w, lw, info);
+  }
+  static double re(const T& x) { return x.x; }
+};
+template <>
+struct Sc<double> {
+  using T = double;
+  using D = double;
+  static constexpr int elem = 1;
+  static constexpr cublasOperation_t opH = CUBLAS_OP_T;
+  static T one() { return 1.0; }
+  static T zero() { return 0.0; }
+  static T mone() { return -1.0; }
+  static cublasStatus_t gemm(cublasHandle_t h, cublasOperation_t a, cublasOperation_t b, int m, int n, int k,
+                             const T* al, const T* A, int lda, const T* B, int ldb, const T* be, T* C, int ldc) {
+    return cublasDgemm(h, a, b, m, n, k, al, A, lda, B, ldb, be, C, ldc);
+  }
+  static cublasStatus_t gemv(cublasHandle_t h, cublasOperation_t a, int m, int n, const T* al, const T* A, int lda,
+                             const T* x, const T* be, T* y) {
+    return cublasDgemv(h, a, m, n, al, A, lda, x, 1, be, y, 1);
+  }
+  static cublasStatus_t trsm_ru(cublasHandle_t h, int m, int n, const T* R, int ldr, T* Y, int ldy) {
+    const T o = one();
+    return cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, m, n, &o, R, ldr,
+                       Y, ldy);
+  }
+  static cusolverStatus_t potrf_bs(cusolverDnHandle_t h, int n, T* A, int lda, int* lw) {
+    return cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_UPPER, n, A, lda, lw);
+  }
+  static cusolverStatus_t potrf(cusolverDnHandle_t h, int n, T* A, int lda, T* w, int lw, int* info) {
+    return cusolverDnDpotrf(h, CUBLAS_FILL_MODE_UPPER, n, A, lda, w, lw, info);
+  }
+  static cusolverStatus_t heevd_bs(cusolverDnHandle_t h, int n, T* A, int lda, double* W, int* lw) {
+    return cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n, A, lda, W, lw);
+  }
+  static cusolverStatus_t heevd(cusolverDnHandle_t h, int n, T* A, int lda, double* W, T* w, int lw, int* info) {
+    return cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n, A, lda, W, w, lw, info);
+  }
+  static cusolverStatus_t geqrf_bs(cusolverDnHandle_t h, int m, int n, T* A, int lda, int* lw) {
+    return cusolverDnDgeqrf_bufferSize(h, m, n, A, lda, lw);
+  }
+  static cusolverStatus_t geqrf(cusolverDnHandle_t h, int m, int n, T* A, int lda, T* tau, T* w, int lw, int* info) {
+    return cusolverDnDgeqrf(h, m, n, A, lda, tau, w, lw, info);
+  }
+  static cusolverStatus_t orgqr_bs(cusolverDnHandle_t h, int m, int n, T* A, int lda, const T* tau, int* lw) {
+    return cusolverDnDorgqr_bufferSize(h, m, n, n, A, lda, tau, lw);
+  }
+  static cusolverStatus_t orgqr(cusolverDnHandle_t h, int m, int n, T* A, int lda, const T* tau, T* w, int lw,
+                                int* info) {
+    return cusolverDnDorgqr(h, m, n, n, A, lda, tau, w, lw, info);
+  }
+  static double re(const T& x) { return x; }
+};
 
-static inline cuDoubleComplex* zc(void* p) { return static_cast<cuDoubleComplex*>(p); }
-static inline const cuDoubleComplex* zc(const void* p) { return static_cast<const cuDoubleComplex*>(p); }
 
 // C (m x n, ldc) = A^H B with A (K x m), B (K x n) local rows, summed over ranks
+template <typename T>
 static chfsi_status gram(chfsi_ctx ctx, int64_t K, int64_t m, int64_t n, const void* A, int64_t lda, const void* B,
                          int64_t ldb, void* C, int64_t ldc) {
-  CUBLAS_TRY(ctx, cublasZgemm(ctx->cublas, CUBLAS_OP_C, CUBLAS_OP_N, (int)m, (int)n, (int)K, &kOne, zc(A), (int)lda,
-                              zc(B), (int)ldb, &kZero, zc(C), (int)ldc));
+  using S = Sc<T>;
+  const T one = S::one(), zero = S::zero();
+  CUBLAS_TRY(ctx, S::gemm(ctx->cublas, S::opH, CUBLAS_OP_N, (int)m, (int)n, (int)K, &one, static_cast<const T*>(A),
+                          (int)lda, static_cast<const T*>(B), (int)ldb, &zero, static_cast<T*>(C), (int)ldc));
   if (ctx->nranks > 1) {
     if (ldc != m) {
       set_err(ctx, "gram: allreduce needs packed C");
       return CHFSI_ERR_ARG;
     }
-    TRY(comm_allreduce_sum(ctx, static_cast<double*>(C), (size_t)2 * m * n));
+    TRY(comm_allreduce_sum(ctx, static_cast<double*>(C), (size_t)S::elem * m * n));
   }
   return CHFSI_OK;
 }
@@ -93,20 +195,24 @@ static void tridiag_extremes(const std::vector<double>& al, const std::vector<do
   }
 }
 
-chfsi_status lanczos_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
-                          int32_t steps, uint64_t seed, double* theta_min, double* theta_max, double* upper) {
+template <typename T>
+chfsi_status lanczos_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh, int32_t steps,
+                       uint64_t seed, double* theta_min, double* theta_max, double* upper) {
+  using S = Sc<T>;
+  using D = typename S::D;
+  const T one = S::one(), zero = S::zero(), mone = S::mone();
   if (steps > n) steps = (int32_t)n;
   const int p = ctx->nranks;
   const int64_t ldv = nloc;
-  TRY(ensure(ctx, ctx->lz, sizeof(double) * 2 * ((size_t)ldv * (steps + 1) + (size_t)n + (size_t)nloc)));
+  TRY(ensure(ctx, ctx->lz, sizeof(D) * ((size_t)ldv * (steps + 1) + (size_t)n + (size_t)nloc)));
   TRY(ensure(ctx, ctx->small3, sizeof(double) * 2 * (size_t)(steps + 8)));
-  double2* V = static_cast<double2*>(ctx->lz.ptr);
-  double2* vfull = V + (size_t)ldv * (steps + 1);
-  double2* w = vfull + n;
-  double2* coef = static_cast<double2*>(ctx->small3.ptr);
-  double* nrm = reinterpret_cast<double*>(coef + steps + 2);
+  D* V = static_cast<D*>(ctx->lz.ptr);
+  D* vfull = V + (size_t)ldv * (steps + 1);
+  D* w = vfull + n;
+  D* coef = static_cast<D*>(ctx->small3.ptr);
+  double* nrm = static_cast<double*>(ctx->small3.ptr) + 2 * (steps + 2);
   std::vector<double> al(steps), be(steps);
-  std::vector<double2> hcoef(steps + 2);
+  std::vector<T> hcoef(steps + 2);
   for (int restart = 0; restart <= 3; ++restart) {
     CHFSI_CUDA_TRY(ctx, launch_random_block(nloc, 1, row0, seed, (4ull << 16) | (uint64_t)restart, 0, V, ldv,
                                             ctx->stream));
@@ -123,32 +229,33 @@ chfsi_status lanczos_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, 
     bool broke = false;
     int j = 0;
     for (; j < steps; ++j) {
-      double2* vj = V + (size_t)j * ldv;
-      const double2* vin = vj;
+      D* vj = V + (size_t)j * ldv;
+      const D* vin = vj;
       if (p > 1) {
-        CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(vfull + (size_t)nloc * ctx->rank, vj, 16 * nloc, cudaMemcpyDeviceToDevice,
-                                            ctx->stream));
-        TRY(comm_allgather_inplace(ctx, reinterpret_cast<double*>(vfull), (size_t)2 * nloc));
+        CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(vfull + (size_t)nloc * ctx->rank, vj, sizeof(D) * nloc,
+                                            cudaMemcpyDeviceToDevice, ctx->stream));
+        TRY(comm_allgather_inplace(ctx, reinterpret_cast<double*>(vfull), (size_t)S::elem * nloc));
         vin = vfull;
       }
-      CHFSI_CUDA_TRY(ctx, launch_hemv(n, nloc, static_cast<const double2*>(Hp), ldh, vin, w, ctx->stream));
+      CHFSI_CUDA_TRY(ctx, launch_hemv(n, nloc, static_cast<const D*>(Hp), ldh, vin, w, ctx->stream));
       ctx->launches++;
       for (int pass = 0; pass < 2; ++pass) {
-        CUBLAS_TRY(ctx, cublasZgemv(ctx->cublas, CUBLAS_OP_C, (int)nloc, j + 1, &kOne, zc(V), (int)ldv, zc(w), 1,
-                                    &kZero, zc(coef), 1));
-        TRY(comm_allreduce_sum(ctx, reinterpret_cast<double*>(coef), (size_t)2 * (j + 1)));
+        CUBLAS_TRY(ctx, S::gemv(ctx->cublas, S::opH, (int)nloc, j + 1, &one, reinterpret_cast<const T*>(V), (int)ldv,
+                                reinterpret_cast<const T*>(w), &zero, reinterpret_cast<T*>(coef)));
+        TRY(comm_allreduce_sum(ctx, reinterpret_cast<double*>(coef), (size_t)S::elem * (j + 1)));
         if (pass == 0) {
-          CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(hcoef.data(), coef, 16 * (j + 1), cudaMemcpyDeviceToHost, ctx->stream));
+          CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(hcoef.data(), coef, sizeof(T) * (j + 1), cudaMemcpyDeviceToHost,
+                                              ctx->stream));
         }
-        CUBLAS_TRY(ctx, cublasZgemv(ctx->cublas, CUBLAS_OP_N, (int)nloc, j + 1, &kMinusOne, zc(V), (int)ldv, zc(coef),
-                                    1, &kOne, zc(w), 1));
+        CUBLAS_TRY(ctx, S::gemv(ctx->cublas, CUBLAS_OP_N, (int)nloc, j + 1, &mone, reinterpret_cast<const T*>(V),
+                                (int)ldv, reinterpret_cast<const T*>(coef), &one, reinterpret_cast<T*>(w)));
       }
       CHFSI_CUDA_TRY(ctx, launch_colnorm2(nloc, 1, w, nloc, nrm, ctx->stream));
       ctx->launches++;
       TRY(comm_allreduce_sum(ctx, nrm, 1));
       CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&h, nrm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
       CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-      al[j] = hcoef[j].x;  // alpha_j = Re(v_j^H H v_j)
+      al[j] = S::re(hcoef[j]);  // alpha_j = Re(v_j^H H v_j)
       be[j] = std::sqrt(h);
       hest = std::max(hest, std::fabs(al[j]) + be[j] + (j > 0 ? be[j - 1] : 0.0));
       if (j + 1 < steps) {
@@ -156,8 +263,8 @@ chfsi_status lanczos_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, 
           broke = true;
           break;
         }
-        double2* vn = V + (size_t)(j + 1) * ldv;
-        CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(vn, w, 16 * nloc, cudaMemcpyDeviceToDevice, ctx->stream));
+        D* vn = V + (size_t)(j + 1) * ldv;
+        CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(vn, w, sizeof(D) * nloc, cudaMemcpyDeviceToDevice, ctx->stream));
         CHFSI_CUDA_TRY(ctx, launch_scale(nloc, vn, 1.0 / be[j], ctx->stream));
         ctx->launches++;
       }
@@ -173,46 +280,50 @@ chfsi_status lanczos_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, 
 
 // ---------------------------------------------------------------------------------------------
 // Householder QR of Y (nloc x ka) with a positive real R diagonal; p > 1 gathers the block.
+template <typename T>
 static chfsi_status householder(chfsi_ctx ctx, int64_t n, int64_t nloc, void* Y, int64_t ldy, int64_t ka) {
+  using S = Sc<T>;
+  using D = typename S::D;
+  const size_t eb = sizeof(T);
   const int p = ctx->nranks;
   void* A = Y;
   int64_t lda = ldy, m = nloc;
   if (p > 1) {
-    TRY(ensure(ctx, ctx->R0, sizeof(double) * 2 * (size_t)n * ka));
-    TRY(ensure(ctx, ctx->w4, sizeof(double) * 2 * (size_t)n * ka));
+    TRY(ensure(ctx, ctx->R0, eb * (size_t)n * ka));
+    TRY(ensure(ctx, ctx->w4, eb * (size_t)n * ka));
     double* R = static_cast<double*>(ctx->R0.ptr);
-    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(R + (size_t)2 * nloc * ka * ctx->rank, 16 * nloc, Y, 16 * ldy, 16 * nloc, ka,
-                                          cudaMemcpyDeviceToDevice, ctx->stream));
-    TRY(comm_allgather_inplace(ctx, R, (size_t)2 * nloc * ka));
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(R + (size_t)S::elem * nloc * ka * ctx->rank, eb * nloc, Y, eb * ldy,
+                                          eb * nloc, ka, cudaMemcpyDeviceToDevice, ctx->stream));
+    TRY(comm_allgather_inplace(ctx, R, (size_t)S::elem * nloc * ka));
     double* F = static_cast<double*>(ctx->w4.ptr);
     for (int q = 0; q < p; ++q)
-      CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(F + (size_t)2 * nloc * q, 16 * n, R + (size_t)2 * nloc * ka * q, 16 * nloc,
-                                            16 * nloc, ka, cudaMemcpyDeviceToDevice, ctx->stream));
+      CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(F + (size_t)S::elem * nloc * q, eb * n, R + (size_t)S::elem * nloc * ka * q,
+                                            eb * nloc, eb * nloc, ka, cudaMemcpyDeviceToDevice, ctx->stream));
     A = F;
     lda = n;
     m = n;
   }
-  TRY(ensure(ctx, ctx->small2, sizeof(double) * 2 * (size_t)ka * (ka + 1)));
+  TRY(ensure(ctx, ctx->small2, eb * (size_t)ka * (ka + 1)));
   TRY(ensure(ctx, ctx->devinfo, 64));
-  cuDoubleComplex* tau = zc(ctx->small2.ptr);
-  cuDoubleComplex* Rd = tau + ka;  // copy of R (ka x ka)
+  T* tau = static_cast<T*>(ctx->small2.ptr);
+  T* Rd = tau + ka;  // copy of R (ka x ka)
+  T* At = static_cast<T*>(A);
   int* info = static_cast<int*>(ctx->devinfo.ptr);
   int lw1 = 0, lw2 = 0;
-  CUSOLVER_TRY(ctx, cusolverDnZgeqrf_bufferSize(ctx->cusolver, (int)m, (int)ka, zc(A), (int)lda, &lw1));
-  CUSOLVER_TRY(ctx, cusolverDnZungqr_bufferSize(ctx->cusolver, (int)m, (int)ka, (int)ka, zc(A), (int)lda, tau, &lw2));
+  CUSOLVER_TRY(ctx, S::geqrf_bs(ctx->cusolver, (int)m, (int)ka, At, (int)lda, &lw1));
+  CUSOLVER_TRY(ctx, S::orgqr_bs(ctx->cusolver, (int)m, (int)ka, At, (int)lda, tau, &lw2));
   const int lw = std::max(lw1, lw2);
-  TRY(ensure(ctx, ctx->solver_ws, sizeof(cuDoubleComplex) * (size_t)std::max(lw, 1)));
-  CUSOLVER_TRY(ctx, cusolverDnZgeqrf(ctx->cusolver, (int)m, (int)ka, zc(A), (int)lda, tau, zc(ctx->solver_ws.ptr), lw,
-                                     info));
-  CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(Rd, 16 * ka, A, 16 * lda, 16 * ka, ka, cudaMemcpyDeviceToDevice, ctx->stream));
-  CUSOLVER_TRY(ctx, cusolverDnZungqr(ctx->cusolver, (int)m, (int)ka, (int)ka, zc(A), (int)lda, tau,
-                                     zc(ctx->solver_ws.ptr), lw, info));
-  CHFSI_CUDA_TRY(ctx, launch_col_phase(m, ka, static_cast<double2*>(A), lda, reinterpret_cast<double2*>(Rd), ka,
-                                       ctx->stream));
+  TRY(ensure(ctx, ctx->solver_ws, eb * (size_t)std::max(lw, 1)));
+  CUSOLVER_TRY(ctx, S::geqrf(ctx->cusolver, (int)m, (int)ka, At, (int)lda, tau, static_cast<T*>(ctx->solver_ws.ptr), lw,
+                             info));
+  CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(Rd, eb * ka, A, eb * lda, eb * ka, ka, cudaMemcpyDeviceToDevice, ctx->stream));
+  CUSOLVER_TRY(ctx, S::orgqr(ctx->cusolver, (int)m, (int)ka, At, (int)lda, tau, static_cast<T*>(ctx->solver_ws.ptr), lw,
+                             info));
+  CHFSI_CUDA_TRY(ctx, launch_col_phase(m, ka, static_cast<D*>(A), lda, reinterpret_cast<D*>(Rd), ka, ctx->stream));
   ctx->launches++;
   if (p > 1) {
     const double* F = static_cast<const double*>(A);
-    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(Y, 16 * ldy, F + (size_t)2 * nloc * ctx->rank, 16 * n, 16 * nloc, ka,
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(Y, eb * ldy, F + (size_t)S::elem * nloc * ctx->rank, eb * n, eb * nloc, ka,
                                           cudaMemcpyDeviceToDevice, ctx->stream));
   }
   int hinfo = 0;
@@ -225,31 +336,36 @@ static chfsi_status householder(chfsi_ctx ctx, int64_t n, int64_t nloc, void* Y,
   return CHFSI_OK;
 }
 
-chfsi_status qr_impl(chfsi_ctx ctx, int64_t n, int64_t nloc, const void* XL, int64_t ldxl, int64_t nl, void* Y,
-                     int64_t ldy, int64_t ka, int32_t* used_fallback) {
+template <typename T>
+chfsi_status qr_t(chfsi_ctx ctx, int64_t n, int64_t nloc, const void* XL, int64_t ldxl, int64_t nl, void* Y, int64_t ldy,
+                  int64_t ka, int32_t* used_fallback) {
+  using S = Sc<T>;
+  using D = typename S::D;
+  const T one = S::one(), mone = S::mone();
   if (used_fallback) *used_fallback = 0;
   if (ka == 0) return CHFSI_OK;
-  TRY(ensure(ctx, ctx->small1, sizeof(double) * 2 * (size_t)std::max<int64_t>(ka, nl) * ka + 64));
+  TRY(ensure(ctx, ctx->small1, sizeof(T) * (size_t)std::max<int64_t>(ka, nl) * ka + 64));
   TRY(ensure(ctx, ctx->devinfo, 64));
-  cuDoubleComplex* S = zc(ctx->small1.ptr);
+  T* G = static_cast<T*>(ctx->small1.ptr);
+  T* Yt = static_cast<T*>(Y);
+  const T* Xt = static_cast<const T*>(XL);
   int* info = static_cast<int*>(ctx->devinfo.ptr);
   // CGS2 against the locked block (R15: the locked columns are not modified)
   if (nl > 0) {
     for (int pass = 0; pass < 2; ++pass) {
-      TRY(gram(ctx, nloc, nl, ka, XL, ldxl, Y, ldy, S, nl));
-      CUBLAS_TRY(ctx, cublasZgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)nl, &kMinusOne,
-                                  zc(XL), (int)ldxl, S, (int)nl, &kOne, zc(Y), (int)ldy));
+      TRY(gram<T>(ctx, nloc, nl, ka, XL, ldxl, Y, ldy, G, nl));
+      CUBLAS_TRY(ctx, S::gemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)nl, &mone, Xt, (int)ldxl, G,
+                              (int)nl, &one, Yt, (int)ldy));
     }
   }
   // CholeskyQR2: S = Y^H Y = R^H R, Y <- Y R^{-1}, twice
   bool ok = true;
   int lw = 0;
-  CUSOLVER_TRY(ctx, cusolverDnZpotrf_bufferSize(ctx->cusolver, CUBLAS_FILL_MODE_UPPER, (int)ka, S, (int)ka, &lw));
-  TRY(ensure(ctx, ctx->solver_ws, sizeof(cuDoubleComplex) * (size_t)std::max(lw, 1)));
+  CUSOLVER_TRY(ctx, S::potrf_bs(ctx->cusolver, (int)ka, G, (int)ka, &lw));
+  TRY(ensure(ctx, ctx->solver_ws, sizeof(T) * (size_t)std::max(lw, 1)));
   for (int pass = 0; pass < 2 && ok; ++pass) {
-    TRY(gram(ctx, nloc, ka, ka, Y, ldy, Y, ldy, S, ka));
-    CUSOLVER_TRY(ctx, cusolverDnZpotrf(ctx->cusolver, CUBLAS_FILL_MODE_UPPER, (int)ka, S, (int)ka,
-                                       zc(ctx->solver_ws.ptr), lw, info));
+    TRY(gram<T>(ctx, nloc, ka, ka, Y, ldy, Y, ldy, G, ka));
+    CUSOLVER_TRY(ctx, S::potrf(ctx->cusolver, (int)ka, G, (int)ka, static_cast<T*>(ctx->solver_ws.ptr), lw, info));
     int hinfo = 0;
     CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
@@ -257,13 +373,12 @@ chfsi_status qr_impl(chfsi_ctx ctx, int64_t n, int64_t nloc, const void* XL, int
       ok = false;
       break;
     }
-    CUBLAS_TRY(ctx, cublasZtrsm(ctx->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
-                                CUBLAS_DIAG_NON_UNIT, (int)nloc, (int)ka, &kOne, S, (int)ka, zc(Y), (int)ldy));
+    CUBLAS_TRY(ctx, S::trsm_ru(ctx->cublas, (int)nloc, (int)ka, G, (int)ka, Yt, (int)ldy));
   }
   if (ok) {  // orthogonality check ||Q^H Q - I||_max <= 1e-12
-    TRY(gram(ctx, nloc, ka, ka, Y, ldy, Y, ldy, S, ka));
+    TRY(gram<T>(ctx, nloc, ka, ka, Y, ldy, Y, ldy, G, ka));
     double* e = reinterpret_cast<double*>(info + 4);
-    CHFSI_CUDA_TRY(ctx, launch_orth_err(ka, reinterpret_cast<double2*>(S), ka, e, ctx->stream));
+    CHFSI_CUDA_TRY(ctx, launch_orth_err(ka, reinterpret_cast<const D*>(G), ka, e, ctx->stream));
     ctx->launches++;
     double he = 0;
     CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&he, e, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -272,58 +387,62 @@ chfsi_status qr_impl(chfsi_ctx ctx, int64_t n, int64_t nloc, const void* XL, int
   }
   if (!ok) {
     if (used_fallback) *used_fallback = 1;
-    TRY(householder(ctx, n, nloc, Y, ldy, ka));
+    TRY(householder<T>(ctx, n, nloc, Y, ldy, ka));
   }
   return CHFSI_OK;
 }
 
 // ---------------------------------------------------------------------------------------------
 // Rayleigh-Ritz with residuals. Q (nloc x ka) in/out. mu (host, ascending), resid (host, nullable).
-chfsi_status rr_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh, void* Q,
-                     int64_t ldq, int64_t ka, double normH, double* mu, double* resid) {
+template <typename T>
+chfsi_status rr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh, void* Q,
+                  int64_t ldq, int64_t ka, double normH, double* mu, double* resid) {
+  using S = Sc<T>;
+  using D = typename S::D;
+  const T one = S::one(), zero = S::zero();
+  const size_t eb = sizeof(T);
   if (ka == 0) return CHFSI_OK;
-  const size_t blk = sizeof(double) * 2 * (size_t)nloc * ka;
+  const size_t blk = eb * (size_t)nloc * ka;
   TRY(ensure(ctx, ctx->w1, blk));
   TRY(ensure(ctx, ctx->w2, blk));
   TRY(ensure(ctx, ctx->w3, blk));
-  TRY(ensure(ctx, ctx->small1, sizeof(double) * 2 * (size_t)ka * ka + 64));
+  TRY(ensure(ctx, ctx->small1, eb * (size_t)ka * ka + 64));
   TRY(ensure(ctx, ctx->small2, sizeof(double) * (size_t)(4 * ka + 64)));
   TRY(ensure(ctx, ctx->devinfo, 64));
-  cuDoubleComplex* W = zc(ctx->w1.ptr);  // H Q
-  cuDoubleComplex* Yr = zc(ctx->w2.ptr);  // Q V
-  cuDoubleComplex* HY = zc(ctx->w3.ptr);  // (H Q) V
-  cuDoubleComplex* G = zc(ctx->small1.ptr);
+  T* W = static_cast<T*>(ctx->w1.ptr);   // H Q
+  T* Yr = static_cast<T*>(ctx->w2.ptr);  // Q V
+  T* HY = static_cast<T*>(ctx->w3.ptr);  // (H Q) V
+  T* G = static_cast<T*>(ctx->small1.ptr);
+  const T* Qt = static_cast<const T*>(Q);
   double* dmu = static_cast<double*>(ctx->small2.ptr);
   double* dr = dmu + ka;
   double* dn = dr + ka;
   int* info = static_cast<int*>(ctx->devinfo.ptr);
-  TRY(hmul_impl(ctx, n, row0, nloc, Hp, ldh, Q, ldq, ka, W, nloc));
-  TRY(gram(ctx, nloc, ka, ka, Q, ldq, W, nloc, G, ka));
-  CHFSI_CUDA_TRY(ctx, launch_hermitize(ka, reinterpret_cast<double2*>(G), ka, ctx->stream));
+  TRY(hmul_impl(ctx, n, row0, nloc, Hp, ldh, Q, ldq, ka, W, nloc, S::elem));
+  TRY(gram<T>(ctx, nloc, ka, ka, Q, ldq, W, nloc, G, ka));
+  CHFSI_CUDA_TRY(ctx, launch_hermitize(ka, reinterpret_cast<D*>(G), ka, ctx->stream));
   ctx->launches++;
   // small dense eigensolve: once, on rank 0, broadcast (identical bits on every rank)
   if (ctx->rank == 0) {
     int lw = 0;
-    CUSOLVER_TRY(ctx, cusolverDnZheevd_bufferSize(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER,
-                                                  (int)ka, G, (int)ka, dmu, &lw));
-    TRY(ensure(ctx, ctx->solver_ws, sizeof(cuDoubleComplex) * (size_t)std::max(lw, 1)));
-    CUSOLVER_TRY(ctx, cusolverDnZheevd(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, (int)ka, G,
-                                       (int)ka, dmu, zc(ctx->solver_ws.ptr), lw, info));
+    CUSOLVER_TRY(ctx, S::heevd_bs(ctx->cusolver, (int)ka, G, (int)ka, dmu, &lw));
+    TRY(ensure(ctx, ctx->solver_ws, eb * (size_t)std::max(lw, 1)));
+    CUSOLVER_TRY(ctx, S::heevd(ctx->cusolver, (int)ka, G, (int)ka, dmu, static_cast<T*>(ctx->solver_ws.ptr), lw, info));
   }
-  TRY(comm_bcast(ctx, reinterpret_cast<double*>(G), (size_t)2 * ka * ka, 0));
+  TRY(comm_bcast(ctx, reinterpret_cast<double*>(G), (size_t)S::elem * ka * ka, 0));
   TRY(comm_bcast(ctx, dmu, (size_t)ka, 0));
-  CUBLAS_TRY(ctx, cublasZgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)ka, &kOne, zc(Q),
-                              (int)ldq, G, (int)ka, &kZero, Yr, (int)nloc));
+  CUBLAS_TRY(ctx, S::gemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)ka, &one, Qt, (int)ldq, G,
+                          (int)ka, &zero, Yr, (int)nloc));
   if (resid) {
-    CUBLAS_TRY(ctx, cublasZgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)ka, &kOne, W,
-                                (int)nloc, G, (int)ka, &kZero, HY, (int)nloc));
-    CHFSI_CUDA_TRY(ctx, launch_resid2(nloc, ka, reinterpret_cast<double2*>(HY), nloc, reinterpret_cast<double2*>(Yr),
+    CUBLAS_TRY(ctx, S::gemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)ka, &one, W, (int)nloc, G,
+                            (int)ka, &zero, HY, (int)nloc));
+    CHFSI_CUDA_TRY(ctx, launch_resid2(nloc, ka, reinterpret_cast<const D*>(HY), nloc, reinterpret_cast<const D*>(Yr),
                                       nloc, dmu, dr, ctx->stream));
-    CHFSI_CUDA_TRY(ctx, launch_colnorm2(nloc, ka, reinterpret_cast<double2*>(Yr), nloc, dn, ctx->stream));
+    CHFSI_CUDA_TRY(ctx, launch_colnorm2(nloc, ka, reinterpret_cast<const D*>(Yr), nloc, dn, ctx->stream));
     ctx->launches += 2;
     TRY(comm_allreduce_sum(ctx, dr, (size_t)2 * ka));  // dr and dn are contiguous
   }
-  CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(Q, 16 * ldq, Yr, 16 * nloc, 16 * nloc, ka, cudaMemcpyDeviceToDevice,
+  CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(Q, eb * ldq, Yr, eb * nloc, eb * nloc, ka, cudaMemcpyDeviceToDevice,
                                         ctx->stream));
   std::vector<double> h(3 * ka);
   CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), dmu, sizeof(double) * (resid ? 3 * ka : ka), cudaMemcpyDeviceToHost,
@@ -341,6 +460,33 @@ chfsi_status rr_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const
     if (resid) resid[j] = std::sqrt(h[ka + j]) / (std::sqrt(h[2 * ka + j]) * normH);
   }
   return CHFSI_OK;
+}
+
+// explicit instantiations + the complex entry points used by the C-ABI and the solver
+template chfsi_status lanczos_t<cuDoubleComplex>(chfsi_ctx, int64_t, int64_t, int64_t, const void*, int64_t, int32_t,
+                                                 uint64_t, double*, double*, double*);
+template chfsi_status lanczos_t<double>(chfsi_ctx, int64_t, int64_t, int64_t, const void*, int64_t, int32_t, uint64_t,
+                                        double*, double*, double*);
+template chfsi_status qr_t<cuDoubleComplex>(chfsi_ctx, int64_t, int64_t, const void*, int64_t, int64_t, void*, int64_t,
+                                            int64_t, int32_t*);
+template chfsi_status qr_t<double>(chfsi_ctx, int64_t, int64_t, const void*, int64_t, int64_t, void*, int64_t, int64_t,
+                                   int32_t*);
+template chfsi_status rr_t<cuDoubleComplex>(chfsi_ctx, int64_t, int64_t, int64_t, const void*, int64_t, void*, int64_t,
+                                            int64_t, double, double*, double*);
+template chfsi_status rr_t<double>(chfsi_ctx, int64_t, int64_t, int64_t, const void*, int64_t, void*, int64_t, int64_t,
+                                   double, double*, double*);
+
+chfsi_status lanczos_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
+                          int32_t steps, uint64_t seed, double* theta_min, double* theta_max, double* upper) {
+  return lanczos_t<cuDoubleComplex>(ctx, n, row0, nloc, Hp, ldh, steps, seed, theta_min, theta_max, upper);
+}
+chfsi_status qr_impl(chfsi_ctx ctx, int64_t n, int64_t nloc, const void* XL, int64_t ldxl, int64_t nl, void* Y,
+                     int64_t ldy, int64_t ka, int32_t* used_fallback) {
+  return qr_t<cuDoubleComplex>(ctx, n, nloc, XL, ldxl, nl, Y, ldy, ka, used_fallback);
+}
+chfsi_status rr_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh, void* Q,
+                     int64_t ldq, int64_t ka, double normH, double* mu, double* resid) {
+  return rr_t<cuDoubleComplex>(ctx, n, row0, nloc, Hp, ldh, Q, ldq, ka, normH, mu, resid);
 }
 
 }  // namespace chfsi

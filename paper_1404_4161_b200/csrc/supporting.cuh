@@ -1,6 +1,8 @@
 // supporting.cuh -- internal entry points of the supporting ChFSI steps (supporting.cu), used by the
 // public C-ABI wrappers and by the sequence solver (solver.cu).
 #pragma once
+#include <cuComplex.h>
+
 #include "ctx.cuh"
 
 namespace chfsi {
@@ -13,5 +15,16 @@ chfsi_status qr_impl(chfsi_ctx ctx, int64_t n, int64_t nloc, const void* XL, int
 // Rayleigh-Ritz on Q (in/out); mu host[ka] ascending; resid host[ka] nullable (R8).
 chfsi_status rr_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh, void* Q,
                      int64_t ldq, int64_t ka, double normH, double* mu, double* resid);
+
+// the same steps templated on the scalar (cuDoubleComplex: Hermitian; double: real symmetric, NEXT-3)
+template <typename T>
+chfsi_status lanczos_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh, int32_t steps,
+                       uint64_t seed, double* theta_min, double* theta_max, double* upper);
+template <typename T>
+chfsi_status qr_t(chfsi_ctx ctx, int64_t n, int64_t nloc, const void* XL, int64_t ldxl, int64_t nl, void* Y, int64_t ldy,
+                  int64_t ka, int32_t* used_fallback);
+template <typename T>
+chfsi_status rr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh, void* Q,
+                  int64_t ldq, int64_t ka, double normH, double* mu, double* resid);
 
 }  // namespace chfsi

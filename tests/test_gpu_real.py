@@ -99,3 +99,38 @@ def test_filter_real_multirank(gpu_lib):
     Y = np.concatenate([y.cpu().numpy() for y in Ys], axis=0)
     Yo, _ = O.chebyshev_filter(H.astype(complex), Y0.astype(complex), deg, l1, c, e)
     assert (np.linalg.norm(Y - Yo.real, axis=0) / np.linalg.norm(Yo.real, axis=0)).max() <= 1e-11
+
+
+def real_known(n, nd, seed):
+    """Real symmetric H = Q diag(lam) Q^T, Q a product of 8 real Householder reflectors (numpy)."""
+    import gen as G
+
+    lam = G.spectrum(n, nd)
+    rng = np.random.default_rng(seed)
+    Q = np.eye(n)
+    for _ in range(8):
+        v = rng.standard_normal((n, 1))
+        Q = Q - 2.0 * (Q @ v) @ v.T / (v.T @ v).item()
+    H = Q @ np.diag(lam) @ Q.T
+    return np.asfortranarray((H + H.T) / 2), lam
+
+
+def test_solve_real_known_spectrum_and_vs_oracle(gpu_lib):
+    n, nd, nev, nex = 512, 480, 32, 16
+    H, lam = real_known(n, nd, 4)
+    X0 = np.asfortranarray(np.random.default_rng(1).standard_normal((n, nev + nex)))
+    ctx = gpu_lib.Context(0)
+    Hd = gpu_lib.to_colmajor(H, real=True)
+    Xd = gpu_lib.to_colmajor(X0, real=True)
+    out = ctx.solve_sequence(lambda ell: Hd, 1, Xd, nev, nex, 1e-10, deg_cap=20, seed=3, real=True)
+    X = Xd.cpu().numpy()[:, :nev]
+    ctx.close()
+    assert out["status"] == 0
+    got = out["lam"][0]
+    assert np.max(np.abs(got - lam[:nev]) / np.abs(lam[:nev])) <= 1e-10
+    res = np.linalg.norm(H @ X - X * got, axis=0) / 40.0
+    assert res.max() <= 1e-10
+    assert np.abs(X.T @ X - np.eye(nev)).max() <= 1e-12
+    ro = O.chfsi_solve(H.astype(complex), X0.astype(complex), nev, nex, 1e-10, 20, seed=3)
+    assert np.max(np.abs(got - ro["lam"]) / np.abs(ro["lam"])) <= 1e-10
+    assert out["reports"][0]["filter_flops"] == pytest.approx(2.0 * n * n * out["reports"][0]["matvecs_filter"])
