@@ -194,6 +194,8 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--emulate-ranks", type=int, default=1,
+                    help="run the N > 1 path as P threads on GPU 0 (correctness of the sharded path; not a timing)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
@@ -209,15 +211,15 @@ def main():
         run_reference(args, cf, rank, world)
         return
 
-    import numpy as np
+    if args.emulate_ranks > 1:
+        run_emulated(args, cf)
+        return
     import torch
 
-    import gen as G
     import paper_1404_4161_b200 as chfsi
 
     torch.cuda.set_device(local_rank)
-    dist = None
-    comm = None
+    group = None
     if world > 1:
         import torch.distributed as dist
 
@@ -228,7 +230,105 @@ def main():
         # the library owns its NCCL communicator: rank 0's ncclUniqueId is broadcast over torch.distributed
         obj = [chfsi.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        comm = obj[0]
+        group = TorchGroup(dist, obj[0])
+    rank_main(args, cf, rank, world, local_rank, group)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+class TorchGroup:
+    """N > 1 ranks = processes under torchrun; the library's NCCL communicator from a broadcast id."""
+
+    def __init__(self, dist, nccl_id):
+        self.dist, self.nccl_id = dist, nccl_id
+
+    def context(self, chfsi, local_rank, rank, world):
+        return chfsi.Context(local_rank, nccl_id=self.nccl_id, rank=rank, nranks=world)
+
+    def barrier(self):
+        import torch
+
+        torch.cuda.synchronize()
+        self.dist.barrier()
+        torch.cuda.synchronize()
+
+    def max(self, x):
+        return max_over_ranks(x, self.dist, "cuda")
+
+
+class ThreadGroup:
+    """--emulate-ranks P: P ranks as threads on GPU 0 (chfsi local group, one stream each). Runs the whole
+    N > 1 code path of this script (row panels, packed operands, collectives, reductions) on one GPU;
+    its timings are not multi-GPU timings (the ranks share one device)."""
+
+    def __init__(self, P):
+        import threading
+
+        import paper_1404_4161_b200 as chfsi
+
+        self.P = P
+        self.lg = chfsi.LocalGroup(P)
+        self.bar = threading.Barrier(P)
+        self.vals = [0.0] * P
+
+    def context(self, chfsi, local_rank, rank, world):
+        import torch
+
+        return chfsi.Context(0, stream=torch.cuda.current_stream(), local_group=self.lg, rank=rank)
+
+    def barrier(self):
+        import torch
+
+        torch.cuda.current_stream().synchronize()
+        self.bar.wait()
+
+    def max(self, x):
+        import threading
+
+        rank = threading.current_thread().rank
+        self.vals[rank] = x
+        self.bar.wait()
+        m = max(self.vals)
+        self.bar.wait()
+        return m
+
+
+def run_emulated(args, cf):
+    import threading
+
+    import torch
+
+    P = args.emulate_ranks
+    group = ThreadGroup(P)
+    errs = []
+
+    def work(r):
+        threading.current_thread().rank = r
+        try:
+            s = torch.cuda.Stream(device=0)
+            with torch.cuda.stream(s):
+                rank_main(args, cf, r, P, 0, group)
+        except BaseException as ex:  # surfaced after join
+            errs.append(ex)
+            group.bar.abort()
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+
+
+def rank_main(args, cf, rank, world, local_rank, group):
+    import numpy as np
+    import torch
+
+    import gen as G
+    import paper_1404_4161_b200 as chfsi
+    from gen.configs import DEG0, LANCZOS_STEPS, MAX_LOOPS
+
     n, nev, nex = cf["n"], cf["nev"], cf["nex"]
     k = nev + nex
     row0, nloc = rank_rows(n, world, rank)
@@ -245,18 +345,21 @@ def main():
         d.copy_(hp)
         dev_H.append(d.t())
     X0 = G.start_basis(n, k, cf["seed"], row0, nloc)
-    torch.cuda.synchronize()
+    torch.cuda.current_stream().synchronize()
     t_gen = time.perf_counter() - t_gen
 
-    ctx = chfsi.Context(local_rank, nccl_id=comm, rank=rank, nranks=world) if world > 1 else chfsi.Context(local_rank)
+    ctx = group.context(chfsi, local_rank, rank, world) if group else chfsi.Context(local_rank)
     ctx.reserve(n, nloc, k)
     stream = torch.cuda.current_stream()
 
     def barrier():
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
+        if group:
+            group.barrier()
+        else:
             torch.cuda.synchronize()
+
+    def rmax(x):
+        return group.max(x) if group else x
 
     def run_pass(e2e: bool):
         Xd = chfsi.to_colmajor(X0)
@@ -269,7 +372,8 @@ def main():
             if ell == W:
                 barrier()
                 launches["start"] = ctx.kernel_launches
-                sampler.start()
+                if rank == 0:
+                    sampler.start()
                 ev["start"] = torch.cuda.Event(enable_timing=True)
                 ev["start"].record(stream)
             if e2e and ell >= W:
@@ -278,22 +382,22 @@ def main():
             return dev_H[ell]
 
         out = ctx.solve_sequence(get_h, nprob, Xd, nev, nex, cf["tol"], deg_cap=cf["cap"], deg0=DEG0,
-                                 max_loops=MAX_LOOPS, lanczos_steps=LANCZOS_STEPS, seed=cf["seed"])
+                                 max_loops=MAX_LOOPS, lanczos_steps=LANCZOS_STEPS, seed=cf["seed"], n=n, row0=row0)
         if e2e:
-            xh = Xd.cpu()  # the final block read back (part of the last step)
+            Xd.cpu()  # the final block read back (part of the last step)
         ev["end"] = torch.cuda.Event(enable_timing=True)
         ev["end"].record(stream)
         barrier()
-        clocks = sampler.stop()
-        ms = max_over_ranks(ev["start"].elapsed_time(ev["end"]), dist, "cuda")
+        clocks = sampler.stop() if rank == 0 else None
+        ms = rmax(ev["start"].elapsed_time(ev["end"]))
         launches["n"] = ctx.kernel_launches - launches["start"]
         return out, ms, clocks, launches["n"]
 
     out, ms, clocks, nlaunch = run_pass(False)
     reps = out["reports"][W:]
     flops = sum(r["filter_flops"] for r in reps)
-    t_filter = max_over_ranks(sum(r["t_filter"] for r in reps), dist, "cuda")
-    t_k1 = max_over_ranks(sum(r["t_filter_kernel"] for r in reps), dist, "cuda")
+    t_filter = rmax(sum(r["t_filter"] for r in reps))
+    t_k1 = rmax(sum(r["t_filter_kernel"] for r in reps))
     k1_launches = sum(r["filter_launches"] for r in reps)
     value = flops / (ms * 1e-3) / 1e12
     filt_tf = flops / t_filter / 1e12  # whole filter calls (incl. the Y -> state copy, finite check)
@@ -335,27 +439,31 @@ def main():
     res_max = float(np.max(out["resid"][W:]))
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": K, "warmup": W,
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": 1 if args.emulate_ranks > 1 else world,
+            "steps": K, "warmup": W,
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: ChFSI sequence, one eigenproblem per step", "n": n,
                        "nev": nev, "nex": nex, "deg_cap": cf["cap"], "tol": cf["tol"], "delta": cf["delta"],
                        "problems": f"{W} warm-up + {K} timed of the correlated sequence",
-                       "parallelism": f"1-D row panels over {world} GPU(s)" if world > 1 else "single GPU",
+                       "parallelism": (f"1-D row panels over {world} emulated ranks on one GPU" if args.emulate_ranks > 1
+                                       else f"1-D row panels over {world} GPU(s)" if world > 1 else "single GPU"),
                        "l2": "inputs larger than L2 (H panel per problem >> 126 MB)"},
             "time_per_eigenproblem_s": ms / K / 1e3,
             "filter_kernel_tflops": filt_tf, "frac_of_peak": filt_tf / FP64_PEAK_TFLOPS,
             "filter_share_of_step": t_filter / (ms * 1e-3),
             "loops_per_problem": [r["loops"] for r in reps],
+            "phase_s_per_problem": {ph: sum(r[f"t_{ph}"] for r in reps) / len(reps)
+                                    for ph in ("lanczos", "filter", "qr", "rr", "opt", "total")},
             "matvecs_filter_per_problem": [r["matvecs_filter"] for r in reps],
             "converged": conv, "max_resid_over_tol": res_max / cf["tol"],
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": nlaunch,
             "input_generation_s": t_gen,
         }
+        if args.emulate_ranks > 1:
+            line["emulated_ranks"] = world
         print(json.dumps(line), flush=True)
     ctx.close()
-    if dist:
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -37,6 +37,8 @@ constexpr Variant kVariants[] = {
     {128, 16, 16, 0.800, 256, 16},  // 5: 8 warps, warp tile 16 x 16 (narrow blocks)
     {128, 32, 8, 0.960, 512, 16},   // 6: 16 warps, warp tile 32 x 8
     {128, 48, 16, 1.000, 384, 32},  // 7: 12 warps, warp tile 32 x 16 (34.9 TF/s at n=13000, k=624)
+    {128, 64, 16, 0.900, 256, 64},  // 8: 8 warps, warp tile 64 x 16 (measured slower; kept for sweeps)
+    {256, 32, 16, 0.970, 256, 64},  // 9: 8 warps, warp tile 64 x 16, BM 256 (best at exact 32-column fits)
 };
 
 }  // namespace
@@ -140,6 +142,10 @@ cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, cons
       return launch_cfg<128, 32, 32, 8, 5>(tmA, tmB, p, stream);
     case 7:
       return launch_cfg<128, 48, 32, 16, 4>(tmA, tmB, p, stream);
+    case 8:
+      return launch_cfg<128, 64, 64, 16, 4>(tmA, tmB, p, stream);
+    case 9:
+      return launch_cfg<256, 32, 64, 16, 3>(tmA, tmB, p, stream);
     // real symmetric (columns are real columns)
     case 100:
       return launch_cfg<128, 96, 32, 32, 3, false>(tmA, tmB, p, stream);

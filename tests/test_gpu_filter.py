@@ -11,7 +11,7 @@ import oracle as O
 from gen.configs import C4_INTERVAL, CONFIGS, c4_ramp
 
 pytestmark = pytest.mark.gpu
-VARIANTS = ["0", "1", "2", "3", "4", "5", "6", "7"]
+VARIANTS = ["0", "1", "2", "3", "4", "5", "6", "7", "8", "9"]
 
 
 def crand(rng, *shape):

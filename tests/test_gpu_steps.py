@@ -266,3 +266,20 @@ def test_solve_batch_independent_sequences(gpu_lib, ctx):
         assert o["status"] == 0
         np.testing.assert_allclose(o["lam"], s["lam"], rtol=1e-13)
         assert [r["loops"] for r in o["reports"]] == [r["loops"] for r in s["reports"]]
+
+
+def test_library_owned_nccl_communicator(gpu_lib):
+    """chfsi_nccl_unique_id + chfsi_ctx_create_nccl: NCCL is dlopen-ed, a communicator is created with
+    ncclCommInitRank (one rank on this one-GPU box) and destroyed with the context; the solver runs on it."""
+    cf = CONFIGS["c0"]
+    n, nev, nex = cf["n"], cf["nev"], cf["nex"]
+    uid = gpu_lib.nccl_unique_id()
+    assert len(uid) == 128
+    ctx = gpu_lib.Context(0, nccl_id=uid, rank=0, nranks=1)
+    w = G.wy(n, cf["nd"], cf["seed"])
+    Hd = gpu_lib.to_colmajor(w.full())
+    Xd = gpu_lib.to_colmajor(G.start_basis(n, nev + nex, cf["seed"]))
+    out = ctx.solve_sequence(lambda ell: Hd, 1, Xd, nev, nex, cf["tol"], deg_cap=cf["cap"], seed=cf["seed"])
+    ctx.close()
+    assert out["status"] == 0
+    assert np.max(np.abs(out["lam"][0] - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
