@@ -9,9 +9,11 @@ nev = 520, nex = 104, degree cap 36, tol 1e-10, H^(l+1) = H^(l) + 5e-4 * 40 * G_
             / device time of the K timed problems (inputs resident in HBM), TFLOP/s
   e2e     = the same, each problem's H^(l) copied host(pinned) -> device inside the timed region and
             the eigenvalues / residuals read back per problem
-  filter_kernel_tflops / frac_of_peak: the filter alone (its CUDA-event time inside the steps)
-  roofline: K1 (the filter kernel), FP64 tensor (DMMA) bound, peak = 37.07 TF measured on this pool
-            (profiles/r01_fp64_peaks.txt; MEASURED_PEAKS.json has no FP64 entry)
+  filter_kernel_tflops: the filter alone (its CUDA-event time inside the steps), same convention
+  roofline / frac_of_peak: K1 (the filter kernel), FP64 tensor (DMMA) bound, peak = 37.07 TF measured
+            on this pool (profiles/r01_fp64_peaks.txt; MEASURED_PEAKS.json has no FP64 entry), counted
+            in the real tensor flops K1 executes: 6 per complex MAC with Gauss's 3M product (default,
+            --zmul 3), 8 with the 4M embedding (--zmul 4)
 
 `python bench.py --gpus N --steps K --warmup W`; N > 1 under torchrun (row-panel sharding, NCCL).
 `--impl reference` times the CPU oracle (oracle/, plain C) on a bounded sample of the same workload.
@@ -194,6 +196,8 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--zmul", type=int, default=3, choices=[3, 4],
+                    help="complex filter arithmetic: 3 = Gauss 3M (default), 4 = 4M real embedding")
     ap.add_argument("--emulate-ranks", type=int, default=1,
                     help="run the N > 1 path as P threads on GPU 0 (correctness of the sharded path; not a timing)")
     args = ap.parse_args()
@@ -349,6 +353,7 @@ def rank_main(args, cf, rank, world, local_rank, group):
     t_gen = time.perf_counter() - t_gen
 
     ctx = group.context(chfsi, local_rank, rank, world) if group else chfsi.Context(local_rank)
+    ctx.set_complex_mult(args.zmul)
     ctx.reserve(n, nloc, k)
     stream = torch.cuda.current_stream()
 
@@ -419,12 +424,18 @@ def rank_main(args, cf, rank, world, local_rank, group):
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "achieved": k1_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": k1_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "kernel": "K1 filter_step_kernel (DMMA.8x8x4, TMA, persistent stream-K)",
+    # the tensor work K1 executes per complex multiply-add: 6 real flops (3M) or 8 (4M); `value` and
+    # filter_kernel_tflops keep the paper's ZGEMM convention 8 n^2 sum(deg)
+    tensor_per_zmac = 6.0 if args.zmul == 3 else 8.0
+    k1_tensor_tf = k1_tf * tensor_per_zmac / 8.0
+    roofline = {"bound": "tensor", "achieved": k1_tensor_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": k1_tensor_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "kernel": f"K1 filter_step_kernel ({args.zmul}M complex arithmetic, DMMA.8x8x4, TMA, persistent stream-K)",
                 "launches": k1_launches, "avg_launch_ms": 1e3 * t_k1 / max(k1_launches, 1),
-                "flops_per_launch": flops / max(k1_launches, 1),
-                "achieved_def": "8 n^2 sum(deg) over the timed problems / sum of CUDA-event times of the K1 launches",
+                "flops_per_launch": flops * tensor_per_zmac / 8.0 / max(k1_launches, 1),
+                "achieved_def": (f"{tensor_per_zmac:g} n^2 sum(deg) (the real FP64 tensor flops of the {args.zmul}M "
+                                 "complex product) over the timed problems / sum of CUDA-event times of the K1 launches"),
+                "achieved_zgemm_equivalent": k1_tf,
                 "peak_source": "measured FP64 DMMA peak (register-only DMMA loop, 1965 MHz), profiles/r01_fp64_peaks.txt"}
 
     cpu = None
@@ -450,7 +461,10 @@ def rank_main(args, cf, rank, world, local_rank, group):
                                        else f"1-D row panels over {world} GPU(s)" if world > 1 else "single GPU"),
                        "l2": "inputs larger than L2 (H panel per problem >> 126 MB)"},
             "time_per_eigenproblem_s": ms / K / 1e3,
-            "filter_kernel_tflops": filt_tf, "frac_of_peak": filt_tf / FP64_PEAK_TFLOPS,
+            "filter_kernel_tflops": filt_tf, "frac_of_peak": filt_tf * tensor_per_zmac / 8.0 / FP64_PEAK_TFLOPS,
+            "flop_convention": ("value / filter_kernel_tflops count 8 n^2 sum(deg) (ZGEMM convention); frac_of_peak "
+                                f"and roofline count the {tensor_per_zmac:g} real tensor flops per complex MAC "
+                                f"the {args.zmul}M kernel executes"),
             "filter_share_of_step": t_filter / (ms * 1e-3),
             "loops_per_problem": [r["loops"] for r in reps],
             "phase_s_per_problem": {ph: sum(r[f"t_{ph}"] for r in reps) / len(reps)

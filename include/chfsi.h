@@ -73,6 +73,27 @@ const char* chfsi_last_error(chfsi_ctx ctx);
 /* Number of kernels of this library launched on the context since creation (instrumentation). */
 int64_t chfsi_kernel_launches(chfsi_ctx ctx);
 
+/* Complex arithmetic of the filter kernel (and of H Q in Rayleigh-Ritz): mults = 3 selects Gauss's
+ * 3-multiplication form (default; 6 real flops per complex multiply-add: P1 = sum Re h Re y, P2 = sum
+ * Im h Im y, P3 = sum (Re h - Im h)(Re y + Im y); Re = P1 + P2, Im = P3 - P1 + P2 for conj(h) y),
+ * mults = 4 the 4M real embedding (8 real flops). Both compute the same p_m(H) Y of Alg 2
+ * to rounding; 3M trades a normwise-equivalent error bound (a few ulps more on the imaginary parts)
+ * for 25 % fewer tensor-core operations and keeps a (Re H - Im H) plane of the panel (8 bytes per
+ * entry) in the context workspace. The environment variable CHFSI_ZMUL=4 selects 4M at context
+ * creation. Errors: CHFSI_ERR_ARG for a null ctx or mults not in {3, 4}. */
+chfsi_status chfsi_ctx_set_complex_mult(chfsi_ctx ctx, int32_t mults);
+
+/* nranks > 1 only: overlap of the per-step exchange with the filter's MMAs (BASELINE.json north_star
+ * "Transfers overlap the next panel's MMA"; SURVEY 8(e) "Overlap"). The active columns of every filter
+ * step are cut into G contiguous column groups of >= group_cols columns (G <= 16; group_cols = 0: one
+ * group, no overlap); group g's in-place allgather runs on a library-owned communication stream while
+ * the filter kernel of group g+1 runs on the ctx stream (CUDA-event ordered, no host synchronisation).
+ * The contraction order per output element is unchanged, so results agree with G = 1 to rounding of
+ * the stream-K partial sums. sm_reserve SMs are left out of the filter kernel's persistent grid for the
+ * collective's thread blocks. Defaults: group_cols = 128, sm_reserve = 0. Errors: CHFSI_ERR_ARG for a
+ * null ctx, negative values or sm_reserve >= the SM count. Ignored at nranks == 1. */
+chfsi_status chfsi_ctx_set_pipeline(chfsi_ctx ctx, int32_t group_cols, int32_t sm_reserve);
+
 /* Chebyshev filter -- Algorithm 2 with the three-term recurrence of eq:3term
  * (P:764-768), reading R1 (line 8's trailing term is Y_{i-1}), R2 (columns run to k), R3 (active
  * start s = #{j : deg[j] <= i} before step i).

@@ -25,7 +25,7 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_NOCONV", 4: "ERR_QR
           7: "ERR_NOMEM"}
 
 EXPORTS = ("chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_ctx_create_nccl", "chfsi_nccl_unique_id", "chfsi_ctx_reserve", "chfsi_ctx_destroy",
-           "chfsi_last_error", "chfsi_kernel_launches", "chfsi_local_group_create", "chfsi_local_group_destroy",
+           "chfsi_last_error", "chfsi_kernel_launches", "chfsi_ctx_set_pipeline", "chfsi_ctx_set_complex_mult", "chfsi_local_group_create", "chfsi_local_group_destroy",
            "chfsi_filter", "chfsi_filter_real", "chfsi_lanczos_bounds", "chfsi_qr", "chfsi_rayleigh_ritz", "chfsi_solve_sequence",
            "chfsi_reduce_generalized", "chfsi_back_transform", "chfsi_solve_batch", "chfsi_solve_sequence_real")
 
@@ -96,6 +96,10 @@ def lib():
         L.chfsi_last_error.restype = ctypes.c_char_p
         L.chfsi_kernel_launches.argtypes = [vp]
         L.chfsi_kernel_launches.restype = i64
+        L.chfsi_ctx_set_pipeline.argtypes = [vp, i32, i32]
+        L.chfsi_ctx_set_pipeline.restype = ctypes.c_int
+        L.chfsi_ctx_set_complex_mult.argtypes = [vp, i32]
+        L.chfsi_ctx_set_complex_mult.restype = ctypes.c_int
         L.chfsi_filter.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, i64, pi32, dbl, dbl, dbl, pi64]
         L.chfsi_filter_real.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, i64, pi32, dbl, dbl, dbl, pi64]
         L.chfsi_filter_real.restype = ctypes.c_int
@@ -228,6 +232,16 @@ class Context:
 
     def reserve(self, n, nloc, kmax):
         self._check(lib().chfsi_ctx_reserve(self.h, n, nloc, kmax))
+
+    def set_complex_mult(self, mults: int = 3):
+        """Complex filter / H Q arithmetic: 3 = Gauss 3M (default), 4 = 4M real embedding
+        (chfsi_ctx_set_complex_mult)."""
+        self._check(lib().chfsi_ctx_set_complex_mult(self.h, mults))
+
+    def set_pipeline(self, group_cols: int = 128, sm_reserve: int = 0):
+        """nranks > 1: column groups of >= group_cols overlap their allgather with the next group's
+        filter kernel (chfsi_ctx_set_pipeline; 0 = one group)."""
+        self._check(lib().chfsi_ctx_set_pipeline(self.h, group_cols, sm_reserve))
 
     # -- Alg 2 -------------------------------------------------------------------------------------
     def filter(self, Hp, Y, deg, lambda1, c, e, n=None, row0=0):

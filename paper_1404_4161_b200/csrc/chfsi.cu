@@ -4,11 +4,13 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "ctx.cuh"
 #include "filter_step.cuh"
+#include "small_kernels.cuh"
 
 namespace chfsi {
 
@@ -104,26 +106,29 @@ chfsi_status sk_workspace(chfsi_ctx ctx, const TileChoice& t, StepParams& p) {
   return CHFSI_OK;
 }
 
-// Common driver for one K1 launch over the active columns [col0, k) of the B operand.
+// The B operand of one K1 launch: its TMA map, the 3M plane's map, and the column coordinate of the
+// first active column.
 struct Operand {
-  CUtensorMap tm;
+  CUtensorMap tm, tm3;
   int32_t b_col0;
 };
 
-// Build the B-operand descriptor for the current step.
-//  p == 1: B = local state buffer (nloc x kcols, ld), column coordinate = absolute column.
-//  p > 1 : B = packed [rank][ka][nloc] buffer, column coordinate = column - col0.
-static chfsi_status b_operand(chfsi_ctx ctx, Operand* op, const void* buf, int64_t n_or_nloc, int64_t ld,
-                              int64_t kcols, int64_t col0, int nranks, int box_cols, int elem = 2) {
-  if (nranks == 1) {
-    op->b_col0 = (int32_t)col0;
-    return make_tmap_3d(ctx, &op->tm, buf, elem * n_or_nloc, kcols, 1, elem * ld, elem * ld * kcols, box_cols);
+// Build the B-operand descriptors for one launch over columns [col0, kcols) of `buf`.
+//  Column slots hold `rows` elements at a column stride of cs = cw * ld doubles, cw = elem (plain
+//  layout) or 3 (3M layout: 2 * ld complex doubles, then the y_r + y_i plane at offset 2 * ld).
+//  p == 1: buf = local state (rows = n), column coordinate = absolute column.
+//  p > 1 : buf = packed [rank][kcols - col0][cs] operand (rows = nloc), coordinate = column - col0.
+static chfsi_status b_operand(chfsi_ctx ctx, Operand* op, const double* buf, int64_t rows, int64_t ld,
+                              int64_t kcols, int64_t col0, int nranks, int box_cols, int elem, bool z3) {
+  const int64_t cs = (z3 ? 3 : elem) * ld;
+  const int64_t cols = nranks == 1 ? kcols : kcols - col0;
+  op->b_col0 = nranks == 1 ? (int32_t)col0 : 0;
+  chfsi_status st = make_tmap_3d(ctx, &op->tm, buf, elem * rows, cols, nranks, cs, cs * cols, box_cols);
+  if (st || !z3) {
+    op->tm3 = op->tm;  // unused outside 3M
+    return st;
   }
-  // packed [rank][ka][ld] (ld = nloc, rounded up to an even count for real data: TMA strides are
-  // multiples of 16 bytes)
-  op->b_col0 = 0;
-  const int64_t ka = kcols - col0;
-  return make_tmap_3d(ctx, &op->tm, buf, elem * n_or_nloc, ka, nranks, elem * ld, elem * ld * ka, box_cols);
+  return make_tmap_3d(ctx, &op->tm3, buf + 2 * ld, rows, cols, nranks, cs, cs * cols, box_cols);
 }
 
 // The A operand (H panel) through TMA needs a 16-byte row stride: real data with an odd ldh is first
@@ -140,36 +145,90 @@ static chfsi_status a_operand(chfsi_ctx ctx, const void** Hp, int64_t* ldh, int6
   return CHFSI_OK;
 }
 
+// 3M: the plane Re H - Im H of the panel (nloc rows x n, row stride ld3), rebuilt unless the solver
+// pinned it for this panel (ctx->h3_pin == Hp for the duration of one eigenproblem).
+chfsi_status h3_prepare(chfsi_ctx ctx, const void* Hp, int64_t ldh, int64_t n, int64_t nloc) {
+  const int64_t ld3 = round_up(n, 2);
+  chfsi_status st = ensure(ctx, ctx->h3, sizeof(double) * (size_t)ld3 * nloc);
+  if (st) return st;
+  CHFSI_CUDA_TRY(ctx, launch_h3_plane(n, nloc, static_cast<const double2*>(Hp), ldh, static_cast<double*>(ctx->h3.ptr),
+                                      ld3, ctx->stream));
+  ctx->launches++;
+  ctx->h3_ld = ld3;
+  return CHFSI_OK;
+}
+
+static chfsi_status a3_operand(chfsi_ctx ctx, CUtensorMap* m, const void* Hp, int64_t ldh, int64_t n, int64_t nloc,
+                               int box_rows, bool* built) {
+  if (!*built) {
+    if (ctx->h3_pin != Hp) {
+      chfsi_status st = h3_prepare(ctx, Hp, ldh, n, nloc);
+      if (st) return st;
+    }
+    *built = true;
+  }
+  return make_tmap_2d(ctx, m, ctx->h3.ptr, n, nloc, ctx->h3_ld, box_rows);
+}
+
+static inline TileChoice pick_tile(chfsi_ctx ctx, int elem, bool z3, int64_t nrows, int64_t ncols, int sms) {
+  (void)ctx;
+  if (elem == 1) return choose_filter_tile_real(nrows, ncols, sms);
+  return z3 ? choose_filter_tile_z3(nrows, ncols, sms) : choose_filter_tile(nrows, ncols, sms);
+}
+
 chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
                        const void* Q, int64_t ldq, int64_t k, void* out, int64_t ldo, int elem) {
   (void)row0;
   if (k == 0) return CHFSI_OK;
   const int p = ctx->nranks;
+  const bool z3 = elem == 2 && ctx->zmul == 3;
+  const int cw = z3 ? 3 : elem;
   const size_t eb = 8 * (size_t)elem;
-  TileChoice t = elem == 2 ? choose_filter_tile(nloc, k, ctx->num_sms) : choose_filter_tile_real(nloc, k, ctx->num_sms);
-  CUtensorMap tmA;
+  TileChoice t = pick_tile(ctx, elem, z3, nloc, k, ctx->num_sms);
+  CUtensorMap tmA, tmA3;
   chfsi_status st = a_operand(ctx, &Hp, &ldh, n, nloc, elem);
   if (st) return st;
   st = make_tmap_2d(ctx, &tmA, Hp, elem * n, nloc, elem * ldh, t.bm);
   if (st) return st;
+  tmA3 = tmA;
+  bool h3_built = false;
+  if (z3) {
+    st = a3_operand(ctx, &tmA3, Hp, ldh, n, nloc, t.bm, &h3_built);
+    if (st) return st;
+  }
   Operand op;
-  const void* bsrc = Q;
+  const double* bsrc = static_cast<const double*>(Q);
   int64_t bld = ldq;
-  const int64_t ldp = elem == 1 ? round_up(nloc, 2) : nloc;  // packed column stride
+  const int64_t ldp = (elem == 1 || z3) ? round_up(nloc, 2) : nloc;  // packed column stride (per plane)
   if (p > 1) {
-    // gather the full-height Q into R0 = [rank][k][ldp]
-    st = ensure(ctx, ctx->R0, sizeof(double) * elem * (size_t)ldp * p * (size_t)k);
+    // gather the full-height Q into R0 = [rank][k][cw * ldp]
+    st = ensure(ctx, ctx->R0, sizeof(double) * cw * (size_t)ldp * p * (size_t)k);
     if (st) return st;
     double* R = static_cast<double*>(ctx->R0.ptr);
-    double* mine = R + (size_t)elem * ldp * k * ctx->rank;
-    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(mine, eb * ldp, Q, eb * ldq, eb * nloc, k, cudaMemcpyDeviceToDevice,
-                                          ctx->stream));
-    st = comm_allgather_inplace(ctx, R, (size_t)elem * ldp * k);
+    double* mine = R + (size_t)cw * ldp * k * ctx->rank;
+    if (z3) {
+      CHFSI_CUDA_TRY(ctx, launch_pack_y3(nloc, k, static_cast<const double2*>(Q), ldq, mine, 3 * ldp, 2 * ldp,
+                                         ctx->stream));
+      ctx->launches++;
+    } else {
+      CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(mine, eb * ldp, Q, eb * ldq, eb * nloc, k, cudaMemcpyDeviceToDevice,
+                                            ctx->stream));
+    }
+    st = comm_allgather_inplace(ctx, R, (size_t)cw * ldp * k);
     if (st) return st;
     bsrc = R;
     bld = ldp;
+  } else if (z3) {  // Q -> L0 in the 3M column layout
+    const int64_t ldl = round_up(nloc, 2);
+    st = ensure(ctx, ctx->L0, sizeof(double) * 3 * (size_t)ldl * k);
+    if (st) return st;
+    CHFSI_CUDA_TRY(ctx, launch_pack_y3(nloc, k, static_cast<const double2*>(Q), ldq, static_cast<double*>(ctx->L0.ptr),
+                                       3 * ldl, 2 * ldl, ctx->stream));
+    ctx->launches++;
+    bsrc = static_cast<const double*>(ctx->L0.ptr);
+    bld = ldl;
   }
-  st = b_operand(ctx, &op, bsrc, p == 1 ? n : nloc, bld, k, 0, p, t.bnc, elem);
+  st = b_operand(ctx, &op, bsrc, p == 1 ? n : nloc, bld, k, 0, p, t.bnc, elem, z3);
   if (st) return st;
   StepParams sp{};
   sp.nrows = nloc;
@@ -190,11 +249,42 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
   schedule_filter_step(t, ctx->num_sms, sp);
   st = sk_workspace(ctx, t, sp);
   if (st) return st;
-  CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, sp, ctx->stream));
+  CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, tmA3, op.tm3, sp, ctx->stream));
   ctx->launches++;
   return CHFSI_OK;
 }
 
+// Column groups for the p > 1 pipeline: G contiguous ranges [gb[g], gb[g+1]) of the k columns, each
+// >= pipe_group_cols wide (G = 1 at p == 1: nothing to overlap).
+static std::vector<int64_t> filter_groups(chfsi_ctx ctx, int64_t k) {
+  int64_t G = 1;
+  if (ctx->nranks > 1 && ctx->pipe_group_cols > 0) G = std::max<int64_t>(1, std::min<int64_t>(k / ctx->pipe_group_cols, 16));
+  std::vector<int64_t> gb(G + 1);
+  for (int64_t g = 0; g <= G; ++g) gb[g] = g * k / G;
+  return gb;
+}
+
+static chfsi_status ensure_events(chfsi_ctx ctx, std::vector<cudaEvent_t>& v, size_t count, unsigned flags) {
+  while (v.size() < count) {
+    cudaEvent_t ev;
+    CHFSI_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ev, flags));
+    v.push_back(ev);
+  }
+  return CHFSI_OK;
+}
+
+static chfsi_status ensure_comm_stream(chfsi_ctx ctx, size_t groups) {
+  if (!ctx->comm_stream) CHFSI_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+  if (!ctx->join_ev) CHFSI_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+  chfsi_status st = ensure_events(ctx, ctx->grp_k, groups, cudaEventDisableTiming);
+  if (!st) st = ensure_events(ctx, ctx->grp_ag, groups, cudaEventDisableTiming);
+  return st;
+}
+
+// Alg 2 on this rank's rows. One K1 launch per (step, column group). At p > 1 the packed
+// B operand of group g lives at R + elem*ldp*p*gb[g] with layout [rank][ka_g][ldp]; the epilogue of
+// step i writes this rank's chunk of step i+1's operand, and an in-place allgather on the comm stream
+// completes it while K1 runs on the next group ("Overlap").
 chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
                          void* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c, double e,
                          bool check_finite, int elem) {
@@ -207,40 +297,69 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
   sigma[0] = e / (lambda1 - c);
   for (int i = 1; i < mk; ++i) sigma[i] = 1.0 / (2.0 / sigma[0] - sigma[i - 1]);
 
-  // elem = 2: complex128 (real embedding in K1), elem = 1: real symmetric (NEXT-3); sizes in doubles
+  // elem = 2: complex128 (K1 in 3M or 4M form), elem = 1: real symmetric (NEXT-3); sizes in doubles.
+  // cw = doubles per row of a column slot: elem, or 3 in the 3M layout [2 ld complex | ld plane]
+  const bool z3 = elem == 2 && ctx->zmul == 3;
+  const int cw = z3 ? 3 : elem;
   const size_t eb = 8 * (size_t)elem;  // bytes per element
   const int64_t ldl = round_up(nloc, 2);
-  chfsi_status st = ensure(ctx, ctx->L0, sizeof(double) * elem * (size_t)ldl * k);
-  if (!st) st = ensure(ctx, ctx->L1, sizeof(double) * elem * (size_t)ldl * k);
+  chfsi_status st = ensure(ctx, ctx->L0, sizeof(double) * cw * (size_t)ldl * k);
+  if (!st) st = ensure(ctx, ctx->L1, sizeof(double) * cw * (size_t)ldl * k);
   if (!st) st = ensure(ctx, ctx->flag, 64);
-  const int64_t ldp = elem == 1 ? round_up(nloc, 2) : nloc;  // packed column stride of R0 / R1
-  if (p > 1 && !st) st = ensure(ctx, ctx->R0, sizeof(double) * elem * (size_t)ldp * p * k);
-  if (p > 1 && !st) st = ensure(ctx, ctx->R1, sizeof(double) * elem * (size_t)ldp * p * k);
+  const int64_t ldp = (elem == 1 || z3) ? round_up(nloc, 2) : nloc;  // packed column stride (per plane)
+  if (p > 1 && !st) st = ensure(ctx, ctx->R0, sizeof(double) * cw * (size_t)ldp * p * k);
+  if (p > 1 && !st) st = ensure(ctx, ctx->R1, sizeof(double) * cw * (size_t)ldp * p * k);
   if (!st) st = a_operand(ctx, &Hp, &ldh, n, nloc, elem);
   if (st) return st;
+  const std::vector<int64_t> gb = filter_groups(ctx, k);
+  const int G = (int)gb.size() - 1;
+  if (p > 1) {
+    st = ensure_comm_stream(ctx, G);
+    if (st) return st;
+  }
+  const int sms = p > 1 ? std::max(1, ctx->num_sms - std::max(0, (int)ctx->pipe_sm_reserve)) : ctx->num_sms;
   double2* L[2] = {static_cast<double2*>(ctx->L0.ptr), static_cast<double2*>(ctx->L1.ptr)};
   double* R[2] = {static_cast<double*>(ctx->R0.ptr), static_cast<double*>(ctx->R1.ptr)};
+  auto region = [&](int b, int g) { return R[b] + (size_t)cw * ldp * p * gb[g]; };  // group g's packed operand
   int* flag = static_cast<int*>(ctx->flag.ptr);
   if (check_finite) CHFSI_CUDA_TRY(ctx, cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
   // Y_0 -> L0 (the caller's Y is the output and must never be the B operand)
-  CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(L[0], eb * ldl, Y, eb * ldy, eb * nloc, k, cudaMemcpyDeviceToDevice,
-                                        ctx->stream));
-  if (p > 1) {
-    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(R[0] + (size_t)elem * ldp * k * ctx->rank, eb * ldp, Y, eb * ldy,
-                                          eb * nloc, k, cudaMemcpyDeviceToDevice, ctx->stream));
-    st = comm_allgather_inplace(ctx, R[0], (size_t)elem * ldp * k);
-    if (st) return st;
+  if (z3) {
+    CHFSI_CUDA_TRY(ctx, launch_pack_y3(nloc, k, static_cast<const double2*>(Y), ldy, reinterpret_cast<double*>(L[0]),
+                                       3 * ldl, 2 * ldl, ctx->stream));
+    ctx->launches++;
+  } else {
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(L[0], eb * ldl, Y, eb * ldy, eb * nloc, k, cudaMemcpyDeviceToDevice,
+                                          ctx->stream));
   }
-  CUtensorMap tmA;
-  int last_bm = -1;
-  // CUDA events around every K1 launch (read back after the final synchronisation)
-  if ((int)ctx->k1_events.size() < 2 * (mk + 1)) {
-    for (int q = (int)ctx->k1_events.size(); q < 2 * (mk + 1); ++q) {
-      cudaEvent_t ev;
-      CHFSI_CUDA_TRY(ctx, cudaEventCreate(&ev));
-      ctx->k1_events.push_back(ev);
+  if (p > 1) {  // step 1's full-height operand: this rank's rows of each group, then one allgather per group
+    for (int g = 0; g < G; ++g) {
+      const int64_t w = gb[g + 1] - gb[g];
+      double* mine = region(0, g) + (size_t)cw * ldp * w * ctx->rank;
+      const char* ysrc = static_cast<const char*>(Y) + eb * ldy * gb[g];
+      if (z3) {
+        CHFSI_CUDA_TRY(ctx, launch_pack_y3(nloc, w, reinterpret_cast<const double2*>(ysrc), ldy, mine, 3 * ldp, 2 * ldp,
+                                           ctx->stream));
+        ctx->launches++;
+      } else {
+        CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(mine, eb * ldp, ysrc, eb * ldy, eb * nloc, w, cudaMemcpyDeviceToDevice,
+                                              ctx->stream));
+      }
+    }
+    CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->join_ev, ctx->stream));
+    CHFSI_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm_stream, ctx->join_ev, 0));
+    for (int g = 0; g < G; ++g) {
+      st = comm_allgather_inplace(ctx, region(0, g), (size_t)cw * ldp * (gb[g + 1] - gb[g]), ctx->comm_stream);
+      if (st) return st;
+      CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->grp_ag[g], ctx->comm_stream));
     }
   }
+  CUtensorMap tmA, tmA3;
+  int last_bm = -1;
+  bool h3_built = false;
+  // CUDA events around every K1 launch (read back after the final synchronisation)
+  st = ensure_events(ctx, ctx->k1_events, (size_t)2 * (mk + 1) * G, cudaEventDefault);
+  if (st) return st;
   int nev_used = 0;
   int64_t s = 0;  // active start s_i = #{j : deg[j] <= i}
   for (int i = 0; i < mk; ++i) {
@@ -248,66 +367,86 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     if (s >= k) break;
     int64_t s_next = s;
     while (s_next < k && deg[s_next] <= i + 1) ++s_next;
-    const int64_t ka = k - s;
-    TileChoice t = elem == 2 ? choose_filter_tile(nloc, ka, ctx->num_sms) : choose_filter_tile_real(nloc, ka, ctx->num_sms);
-    if (t.bm != last_bm) {
-      st = make_tmap_2d(ctx, &tmA, Hp, elem * n, nloc, elem * ldh, t.bm);
-      if (st) return st;
-      last_bm = t.bm;
-    }
     const int cur = i & 1, oth = cur ^ 1;
-    Operand op;
-    if (p == 1)
-      st = b_operand(ctx, &op, L[cur], n, ldl, k, s, 1, t.bnc, elem);
-    else
-      st = b_operand(ctx, &op, R[cur], nloc, ldp, k, s, p, t.bnc, elem);
-    if (st) return st;
-    StepParams sp{};
-    sp.nrows = nloc;
-    const int64_t kr = p == 1 ? elem * n : elem * nloc;
-    sp.kt_per_rank = (int32_t)((kr + kBK - 1) / kBK);
-    sp.num_kt = sp.kt_per_rank * p;
-    sp.a_rank_stride = (int32_t)(elem * nloc);
-    sp.col0 = (int32_t)s;
-    sp.col_end = (int32_t)k;
-    sp.fin_end = (int32_t)s_next;
-    sp.b_col0 = op.b_col0;
-    if (i == 0) {  // Y_1 = (sigma_1/e)(H - cI) Y_0
-      sp.a = sigma[0] / e;
-      sp.b = 0.0;
-      sp.flags = 1;
-    } else {  // Y_{i+1} = (2 sigma_{i+1}/e)(H - cI) Y_i - sigma_{i+1} sigma_i Y_{i-1}
-      sp.a = 2.0 * sigma[i] / e;
-      sp.b = sigma[i] * sigma[i - 1];
-      sp.flags = 3;
-    }
-    sp.c = c;
-    sp.y_cur = L[cur];
-    sp.ld_cur = ldl;
-    sp.y_prev = L[oth];
-    sp.ld_prev = ldl;
-    sp.y_next = L[oth];
-    sp.ld_next = ldl;
-    sp.out = static_cast<double2*>(Y);
-    sp.ld_out = ldy;
-    const int64_t ka_next = k - s_next;
-    if (p > 1 && ka_next > 0) {
-      sp.r_next = reinterpret_cast<double2*>(R[oth] + (size_t)elem * ldp * ka_next * ctx->rank);
-      sp.ld_r_next = ldp;
-    }
-    sp.nonfinite = check_finite ? flag : nullptr;
-    schedule_filter_step(t, ctx->num_sms, sp);
-    st = sk_workspace(ctx, t, sp);
-    if (st) return st;
-    CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used], ctx->stream));
-    CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, sp, ctx->stream));
-    CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used + 1], ctx->stream));
-    nev_used += 2;
-    ctx->launches++;
-    if (p > 1 && ka_next > 0) {
-      st = comm_allgather_inplace(ctx, R[oth], (size_t)elem * ldp * ka_next);
+    for (int g = 0; g < G; ++g) {
+      const int64_t c0 = std::max(s, gb[g]), ce = gb[g + 1];
+      if (c0 >= ce) continue;  // every column of this group has finished
+      const int64_t fin = std::min(std::max(s_next, c0), ce);
+      const int64_t ka = ce - c0, ka_next = ce - fin;
+      TileChoice t = pick_tile(ctx, elem, z3, nloc, ka, sms);
+      if (t.bm != last_bm) {
+        st = make_tmap_2d(ctx, &tmA, Hp, elem * n, nloc, elem * ldh, t.bm);
+        if (!st && z3) st = a3_operand(ctx, &tmA3, Hp, ldh, n, nloc, t.bm, &h3_built);
+        if (st) return st;
+        if (!z3) tmA3 = tmA;
+        last_bm = t.bm;
+      }
+      Operand op;
+      if (p == 1)
+        st = b_operand(ctx, &op, reinterpret_cast<const double*>(L[cur]), n, ldl, k, c0, 1, t.bnc, elem, z3);
+      else
+        st = b_operand(ctx, &op, region(cur, g), nloc, ldp, ce, c0, p, t.bnc, elem, z3);
       if (st) return st;
+      StepParams sp{};
+      sp.nrows = nloc;
+      const int64_t kr = p == 1 ? elem * n : elem * nloc;
+      sp.kt_per_rank = (int32_t)((kr + kBK - 1) / kBK);
+      sp.num_kt = sp.kt_per_rank * p;
+      sp.a_rank_stride = (int32_t)(elem * nloc);
+      sp.col0 = (int32_t)c0;
+      sp.col_end = (int32_t)ce;
+      sp.fin_end = (int32_t)fin;
+      sp.b_col0 = op.b_col0;
+      if (i == 0) {  // Y_1 = (sigma_1/e)(H - cI) Y_0
+        sp.a = sigma[0] / e;
+        sp.b = 0.0;
+        sp.flags = 1;
+      } else {  // Y_{i+1} = (2 sigma_{i+1}/e)(H - cI) Y_i - sigma_{i+1} sigma_i Y_{i-1}
+        sp.a = 2.0 * sigma[i] / e;
+        sp.b = sigma[i] * sigma[i - 1];
+        sp.flags = 3;
+      }
+      sp.c = c;
+      // state column stride in the kernel's units (double2 for complex, double for real); 3M: the
+      // plane of column j starts 2 * ldl doubles after it
+      const int64_t lds = z3 ? 3 * ldl / 2 : ldl;
+      sp.y_cur = L[cur];
+      sp.ld_cur = lds;
+      sp.y_prev = L[oth];
+      sp.ld_prev = lds;
+      sp.y_next = L[oth];
+      sp.ld_next = lds;
+      sp.y3_off = 2 * ldl;
+      sp.out = static_cast<double2*>(Y);
+      sp.ld_out = ldy;
+      if (p > 1 && ka_next > 0) {
+        sp.r_next = reinterpret_cast<double2*>(region(oth, g) + (size_t)cw * ldp * ka_next * ctx->rank);
+        sp.ld_r_next = z3 ? 3 * ldp / 2 : ldp;
+        sp.y3_off_r = 2 * ldp;
+      }
+      sp.nonfinite = check_finite ? flag : nullptr;
+      schedule_filter_step(t, sms, sp);
+      st = sk_workspace(ctx, t, sp);
+      if (st) return st;
+      // this group's operand for step i is complete once its allgather (comm stream) has landed
+      if (p > 1) CHFSI_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->grp_ag[g], 0));
+      CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used], ctx->stream));
+      CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, tmA3, op.tm3, sp, ctx->stream));
+      CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used + 1], ctx->stream));
+      nev_used += 2;
+      ctx->launches++;
+      if (p > 1 && ka_next > 0) {  // complete step i+1's operand of this group behind the next group's K1
+        CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->grp_k[g], ctx->stream));
+        CHFSI_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm_stream, ctx->grp_k[g], 0));
+        st = comm_allgather_inplace(ctx, region(oth, g), (size_t)cw * ldp * ka_next, ctx->comm_stream);
+        if (st) return st;
+        CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->grp_ag[g], ctx->comm_stream));
+      }
     }
+  }
+  if (p > 1) {  // nothing on the comm stream outlives the call
+    CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->join_ev, ctx->comm_stream));
+    CHFSI_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   }
   CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   for (int q = 0; q < nev_used; q += 2) {
@@ -358,6 +497,7 @@ static chfsi_status ctx_create_impl(chfsi_ctx* out, int32_t device, void* cuda_s
   ctx->num_sms = prop.multiProcessorCount;
   ctx->nccl_comm = nccl_comm;
   ctx->local_group = group;
+  if (const char* zm = getenv("CHFSI_ZMUL")) ctx->zmul = atoi(zm) == 4 ? 4 : 3;
   if (nccl_id) {
     memcpy(ctx->nccl_id, nccl_id, sizeof(ctx->nccl_id));
     ctx->nccl_id_valid = true;
@@ -403,15 +543,17 @@ chfsi_status chfsi_ctx_reserve(chfsi_ctx ctx, int64_t n, int64_t nloc, int64_t k
   if (!ctx || n < 1 || nloc < 1 || kmax < 1 || nloc > n) return CHFSI_ERR_ARG;
   cudaSetDevice(ctx->device);
   const size_t ldl = (size_t)round_up(nloc, 2);
-  const size_t blk = sizeof(double) * 2 * ldl * kmax;
+  const size_t blk = sizeof(double) * 3 * ldl * kmax;  // 3M column layout (the widest)
   chfsi_status st = CHFSI_OK;
   if (!st) st = ensure(ctx, ctx->L0, blk);
   if (!st) st = ensure(ctx, ctx->L1, blk);
   if (!st) st = ensure(ctx, ctx->flag, 64);
   if (ctx->nranks > 1) {
-    if (!st) st = ensure(ctx, ctx->R0, sizeof(double) * 2 * (size_t)n * kmax);
-    if (!st) st = ensure(ctx, ctx->R1, sizeof(double) * 2 * (size_t)n * kmax);
+    const size_t rb = sizeof(double) * 3 * (size_t)round_up(nloc, 2) * ctx->nranks * kmax;
+    if (!st) st = ensure(ctx, ctx->R0, rb);
+    if (!st) st = ensure(ctx, ctx->R1, rb);
   }
+  if (!st && ctx->zmul == 3) st = ensure(ctx, ctx->h3, sizeof(double) * (size_t)round_up(n, 2) * nloc);
   return st;
 }
 
@@ -420,12 +562,16 @@ void chfsi_ctx_destroy(chfsi_ctx ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   comm_destroy(ctx);
-  DevBuf* bufs[] = {&ctx->L0, &ctx->L1, &ctx->R0, &ctx->R1, &ctx->flag, &ctx->sk, &ctx->hpad, &ctx->w1, &ctx->w2, &ctx->w3, &ctx->w4,
+  DevBuf* bufs[] = {&ctx->h3, &ctx->L0, &ctx->L1, &ctx->R0, &ctx->R1, &ctx->flag, &ctx->sk, &ctx->hpad, &ctx->w1, &ctx->w2, &ctx->w3, &ctx->w4,
                     &ctx->small1, &ctx->small2, &ctx->small3, &ctx->solver_ws, &ctx->devinfo, &ctx->lz,
                     &ctx->ya,    &ctx->xl,     &ctx->tb,     &ctx->idx};
   for (DevBuf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   for (cudaEvent_t ev : ctx->k1_events) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : ctx->grp_k) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : ctx->grp_ag) cudaEventDestroy(ev);
+  if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->cublas) cublasDestroy(ctx->cublas);
   if (ctx->cusolver) cusolverDnDestroy(ctx->cusolver);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -435,6 +581,19 @@ void chfsi_ctx_destroy(chfsi_ctx ctx) {
 const char* chfsi_last_error(chfsi_ctx ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int64_t chfsi_kernel_launches(chfsi_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+chfsi_status chfsi_ctx_set_complex_mult(chfsi_ctx ctx, int32_t mults) {
+  if (!ctx || (mults != 3 && mults != 4)) return CHFSI_ERR_ARG;
+  ctx->zmul = mults;
+  return CHFSI_OK;
+}
+
+chfsi_status chfsi_ctx_set_pipeline(chfsi_ctx ctx, int32_t group_cols, int32_t sm_reserve) {
+  if (!ctx || group_cols < 0 || sm_reserve < 0 || sm_reserve >= ctx->num_sms) return CHFSI_ERR_ARG;
+  ctx->pipe_group_cols = group_cols;
+  ctx->pipe_sm_reserve = sm_reserve;
+  return CHFSI_OK;
+}
 
 static chfsi_status filter_entry(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
                                  void* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c,

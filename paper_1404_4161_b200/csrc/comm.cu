@@ -115,43 +115,42 @@ __global__ void sum_ranks_kernel(const double* const* src, int P, size_t count, 
 }
 
 // publish `buf`, wait until every rank has published and its producer work is ordered before ours
-void lg_enter(chfsi_ctx ctx, const void* buf) {
+void lg_enter(chfsi_ctx ctx, const void* buf, cudaStream_t st) {
   chfsi_local_group g = ctx->comm->local;
   g->bufs[ctx->rank] = buf;
-  cudaEventRecord(g->ready[ctx->rank], ctx->stream);
+  cudaEventRecord(g->ready[ctx->rank], st);
   g->barrier();
   for (int q = 0; q < g->P; ++q)
-    if (q != ctx->rank) cudaStreamWaitEvent(ctx->stream, g->ready[q], 0);
+    if (q != ctx->rank) cudaStreamWaitEvent(st, g->ready[q], 0);
 }
 
 // every rank's reads of the published buffers are ordered before anyone's later writes
-void lg_exit(chfsi_ctx ctx) {
+void lg_exit(chfsi_ctx ctx, cudaStream_t st) {
   chfsi_local_group g = ctx->comm->local;
-  cudaEventRecord(g->done[ctx->rank], ctx->stream);
+  cudaEventRecord(g->done[ctx->rank], st);
   g->barrier();
   for (int q = 0; q < g->P; ++q)
-    if (q != ctx->rank) cudaStreamWaitEvent(ctx->stream, g->done[q], 0);
+    if (q != ctx->rank) cudaStreamWaitEvent(st, g->done[q], 0);
   g->barrier();  // nobody re-records its events before all waits above were issued
 }
 
 }  // namespace
 
-chfsi_status comm_allgather_inplace(chfsi_ctx ctx, double* buf, size_t count) {
+chfsi_status comm_allgather_inplace(chfsi_ctx ctx, double* buf, size_t count, cudaStream_t st) {
   if (ctx->nranks == 1 || count == 0) return CHFSI_OK;
+  if (!st) st = ctx->stream;
   if (ctx->comm->local) {
     chfsi_local_group g = ctx->comm->local;
-    lg_enter(ctx, buf);
+    lg_enter(ctx, buf, st);
     for (int q = 0; q < g->P; ++q) {
       if (q == ctx->rank) continue;
       const double* src = static_cast<const double*>(g->bufs[q]) + count * q;
-      CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(buf + count * q, src, count * sizeof(double), cudaMemcpyDeviceToDevice,
-                                          ctx->stream));
+      CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(buf + count * q, src, count * sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
-    lg_exit(ctx);
+    lg_exit(ctx, st);
     return CHFSI_OK;
   }
-  return nccl_check(ctx,
-                    ctx->comm->allgather(buf + count * ctx->rank, buf, count, ncclDouble, ctx->comm->comm, ctx->stream),
+  return nccl_check(ctx, ctx->comm->allgather(buf + count * ctx->rank, buf, count, ncclDouble, ctx->comm->comm, st),
                     "ncclAllGather");
 }
 
@@ -168,7 +167,7 @@ chfsi_status comm_allreduce_sum(chfsi_ctx ctx, double* buf, size_t count) {
       CHFSI_CUDA_TRY(ctx, cudaMalloc(&c->scratch, sizeof(double) * (count + (size_t)g->P)));
       c->scratch_n = count + (size_t)g->P;
     }
-    lg_enter(ctx, buf);
+    lg_enter(ctx, buf, ctx->stream);
     const double** ptrs = reinterpret_cast<const double**>(c->scratch + count);
     std::vector<const double*> hp(g->P);
     for (int q = 0; q < g->P; ++q) hp[q] = static_cast<const double*>(g->bufs[q]);
@@ -177,7 +176,7 @@ chfsi_status comm_allreduce_sum(chfsi_ctx ctx, double* buf, size_t count) {
     sum_ranks_kernel<<<blocks, 256, 0, ctx->stream>>>(ptrs, g->P, count, c->scratch);
     CHFSI_CUDA_TRY(ctx, cudaGetLastError());
     ctx->launches++;
-    lg_exit(ctx);
+    lg_exit(ctx, ctx->stream);
     CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(buf, c->scratch, count * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
     // the pointer table is rewritten by the next call only after this stream's work: order it
     CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
@@ -191,11 +190,11 @@ chfsi_status comm_bcast(chfsi_ctx ctx, double* buf, size_t count, int root) {
   if (ctx->nranks == 1 || count == 0) return CHFSI_OK;
   if (ctx->comm->local) {
     chfsi_local_group g = ctx->comm->local;
-    lg_enter(ctx, buf);
+    lg_enter(ctx, buf, ctx->stream);
     if (ctx->rank != root)
       CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(buf, g->bufs[root], count * sizeof(double), cudaMemcpyDeviceToDevice,
                                           ctx->stream));
-    lg_exit(ctx);
+    lg_exit(ctx, ctx->stream);
     return CHFSI_OK;
   }
   return nccl_check(ctx, ctx->comm->bcast(buf, buf, count, ncclDouble, root, ctx->comm->comm, ctx->stream),

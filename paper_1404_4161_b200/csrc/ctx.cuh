@@ -67,6 +67,21 @@ struct chfsi_ctx_s {
   double k1_seconds = 0;
   int64_t k1_launches = 0;
   std::vector<cudaEvent_t> k1_events;
+  // p > 1 filter pipelining (SURVEY 8(e) "Overlap"): the active block is cut into column groups of
+  // >= pipe_group_cols columns; group g's allgather (comm_stream) overlaps group g+1's K1 (stream).
+  // pipe_sm_reserve SMs are left out of K1's persistent grid for the collective's CTAs.
+  int32_t pipe_group_cols = 128;
+  int32_t pipe_sm_reserve = 0;
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> grp_k, grp_ag;  // per group: K1 done (stream), allgather done (comm_stream)
+  cudaEvent_t join_ev = nullptr;
+  // complex filter arithmetic: 3 = Gauss 3M (default), 4 = the 4M real embedding (CHFSI_ZMUL=4 or
+  // chfsi_ctx_set_complex_mult); h3 = the Re H - Im H plane of the panel, valid for h3_pin while the
+  // solver holds one eigenproblem's H fixed
+  int zmul = 3;
+  chfsi::DevBuf h3;
+  int64_t h3_ld = 0;
+  const void* h3_pin = nullptr;
 
   // workspace
   chfsi::DevBuf L0, L1;          // filter local state (nloc x k each)
@@ -104,8 +119,9 @@ chfsi_status make_tmap_3d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64
 // Communication (comm.cu). With nranks == 1 every collective is a no-op / local copy.
 chfsi_status comm_init(chfsi_ctx ctx);
 void comm_destroy(chfsi_ctx ctx);
-// in-place allgather: buf holds nranks chunks of `count` doubles; chunk `rank` is the send part
-chfsi_status comm_allgather_inplace(chfsi_ctx ctx, double* buf, size_t count);
+// in-place allgather: buf holds nranks chunks of `count` doubles; chunk `rank` is the send part.
+// Enqueued on `st` (nullptr: the ctx stream).
+chfsi_status comm_allgather_inplace(chfsi_ctx ctx, double* buf, size_t count, cudaStream_t st = nullptr);
 chfsi_status comm_allreduce_sum(chfsi_ctx ctx, double* buf, size_t count);
 chfsi_status comm_bcast(chfsi_ctx ctx, double* buf, size_t count, int root);
 
@@ -114,6 +130,8 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
                          void* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c, double e,
                          bool check_finite, int elem = 2);
 // HQ: out (nloc x k) = H Q for Q (nloc x k, this rank's rows). Uses the K1 kernel, plain epilogue.
+// 3M: (re)build the Re H - Im H plane of the panel in ctx->h3
+chfsi_status h3_prepare(chfsi_ctx ctx, const void* Hp, int64_t ldh, int64_t n, int64_t nloc);
 chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
                        const void* Q, int64_t ldq, int64_t k, void* out, int64_t ldo, int elem = 2);
 

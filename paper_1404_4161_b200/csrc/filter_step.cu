@@ -7,18 +7,18 @@ namespace chfsi {
 
 namespace {
 
-template <int BM, int BNC, int WM, int WNC, int STAGES, bool CPLX = true>
-cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, const StepParams& p,
-                       cudaStream_t stream) {
-  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>;
-  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, CPLX>;
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M>
+cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3,
+                       const CUtensorMap& tmB3, const StepParams& p, cudaStream_t stream) {
+  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>;
+  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, MODE>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<p.grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tmA, tmB, p);
+  kern<<<p.grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tmA, tmB, tmA3, tmB3, p);
   return cudaGetLastError();
 }
 
@@ -107,6 +107,42 @@ TileChoice choose_filter_tile_real(int64_t nrows, int64_t ncols, int num_sms) {
   return TileChoice{rv[best].id, rv[best].bm, rv[best].bnc, rv[best].threads, rv[best].acc, rv[best].wnc};
 }
 
+TileChoice choose_filter_tile_z3(int64_t nrows, int64_t ncols, int num_sms) {
+  (void)num_sms;
+  // 3M variants: accumulators are 3 sets (P1, P2, P3) of (WM/8) x (WNC/8) 8x8 tiles
+  struct ZV {
+    int id, bm, bnc, wnc, threads, acc;
+    double eff;
+  };
+  // eff: measured full-width rates relative to 200 (n = 13000, k = 624: 45.2 / 42.0 / 32.4 / 41.8 /
+  // 30.2 TF/s ZGEMM-equivalent; profiles/r01_z3_variants.log)
+  static const ZV zv[] = {{200, 128, 48, 16, 384, 48, 1.0},  {201, 128, 32, 16, 256, 48, 0.93},
+                          {202, 128, 16, 8, 256, 24, 0.72},  {203, 64, 64, 16, 256, 48, 0.925},
+                          {204, 192, 32, 16, 384, 48, 0.67}};
+  const int nv = (int)(sizeof(zv) / sizeof(zv[0]));
+  const char* fs = getenv("CHFSI_FILTER_VARIANT_Z3");
+  const int forced = fs ? atoi(fs) : -1;
+  int best = 0;
+  double best_cost = 1e300;
+  for (int v = 0; v < nv; ++v) {
+    if (forced >= 0 && zv[v].id != forced) continue;
+    const int64_t tm = (nrows + zv[v].bm - 1) / zv[v].bm;
+    const int64_t units = (ncols + zv[v].wnc - 1) / zv[v].wnc;
+    const int64_t tn = (ncols + zv[v].bnc - 1) / zv[v].bnc;
+    const int64_t per = (units + tn - 1) / tn;
+    const int warps_m = zv[v].threads / 32 / (zv[v].bnc / zv[v].wnc);
+    const double active_warps = (double)per * warps_m;
+    const double occ = active_warps >= 8 ? 1.0 : 0.6 + 0.05 * active_warps;
+    const double cols = 0.3 * (double)(tn * per * zv[v].wnc) + 0.7 * (double)ncols;
+    const double cost = (double)tm * zv[v].bm * cols / (zv[v].eff * occ);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = v;
+    }
+  }
+  return TileChoice{zv[best].id, zv[best].bm, zv[best].bnc, zv[best].threads, zv[best].acc, zv[best].wnc};
+}
+
 void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
   const int64_t ncols = p.col_end - p.col0;
   const int64_t tm = (p.nrows + t.bm - 1) / t.bm, tn = (ncols + t.bnc - 1) / t.bnc;
@@ -124,38 +160,52 @@ void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
 size_t filter_partials_doubles(const TileChoice& t, int num_sms) { return (size_t)2 * num_sms * t.acc * t.threads; }
 
 cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                               const StepParams& p, cudaStream_t stream) {
+                               const CUtensorMap& tmA3, const CUtensorMap& tmB3, const StepParams& p,
+                               cudaStream_t stream) {
+#define LC(BM, BNC, WM, WNC, ST, MODE) launch_cfg<BM, BNC, WM, WNC, ST, MODE>(tmA, tmB, tmA3, tmB3, p, stream)
   switch (t.id) {
     case 0:
-      return launch_cfg<128, 32, 32, 16, 5>(tmA, tmB, p, stream);
+      return LC(128, 32, 32, 16, 5, kZ4M);
     case 1:
-      return launch_cfg<64, 64, 32, 16, 6>(tmA, tmB, p, stream);
+      return LC(64, 64, 32, 16, 6, kZ4M);
     case 2:
-      return launch_cfg<128, 64, 32, 32, 4>(tmA, tmB, p, stream);
+      return LC(128, 64, 32, 32, 4, kZ4M);
     case 3:
-      return launch_cfg<64, 32, 32, 16, 8>(tmA, tmB, p, stream);
+      return LC(64, 32, 32, 16, 8, kZ4M);
     case 4:
-      return launch_cfg<128, 64, 32, 16, 4>(tmA, tmB, p, stream);
+      return LC(128, 64, 32, 16, 4, kZ4M);
     case 5:
-      return launch_cfg<128, 16, 16, 16, 6>(tmA, tmB, p, stream);
+      return LC(128, 16, 16, 16, 6, kZ4M);
     case 6:
-      return launch_cfg<128, 32, 32, 8, 5>(tmA, tmB, p, stream);
+      return LC(128, 32, 32, 8, 5, kZ4M);
     case 7:
-      return launch_cfg<128, 48, 32, 16, 4>(tmA, tmB, p, stream);
+      return LC(128, 48, 32, 16, 4, kZ4M);
     case 8:
-      return launch_cfg<128, 64, 64, 16, 4>(tmA, tmB, p, stream);
+      return LC(128, 64, 64, 16, 4, kZ4M);
     case 9:
-      return launch_cfg<256, 32, 64, 16, 3>(tmA, tmB, p, stream);
+      return LC(256, 32, 64, 16, 3, kZ4M);
     // real symmetric (columns are real columns)
     case 100:
-      return launch_cfg<128, 96, 32, 32, 3, false>(tmA, tmB, p, stream);
+      return LC(128, 96, 32, 32, 3, kReal);
     case 101:
-      return launch_cfg<128, 64, 32, 32, 4, false>(tmA, tmB, p, stream);
+      return LC(128, 64, 32, 32, 4, kReal);
     case 102:
-      return launch_cfg<128, 32, 32, 16, 5, false>(tmA, tmB, p, stream);
+      return LC(128, 32, 32, 16, 5, kReal);
+    // complex 3M (columns are complex columns)
+    case 200:
+      return LC(128, 48, 32, 16, 3, kZ3M);
+    case 201:
+      return LC(128, 32, 32, 16, 3, kZ3M);
+    case 202:
+      return LC(128, 16, 32, 8, 3, kZ3M);
+    case 203:
+      return LC(64, 64, 32, 16, 4, kZ3M);
+    case 204:
+      return LC(192, 32, 32, 16, 2, kZ3M);
     default:
       return cudaErrorInvalidValue;
   }
+#undef LC
 }
 
 }  // namespace chfsi

@@ -47,6 +47,10 @@ struct StepParams {
   int64_t ld_out;
   double2* r_next;      // p > 1: this rank's chunk of the next step's packed B operand (nullable)
   int64_t ld_r_next;
+  // 3M mode: every B-operand column carries, after its 2*ld complex doubles, the real plane
+  // y_r + y_i at double offset y3_off (state buffers) / y3_off_r (packed r_next) from the column start
+  int64_t y3_off;
+  int64_t y3_off_r;
   int* nonfinite;       // set to 1 if any written value is not finite (nullable)
 };
 
@@ -54,21 +58,34 @@ constexpr int kBKHalf = 16;            // doubles per 128-byte swizzle row
 constexpr int kHalves = 2;             // two swizzle rows per stage -> 32 real K per stage
 constexpr int kBK = kBKHalf * kHalves;  // real K per stage
 
-// CPLX: complex Hermitian (BNC, WNC count complex columns; real embedding with B'' in registers) or
-// real symmetric (BNC, WNC count real columns, a plain real GEMM).
-template <int BM, int BNC, int WM, int WNC, int STAGES, bool CPLX = true>
+// MODE (the arithmetic of one step):
+//  kReal: real symmetric (BNC, WNC count real columns, a plain real GEMM);
+//  kZ4M:  complex Hermitian by the real embedding A' [B' B''] (BNC, WNC count complex columns; B'' in
+//         registers): 4 real MACs per complex MAC;
+//  kZ3M:  complex Hermitian by Gauss's 3-multiplication form: for conj(h) y with
+//         h = a_r + i a_i, y = y_r + i y_i,  P1 = sum a_r y_r,  P2 = sum a_i y_i,
+//         P3 = sum (a_r - a_i)(y_r + y_i);  Re = P1 + P2,  Im = P3 - P1 + P2  -- 3 real MACs per
+//         complex MAC. The planes a_r - a_i (of H, once per call) and y_r + y_i (of Y, written by the
+//         previous step's epilogue) are extra TMA operands, so the main loop has no FP64 add.
+constexpr int kReal = 0, kZ4M = 1, kZ3M = 2;
+
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M>
 struct FilterCfg {
+  static constexpr bool kCplx = MODE != kReal;  // complex output columns
   static constexpr int kWarpsM = BM / WM;
   static constexpr int kWarpsN = BNC / WNC;
   static constexpr int kConsumerWarps = kWarpsM * kWarpsN;
   static constexpr int kThreads = kConsumerWarps * 32;  // thread 0 doubles as the TMA producer
   static constexpr int kMT = WM / 8;   // 8-row MMA tiles per warp
-  static constexpr int kNT = CPLX ? WNC / 4 : WNC / 8;  // 8-real-column MMA tiles per warp
-  static constexpr int kABytes = kHalves * BM * 128;
-  static constexpr int kBBytes = kHalves * BNC * 128;
+  static constexpr int kNT = MODE == kZ4M ? WNC / 4 : WNC / 8;  // 8-real-column MMA tiles per warp
+  static constexpr int kNP = MODE == kZ3M ? 3 : 1;              // accumulator sets (P1, P2, P3)
+  static constexpr int kA3 = MODE == kZ3M ? BM * 128 : 0;       // a_r - a_i plane, one swizzle row
+  static constexpr int kB3 = MODE == kZ3M ? BNC * 128 : 0;      // y_r + y_i plane
+  static constexpr int kABytes = kHalves * BM * 128 + kA3;
+  static constexpr int kBBytes = kHalves * BNC * 128 + kB3;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kSmemBytes = STAGES * kStageBytes + 2 * STAGES * 8 + 1024;  // + barriers + align
-  static_assert(WM % 8 == 0 && WNC % (CPLX ? 4 : 8) == 0 && BM % WM == 0 && BNC % WNC == 0, "tile shape");
+  static_assert(WM % 8 == 0 && WNC % (MODE == kZ4M ? 4 : 8) == 0 && BM % WM == 0 && BNC % WNC == 0, "tile shape");
   static_assert(BM <= 256 && BNC <= 256, "TMA box limit");
 };
 
@@ -101,12 +118,15 @@ __device__ __forceinline__ double xor_sign(double x, uint32_t mask) {
   return __hiloint2double(hi, __double2loint(x));
 }
 
-template <int BM, int BNC, int WM, int WNC, int STAGES, bool CPLX = true>
-__global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>::kThreads, 1)
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M>
+__global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kThreads, 1)
     filter_step_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB3,
                        const StepParams p) {
-  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>;
-  constexpr int kAcc = Cfg::kMT * Cfg::kNT * 2;  // accumulator doubles per thread
+  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>;
+  constexpr bool CPLX = MODE == kZ4M;  // the A' [B' B''] embedding
+  constexpr int kNP = Cfg::kNP;
+  constexpr int kAcc = kNP * Cfg::kMT * Cfg::kNT * 2;  // accumulator doubles per thread
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align to 1024 B (128B-swizzle atoms) by pointer arithmetic on the shared array, so the compiler
   // keeps the shared address space and emits LDS (an integer round-trip would give generic LD)
@@ -186,6 +206,10 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>::kTh
       tma_load_2d(sa + h * BM * 128, &tmA, ka + h * kBKHalf, m0, &full[pc_stage]);
       tma_load_3d(sb + h * BNC * 128, &tmB, kb + h * kBKHalf, bcol, q, &full[pc_stage]);
     }
+    if constexpr (MODE == kZ3M) {  // the real planes: 16 complex entries = one 128-byte row
+      tma_load_2d(sa + kHalves * BM * 128, &tmA3, ka / 2, m0, &full[pc_stage]);
+      tma_load_3d(sb + kHalves * BNC * 128, &tmB3, kb / 2, bcol, q, &full[pc_stage]);
+    }
     ++pc_j;
     if (++pc_stage == STAGES) pc_stage = 0;
     if (++pc_kt == KT) {
@@ -204,6 +228,10 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>::kTh
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if constexpr (MODE == kZ3M) {
+      tma_prefetch(&tmA3);
+      tma_prefetch(&tmB3);
+    }
     pc_j = 0;
     pc_stage = 0;
     pc_dp_left = p.dp_units;
@@ -220,10 +248,29 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>::kTh
   const int a_row0 = wm * WM + g;
   // B smem row of this lane's first MMA column: complex -> complex column (lane >> 3), the lane pair
   // (2c, 2c+1) building (B', B''); real -> real column g
-  const int b_row0 = CPLX ? wn * WNC + (lane >> 3) : wn * WNC + g;
+  const int b_row0 = CPLX ? wn * WNC + (lane >> 3) : wn * WNC + g;  // 3M: complex column g
   bool bad = false;
 
   double acc[Cfg::kMT][Cfg::kNT][2];
+  double acc2[MODE == kZ3M ? Cfg::kMT : 1][MODE == kZ3M ? Cfg::kNT : 1][2];  // 3M: P2
+  double acc3[MODE == kZ3M ? Cfg::kMT : 1][MODE == kZ3M ? Cfg::kNT : 1][2];  // 3M: P3
+  auto zero_acc = [&]() {
+#pragma unroll
+    for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < Cfg::kNT; ++jj) {
+        acc[i][jj][0] = acc[i][jj][1] = 0.0;
+        if constexpr (MODE == kZ3M) acc2[i][jj][0] = acc2[i][jj][1] = acc3[i][jj][0] = acc3[i][jj][1] = 0.0;
+      }
+  };
+  // accumulator element x of set s (s = 0: P1 / the only set, 1: P2, 2: P3) -- flat view for stream-K
+  auto acc_ref = [&](int sset, int i, int jj, int e) -> double& {
+    if constexpr (MODE == kZ3M) {
+      if (sset == 1) return acc2[i][jj][e];
+      if (sset == 2) return acc3[i][jj][e];
+    }
+    return acc[i][jj][e];
+  };
 
   // fused epilogue: three-term recurrence, degree masking, finished-column store
   auto store_val = [&](int col, int64_t r, double v) {  // real: one value of column col
@@ -240,19 +287,58 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>::kTh
       if (p.r_next) reinterpret_cast<double*>(p.r_next)[(int64_t)(col - p.fin_end) * p.ld_r_next + r] = v;
     }
   };
+  // 3M: one complex output (vr, vi) of column col; also writes the y_r + y_i plane of the next operand
+  auto store_z3 = [&](int col, int64_t r, double vr, double vi) {
+    if (p.flags & 1) {
+      const double2 yc = p.y_cur[(int64_t)col * p.ld_cur + r];
+      vr -= p.c * yc.x;
+      vi -= p.c * yc.y;
+    }
+    vr *= p.a;
+    vi *= p.a;
+    if (p.flags & 2) {
+      const double2 yp = p.y_prev[(int64_t)col * p.ld_prev + r];
+      vr -= p.b * yp.x;
+      vi -= p.b * yp.y;
+    }
+    bad |= !(isfinite(vr) && isfinite(vi));
+    const double2 v = make_double2(vr, vi);
+    if (col < p.fin_end) {
+      p.out[(int64_t)col * p.ld_out + r] = v;
+    } else {
+      double2* yn = p.y_next + (int64_t)col * p.ld_next;
+      yn[r] = v;
+      reinterpret_cast<double*>(yn)[p.y3_off + r] = vr + vi;
+      if (p.r_next) {
+        double2* rn = p.r_next + (int64_t)(col - p.fin_end) * p.ld_r_next;
+        rn[r] = v;
+        reinterpret_cast<double*>(rn)[p.y3_off_r + r] = vr + vi;
+      }
+    }
+  };
   auto epilogue = [&](int tile) {
     const int m0 = (tile / p.tiles_n) * BM;
     int nu;
     const int c0 = tile_cols(tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
     if (wn >= nu) return;  // this warp's columns belong to the next tile
-    const int col_base = p.col0 + c0 + wn * WNC + (CPLX ? qd : 2 * qd);
+    const int col_base = p.col0 + c0 + wn * WNC + (CPLX ? qd : 2 * qd);  // (unused by 3M)
 #pragma unroll
     for (int i = 0; i < Cfg::kMT; ++i) {
       const int64_t r = (int64_t)m0 + wm * WM + i * 8 + g;
       if (r >= p.nrows) continue;
 #pragma unroll
       for (int j = 0; j < Cfg::kNT; ++j) {
-        if constexpr (!CPLX) {
+        if constexpr (MODE == kZ3M) {
+          // lane owns complex columns col, col + 1 of row r: Re = P1 + P2, Im = P3 - P1 + P2
+          const int col = p.col0 + c0 + wn * WNC + j * 8 + 2 * qd;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (col + e >= p.col_end) continue;
+            store_z3(col + e, r, acc[i][j][e] + acc2[i][j][e], (acc3[i][j][e] - acc[i][j][e]) + acc2[i][j][e]);
+          }
+          continue;
+        }
+        if constexpr (MODE == kReal) {
           const int col = col_base + j * 8;
           if (col < p.col_end) store_val(col, r, acc[i][j][0]);
           if (col + 1 < p.col_end) store_val(col + 1, r, acc[i][j][1]);
@@ -298,10 +384,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>::kTh
       const int64_t tile_end_g = (g0 / KT + 1) * KT;
       kend = (int)(KT - (tile_end_g - (t_end < tile_end_g ? t_end : tile_end_g)));
     }
-#pragma unroll
-    for (int i = 0; i < Cfg::kMT; ++i)
-#pragma unroll
-      for (int jj = 0; jj < Cfg::kNT; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+    zero_acc();
 
     // a warp whose columns all lie past the active block (ragged last N tile) skips the MMAs: the
     // DMMA pipe is shared per SM sub-partition, so the padding costs no tensor-core time
@@ -313,6 +396,52 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>::kTh
       mbar_wait(&full[s], phase);
       const uint8_t* sa = smem + s * Cfg::kStageBytes;
       const uint8_t* sb = sa + Cfg::kABytes;
+      if constexpr (MODE == kZ3M) {
+        if (warp_active) {
+          const uint8_t* a3 = sa + kHalves * BM * 128;
+          const uint8_t* b3 = sb + kHalves * BNC * 128;
+#pragma unroll
+          for (int h = 0; h < kHalves; ++h) {
+            const uint8_t* ah = sa + h * BM * 128;
+            const uint8_t* bh = sb + h * BNC * 128;
+#pragma unroll
+            for (int sub = 0; sub < 2; ++sub) {
+              // P1, P2: complex entry 2*qd + sub of this half -> (a_r, a_i) and (y_r, y_i) in one LDS.128
+              const int chunk = 2 * qd + sub;
+              double2 av[Cfg::kMT], bv[Cfg::kNT];
+#pragma unroll
+              for (int i = 0; i < Cfg::kMT; ++i) av[i] = *reinterpret_cast<const double2*>(ah + swz(a_row0 + i * 8, chunk));
+#pragma unroll
+              for (int jj = 0; jj < Cfg::kNT; ++jj) bv[jj] = *reinterpret_cast<const double2*>(bh + swz(b_row0 + jj * 8, chunk));
+#pragma unroll
+              for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+                for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], av[i].x, bv[jj].x);
+#pragma unroll
+              for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+                for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc2[i][jj][0], acc2[i][jj][1], av[i].y, bv[jj].y);
+            }
+            // P3: entries 8h + 2qd + {0, 1} of the planes (one 16-byte chunk of the 128-byte row)
+            {
+              const int chunk = 4 * h + qd;
+              double2 cv[Cfg::kMT], dv[Cfg::kNT];
+#pragma unroll
+              for (int i = 0; i < Cfg::kMT; ++i) cv[i] = *reinterpret_cast<const double2*>(a3 + swz(a_row0 + i * 8, chunk));
+#pragma unroll
+              for (int jj = 0; jj < Cfg::kNT; ++jj) dv[jj] = *reinterpret_cast<const double2*>(b3 + swz(b_row0 + jj * 8, chunk));
+#pragma unroll
+              for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+                for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc3[i][jj][0], acc3[i][jj][1], cv[i].x, dv[jj].x);
+#pragma unroll
+              for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+                for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc3[i][jj][0], acc3[i][jj][1], cv[i].y, dv[jj].y);
+            }
+          }
+        }
+      } else
 #pragma unroll
       for (int h = 0; h < kHalves && warp_active; ++h) {
         const uint8_t* ah = sa + h * BM * 128;
@@ -370,11 +499,14 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>::kTh
     const int my_slot = (t_beg / KT == u) ? 0 : 1;
     double* mine = p.partials + ((cta * 2 + my_slot) * kAcc) * (int64_t)Cfg::kThreads;
 #pragma unroll
-    for (int i = 0; i < Cfg::kMT; ++i)
+    for (int ps = 0; ps < kNP; ++ps)
 #pragma unroll
-      for (int jj = 0; jj < Cfg::kNT; ++jj)
+      for (int i = 0; i < Cfg::kMT; ++i)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) __stcg(mine + ((i * Cfg::kNT + jj) * 2 + e) * Cfg::kThreads + threadIdx.x, acc[i][jj][e]);
+        for (int jj = 0; jj < Cfg::kNT; ++jj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            __stcg(mine + (((ps * Cfg::kMT + i) * Cfg::kNT + jj) * 2 + e) * Cfg::kThreads + threadIdx.x, acc_ref(ps, i, jj, e));
     __threadfence();
     __syncthreads();
     const int64_t c_lo = sk_owner(U0, p.tail_iters, p.grid), c_hi = sk_owner(U1 - 1, p.tail_iters, p.grid);
@@ -385,21 +517,21 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, CPLX>::kTh
     __syncthreads();
     if (s_ticket != nseg - 1) continue;  // not the last contributor
     __threadfence();
-#pragma unroll
-    for (int i = 0; i < Cfg::kMT; ++i)
-#pragma unroll
-      for (int jj = 0; jj < Cfg::kNT; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+    zero_acc();
     for (int64_t c = c_lo; c <= c_hi; ++c) {  // fixed k order: deterministic sum
       const int64_t cs = sk_start(c, p.tail_iters, p.grid);
       if (sk_start(c + 1, p.tail_iters, p.grid) <= cs) continue;
       const int slot = (cs / KT == u) ? 0 : 1;
       const double* src = p.partials + ((c * 2 + slot) * kAcc) * (int64_t)Cfg::kThreads;
 #pragma unroll
-      for (int i = 0; i < Cfg::kMT; ++i)
+      for (int ps = 0; ps < kNP; ++ps)
 #pragma unroll
-        for (int jj = 0; jj < Cfg::kNT; ++jj)
+        for (int i = 0; i < Cfg::kMT; ++i)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) acc[i][jj][e] += __ldcg(src + ((i * Cfg::kNT + jj) * 2 + e) * Cfg::kThreads + threadIdx.x);
+          for (int jj = 0; jj < Cfg::kNT; ++jj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              acc_ref(ps, i, jj, e) += __ldcg(src + (((ps * Cfg::kMT + i) * Cfg::kNT + jj) * 2 + e) * Cfg::kThreads + threadIdx.x);
     }
     epilogue(tile);
     if (threadIdx.x == 0) p.tickets[u] = 0;  // ready for the next launch (stream ordered)
@@ -420,9 +552,13 @@ TileChoice choose_filter_tile(int64_t nrows, int64_t ncols, int num_sms);
 void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p);
 // workspace the schedule needs: partial slots (doubles) and tickets (ints)
 size_t filter_partials_doubles(const TileChoice& t, int num_sms);
+// tmA3 / tmB3: the 3M planes (ignored by the other modes)
 cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                               const StepParams& p, cudaStream_t stream);
+                               const CUtensorMap& tmA3, const CUtensorMap& tmB3, const StepParams& p,
+                               cudaStream_t stream);
 // real-symmetric variants (ids >= 100)
 TileChoice choose_filter_tile_real(int64_t nrows, int64_t ncols, int num_sms);
+// complex 3M variants (ids >= 200)
+TileChoice choose_filter_tile_z3(int64_t nrows, int64_t ncols, int num_sms);
 
 }  // namespace chfsi

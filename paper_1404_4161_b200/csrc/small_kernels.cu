@@ -1,4 +1,6 @@
 // small_kernels.cu -- see small_kernels.cuh.
+#include <algorithm>
+
 #include "small_kernels.cuh"
 
 namespace chfsi {
@@ -29,6 +31,26 @@ __global__ void hemv_kernel(int64_t n, int64_t nloc, const double2* __restrict__
   }
   double sr = warp_sum(sr0 + sr1), si = warp_sum(si0 + si1);
   if (lane == 0) w[r] = make_double2(sr, si);
+}
+
+__global__ void h3_plane_kernel(int64_t n, int64_t nloc, const double2* __restrict__ Hp, int64_t ldh,
+                                double* __restrict__ H3, int64_t ld3) {
+  const int64_t r = blockIdx.y;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 h = __ldcs(Hp + r * ldh + q);
+    H3[r * ld3 + q] = h.x - h.y;
+  }
+}
+
+__global__ void pack_y3_kernel(int64_t rows, const double2* __restrict__ X, int64_t ldx, double* __restrict__ dst,
+                               int64_t cs, int64_t y3_off) {
+  const int64_t j = blockIdx.y;
+  double* col = dst + j * cs;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const double2 x = X[j * ldx + r];
+    reinterpret_cast<double2*>(col)[r] = x;
+    col[y3_off + r] = x.x + x.y;
+  }
 }
 
 template <int NT>
@@ -371,6 +393,22 @@ cudaError_t launch_orth_err(int64_t k, const double* G, int64_t ldg, double* out
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((k + 255) / 256), (unsigned)k);
   orth_err_real_kernel<<<grid, 256, 0, st>>>(k, G, ldg, reinterpret_cast<unsigned long long*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_h3_plane(int64_t n, int64_t nloc, const double2* Hp, int64_t ldh, double* H3, int64_t ld3,
+                            cudaStream_t st) {
+  if (n <= 0 || nloc <= 0) return cudaSuccess;
+  const unsigned bx = (unsigned)std::min<int64_t>((n + 255) / 256, 16);
+  h3_plane_kernel<<<dim3(bx, (unsigned)nloc), 256, 0, st>>>(n, nloc, Hp, ldh, H3, ld3);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_y3(int64_t rows, int64_t cols, const double2* X, int64_t ldx, double* dst, int64_t cs,
+                           int64_t y3_off, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  const unsigned bx = (unsigned)std::min<int64_t>((rows + 255) / 256, 64);
+  pack_y3_kernel<<<dim3(bx, (unsigned)cols), 256, 0, st>>>(rows, X, ldx, dst, cs, y3_off);
   return cudaGetLastError();
 }
 

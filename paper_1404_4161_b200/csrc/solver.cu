@@ -99,6 +99,17 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
     return CHFSI_OK;
   };
 
+  // 3M filter / H Q: the Re H - Im H plane of this problem's panel, built once and reused by every
+  // filter step and Rayleigh-Ritz product of the problem (unpinned on every exit path)
+  struct PinGuard {
+    chfsi_ctx c;
+    ~PinGuard() { c->h3_pin = nullptr; }
+  } pin_guard{ctx};
+  if (elem == 2 && ctx->zmul == 3) {
+    TRY(h3_prepare(ctx, Hp, ldh, n, nloc));
+    ctx->h3_pin = Hp;
+  }
+
   // Alg 1 l3: Lanczos upper bound beta (R17) and ||H||_est (R8)
   double tmin, tmax, beta;
   auto t0 = tm.begin();

@@ -11,7 +11,8 @@ import oracle as O
 from gen.configs import C4_INTERVAL, CONFIGS, c4_ramp
 
 pytestmark = pytest.mark.gpu
-VARIANTS = ["0", "1", "2", "3", "4", "5", "6", "7", "8", "9"]
+# 3M variants (the default complex arithmetic, ids 200..204) and the 4M real-embedding variants (0..9)
+VARIANTS = ["200", "201", "202", "203", "204", "0", "1", "2", "3", "4", "5", "6", "7", "8", "9"]
 
 
 def crand(rng, *shape):
@@ -26,10 +27,13 @@ def ctx(gpu_lib):
 
 
 @pytest.fixture(params=VARIANTS)
-def variant(request):
-    os.environ["CHFSI_FILTER_VARIANT"] = request.param
+def variant(request, ctx):
+    z3 = int(request.param) >= 200
+    env = "CHFSI_FILTER_VARIANT_Z3" if z3 else "CHFSI_FILTER_VARIANT"
+    ctx.set_complex_mult(3 if z3 else 4)
+    os.environ[env] = request.param
     yield request.param
-    os.environ.pop("CHFSI_FILTER_VARIANT", None)
+    os.environ.pop(env, None)
 
 
 def run_filter(chfsi, ctx, H, Y0, deg, l1, c, e):
@@ -138,3 +142,26 @@ def test_filter_c1_shape_sampled(gpu_lib, ctx):
     cols = [0, 1, 119, 238, 239]
     Yo, _ = O.chebyshev_filter(Gm, Y0[:, cols], [deg[j] for j in cols], iv["lambda1"], c, e)
     assert colrel(Y[:, cols], Yo).max() <= 1e-11
+
+
+@pytest.mark.parametrize("n,k", [(1000, 64), (515, 21)])
+def test_filter_3m_matches_4m_and_oracle(gpu_lib, n, k):
+    """Gauss 3M (default) and the 4M real embedding compute the same Alg 2 result: both within the
+    filter tolerance of the oracle, and within a few ulps (normwise) of each other."""
+    Gm = G.gue(n, 11, G.stream(5, n))
+    rng = np.random.default_rng(n + k)
+    Y0 = crand(rng, n, k)
+    deg = sorted(rng.integers(1, 31, k).tolist())
+    iv = C4_INTERVAL
+    c, e = (iv["alpha"] + iv["beta"]) / 2, (iv["beta"] - iv["alpha"]) / 2
+    out = {}
+    for mults in (3, 4):
+        cx = gpu_lib.Context(0)
+        cx.set_complex_mult(mults)
+        out[mults] = run_filter(gpu_lib, cx, Gm, Y0, deg, iv["lambda1"], c, e)
+        cx.close()
+    assert colrel(out[3], out[4]).max() <= 1e-12
+    cols = [0, k // 2, k - 1]
+    Yo, _ = O.chebyshev_filter(Gm, Y0[:, cols], [deg[j] for j in cols], iv["lambda1"], c, e)
+    for mults in (3, 4):
+        assert colrel(out[mults][:, cols], Yo).max() <= 1e-11

@@ -18,14 +18,18 @@ def crand(rng, *shape):
     return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
 
 
-def run_ranks(chfsi, P, fn):
-    """Run fn(rank, ctx) for rank = 0..P-1 concurrently (one thread + one stream per rank)."""
+def run_ranks(chfsi, P, fn, group_cols=None):
+    """Run fn(rank, ctx) for rank = 0..P-1 concurrently (one thread + one stream per rank).
+    group_cols: column-group width of the filter's comm/compute pipeline (chfsi_ctx_set_pipeline)."""
     import torch
 
     torch.cuda.synchronize()
     g = chfsi.LocalGroup(P)
     streams = [torch.cuda.Stream() for _ in range(P)]
     ctxs = [chfsi.Context(0, stream=streams[r], local_group=g, rank=r) for r in range(P)]
+    if group_cols is not None:
+        for c in ctxs:
+            c.set_pipeline(group_cols)
     out = [None] * P
     errs = []
 
@@ -57,8 +61,11 @@ def slabs(chfsi, H, P):
     return [chfsi.to_colmajor(np.asfortranarray(H[:, r * nloc:(r + 1) * nloc])) for r in range(P)], nloc
 
 
-@pytest.mark.parametrize("n,P", [(512, 2), (600, 4), (256, 8)])
-def test_filter_multirank(gpu_lib, n, P):
+@pytest.mark.parametrize("n,P,group_cols", [(512, 2, None), (600, 4, None), (256, 8, None), (512, 2, 8),
+                                             (600, 4, 10), (256, 8, 0)])
+def test_filter_multirank(gpu_lib, n, P, group_cols):
+    """group_cols: None = default (one group at k = 37), 8 / 10 = 4 / 3 column groups whose
+    allgathers overlap the next group's K1 on a separate stream, 0 = pipelining off."""
     k = 37
     w = G.wy(n, int(0.9 * n), n + P)
     H = w.full()
@@ -73,7 +80,7 @@ def test_filter_multirank(gpu_lib, n, P):
     def fn(r, ctx):
         return ctx.filter(Hs[r], Ys[r], deg, l1, c, e, n=n, row0=r * nloc)
 
-    mv = run_ranks(gpu_lib, P, fn)
+    mv = run_ranks(gpu_lib, P, fn, group_cols)
     assert all(m == sum(deg) for m in mv)
     Y = np.concatenate([y.cpu().numpy() for y in Ys], axis=0)
     ctx1 = gpu_lib.Context(0)
@@ -135,8 +142,8 @@ def test_householder_fallback_multirank(gpu_lib):
     assert np.abs(Q.conj().T @ Q - np.eye(k)).max() <= 1e-13
 
 
-@pytest.mark.parametrize("P", [2, 4])
-def test_solve_multirank_c0(gpu_lib, P):
+@pytest.mark.parametrize("P,group_cols", [(2, None), (4, None), (4, 12)])
+def test_solve_multirank_c0(gpu_lib, P, group_cols):
     cf = CONFIGS["c0"]
     n, nev, nex = cf["n"], cf["nev"], cf["nex"]
     w = G.wy(n, cf["nd"], cf["seed"])
@@ -149,7 +156,7 @@ def test_solve_multirank_c0(gpu_lib, P):
         return ctx.solve_sequence(lambda ell: Hs[r], 1, Xs[r], nev, nex, cf["tol"], deg_cap=cf["cap"],
                                   seed=cf["seed"], n=n, row0=r * nloc)
 
-    out = run_ranks(gpu_lib, P, fn)
+    out = run_ranks(gpu_lib, P, fn, group_cols)
     for o in out:
         assert o["status"] == 0
         assert np.max(np.abs(o["lam"][0] - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
