@@ -116,11 +116,13 @@ struct Operand {
 // Build the B-operand descriptors for one launch over columns [col0, kcols) of `buf`.
 //  Column slots hold `rows` elements at a column stride of cs = cw * ld doubles, cw = elem (plain
 //  layout) or 3 (3M layout: 2 * ld complex doubles, then the y_r + y_i plane at offset 2 * ld).
+//  z3: the launch runs the 3M kernel and also needs the plane's map (a 4M launch on a 3M-layout
+//  buffer just skips the planes).
 //  p == 1: buf = local state (rows = n), column coordinate = absolute column.
 //  p > 1 : buf = packed [rank][kcols - col0][cs] operand (rows = nloc), coordinate = column - col0.
 static chfsi_status b_operand(chfsi_ctx ctx, Operand* op, const double* buf, int64_t rows, int64_t ld,
-                              int64_t kcols, int64_t col0, int nranks, int box_cols, int elem, bool z3) {
-  const int64_t cs = (z3 ? 3 : elem) * ld;
+                              int64_t kcols, int64_t col0, int nranks, int box_cols, int elem, int cw, bool z3) {
+  const int64_t cs = cw * ld;
   const int64_t cols = nranks == 1 ? kcols : kcols - col0;
   op->b_col0 = nranks == 1 ? (int32_t)col0 : 0;
   chfsi_status st = make_tmap_3d(ctx, &op->tm, buf, elem * rows, cols, nranks, cs, cs * cols, box_cols);
@@ -170,10 +172,28 @@ static chfsi_status a3_operand(chfsi_ctx ctx, CUtensorMap* m, const void* Hp, in
   return make_tmap_2d(ctx, m, ctx->h3.ptr, n, nloc, ctx->h3_ld, box_rows);
 }
 
-static inline TileChoice pick_tile(chfsi_ctx ctx, int elem, bool z3, int64_t nrows, int64_t ncols, int sms) {
-  (void)ctx;
+// Tile variant and arithmetic of one launch. With the 3M column layout available (z3_layout) the
+// launch runs 3M or 4M, whichever the step model rates faster: 3M does 25 % fewer tensor flops but
+// streams 24 bytes of H per complex entry (interleaved + plane) against 16, so narrow, HBM-bound
+// steps run 4M. Below 28 active columns 4M is used regardless (measured at n = 16384: 4M 1.55 ms vs 3M
+// 1.77 ms per step at 20 and 24 columns, 3M ahead from 32; profiles/r01_ab_narrow.log);
+// CHFSI_Z3_MIN_COLS overrides that threshold.
+static TileChoice pick_tile(int elem, bool z3_layout, int64_t nrows, int64_t ncols, int sms, bool* z3k) {
+  *z3k = false;
   if (elem == 1) return choose_filter_tile_real(nrows, ncols, sms);
-  return z3 ? choose_filter_tile_z3(nrows, ncols, sms) : choose_filter_tile(nrows, ncols, sms);
+  TileChoice t4 = choose_filter_tile(nrows, ncols, sms);
+  if (!z3_layout) return t4;
+  static const int64_t min_cols = [] {
+    const char* e = getenv("CHFSI_Z3_MIN_COLS");
+    return e ? (int64_t)atoll(e) : (int64_t)28;
+  }();
+  if (ncols < min_cols) return t4;
+  TileChoice t3 = choose_filter_tile_z3(nrows, ncols, sms);
+  if (t3.cost <= t4.cost) {
+    *z3k = true;
+    return t3;
+  }
+  return t4;
 }
 
 chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
@@ -181,10 +201,10 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
   (void)row0;
   if (k == 0) return CHFSI_OK;
   const int p = ctx->nranks;
-  const bool z3 = elem == 2 && ctx->zmul == 3;
+  bool z3 = false;
+  TileChoice t = pick_tile(elem, elem == 2 && ctx->zmul == 3, nloc, k, ctx->num_sms, &z3);
   const int cw = z3 ? 3 : elem;
   const size_t eb = 8 * (size_t)elem;
-  TileChoice t = pick_tile(ctx, elem, z3, nloc, k, ctx->num_sms);
   CUtensorMap tmA, tmA3;
   chfsi_status st = a_operand(ctx, &Hp, &ldh, n, nloc, elem);
   if (st) return st;
@@ -228,7 +248,7 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
     bsrc = static_cast<const double*>(ctx->L0.ptr);
     bld = ldl;
   }
-  st = b_operand(ctx, &op, bsrc, p == 1 ? n : nloc, bld, k, 0, p, t.bnc, elem, z3);
+  st = b_operand(ctx, &op, bsrc, p == 1 ? n : nloc, bld, k, 0, p, t.bnc, elem, cw, z3);
   if (st) return st;
   StepParams sp{};
   sp.nrows = nloc;
@@ -355,12 +375,13 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     }
   }
   CUtensorMap tmA, tmA3;
-  int last_bm = -1;
+  int last_bm = -1, last_bm3 = -1;
   bool h3_built = false;
   // CUDA events around every K1 launch (read back after the final synchronisation)
   st = ensure_events(ctx, ctx->k1_events, (size_t)2 * (mk + 1) * G, cudaEventDefault);
   if (st) return st;
   int nev_used = 0;
+  std::vector<char> plane_ok(G, 1);  // group's B operand carries a current 3M plane
   int64_t s = 0;  // active start s_i = #{j : deg[j] <= i}
   for (int i = 0; i < mk; ++i) {
     while (s < k && deg[s] <= i) ++s;
@@ -373,19 +394,26 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       if (c0 >= ce) continue;  // every column of this group has finished
       const int64_t fin = std::min(std::max(s_next, c0), ce);
       const int64_t ka = ce - c0, ka_next = ce - fin;
-      TileChoice t = pick_tile(ctx, elem, z3, nloc, ka, sms);
+      // this launch's arithmetic; a 4M epilogue does not write the y_r + y_i plane, so once a group
+      // ran a 4M step its later steps stay 4M
+      bool z3k = false;
+      TileChoice t = pick_tile(elem, z3 && plane_ok[g], nloc, ka, sms, &z3k);
+      if (!z3k) plane_ok[g] = 0;
       if (t.bm != last_bm) {
         st = make_tmap_2d(ctx, &tmA, Hp, elem * n, nloc, elem * ldh, t.bm);
-        if (!st && z3) st = a3_operand(ctx, &tmA3, Hp, ldh, n, nloc, t.bm, &h3_built);
         if (st) return st;
-        if (!z3) tmA3 = tmA;
         last_bm = t.bm;
+      }
+      if (z3k && t.bm != last_bm3) {
+        st = a3_operand(ctx, &tmA3, Hp, ldh, n, nloc, t.bm, &h3_built);
+        if (st) return st;
+        last_bm3 = t.bm;
       }
       Operand op;
       if (p == 1)
-        st = b_operand(ctx, &op, reinterpret_cast<const double*>(L[cur]), n, ldl, k, c0, 1, t.bnc, elem, z3);
+        st = b_operand(ctx, &op, reinterpret_cast<const double*>(L[cur]), n, ldl, k, c0, 1, t.bnc, elem, cw, z3k);
       else
-        st = b_operand(ctx, &op, region(cur, g), nloc, ldp, ce, c0, p, t.bnc, elem, z3);
+        st = b_operand(ctx, &op, region(cur, g), nloc, ldp, ce, c0, p, t.bnc, elem, cw, z3k);
       if (st) return st;
       StepParams sp{};
       sp.nrows = nloc;
@@ -431,7 +459,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       // this group's operand for step i is complete once its allgather (comm stream) has landed
       if (p > 1) CHFSI_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->grp_ag[g], 0));
       CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used], ctx->stream));
-      CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, tmA3, op.tm3, sp, ctx->stream));
+      CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, z3k ? tmA3 : tmA, op.tm3, sp, ctx->stream));
       CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used + 1], ctx->stream));
       nev_used += 2;
       ctx->launches++;

@@ -23,127 +23,112 @@ cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUt
 }
 
 struct Variant {
-  int bm, bnc, wnc;
-  double eff;   // relative per-flop efficiency of the variant (measured)
-  int threads;  // CTA size
-  int acc;      // accumulator doubles per thread
+  int id, bm, bnc, wnc, threads, acc;
+  double eff;  // per-flop efficiency relative to the family's best full-width variant (measured)
 };
+// 4M (real embedding) variants; ids are the launch_filter_step cases
 constexpr Variant kVariants[] = {
-    {128, 32, 16, 0.930, 256, 32},  // 0: 8 warps, warp tile 32 x 16
-    {64, 64, 16, 0.920, 256, 32},   // 1: 8 warps, warp tile 32 x 16
-    {128, 64, 32, 0.940, 256, 64},  // 2: 8 warps, warp tile 32 x 32
-    {64, 32, 16, 0.700, 128, 32},   // 3: 4 warps
-    {128, 64, 16, 0.950, 512, 32},  // 4: 16 warps (4 per SMSP), warp tile 32 x 16
-    {128, 16, 16, 0.800, 256, 16},  // 5: 8 warps, warp tile 16 x 16 (narrow blocks)
-    {128, 32, 8, 0.960, 512, 16},   // 6: 16 warps, warp tile 32 x 8
-    {128, 48, 16, 1.000, 384, 32},  // 7: 12 warps, warp tile 32 x 16 (34.9 TF/s at n=13000, k=624)
-    {128, 64, 16, 0.900, 256, 64},  // 8: 8 warps, warp tile 64 x 16 (measured slower; kept for sweeps)
-    {256, 32, 16, 0.970, 256, 64},  // 9: 8 warps, warp tile 64 x 16, BM 256 (best at exact 32-column fits)
+    {0, 128, 32, 16, 256, 32, 0.930},  // 8 warps, warp tile 32 x 16
+    {1, 64, 64, 16, 256, 32, 0.920},   // 8 warps, warp tile 32 x 16
+    {2, 128, 64, 32, 256, 64, 0.940},  // 8 warps, warp tile 32 x 32
+    {3, 64, 32, 16, 128, 32, 0.700},   // 4 warps
+    {4, 128, 64, 16, 512, 32, 0.950},  // 16 warps (4 per SMSP), warp tile 32 x 16
+    {5, 128, 16, 16, 256, 16, 0.800},  // 8 warps, warp tile 16 x 16 (narrow blocks)
+    {6, 128, 32, 8, 512, 16, 0.960},   // 16 warps, warp tile 32 x 8
+    {7, 128, 48, 16, 384, 32, 1.000},  // 12 warps, warp tile 32 x 16 (34.9 TF/s at n=13000, k=624)
+    {8, 128, 64, 16, 256, 64, 0.900},  // 8 warps, warp tile 64 x 16 (measured slower; kept for sweeps)
+    {9, 256, 32, 16, 256, 64, 0.970},  // 8 warps, warp tile 64 x 16, BM 256 (best at exact 32-column fits)
+    {10, 256, 4, 4, 256, 8, 0.800},    // narrow (HBM-bound) steps: 8 warps, warp tile 32 x 4
+    {11, 128, 8, 4, 256, 8, 0.800},    // narrow: 8 warps (4 x 2), warp tile 32 x 4
+    {12, 128, 12, 4, 384, 8, 0.800},   // narrow: 12 warps (4 x 3), warp tile 32 x 4
 };
+// 3M variants: accumulators are 3 sets (P1, P2, P3) of (WM/8) x (WNC/8) 8x8 tiles. eff: measured
+// full-width rates relative to 200 (n = 13000, k = 624: 45.5 / 42.0 / 32.4 / 41.8 / 30.2 TF/s
+// ZGEMM-equivalent; profiles/r01_z3_variants.log)
+constexpr Variant kVariantsZ3[] = {
+    {200, 128, 48, 16, 384, 48, 1.0}, {201, 128, 32, 16, 256, 48, 0.93}, {202, 128, 16, 8, 256, 24, 0.72},
+    {203, 64, 64, 16, 256, 48, 0.925}, {204, 192, 32, 16, 384, 48, 0.67},
+};
+// real-symmetric variants
+constexpr Variant kVariantsReal[] = {
+    {100, 128, 96, 32, 384, 32, 1.0}, {101, 128, 64, 32, 256, 32, 0.97}, {102, 128, 32, 16, 256, 16, 0.93},
+};
+
+// Model time of one step of `ncols` active columns over `nrows` rows for variant V, in units of a
+// full-efficiency 4M column-row (8 n flops at 34.9 TF/s):
+//  compute: the balanced N split gives every N tile `per` warp-column units; active warps compute
+//           whole units (padding inside a unit is real work), idle warps skip their MMAs but are not
+//           free (30 %), fewer than two active warps per SM sub-partition lose latency hiding;
+//           `speed` = the family's best full-width rate relative to 4M (3M: 45.5 / 34.9)
+//  memory:  H streamed once per step per N tile column (re-reads mostly from L2: +25 % per extra N
+//           tile), `hbm_cols` = the column count at which the family's compute time equals its H
+//           stream at ~5.9 TB/s (4M: 16 B / entry -> 11.8; 3M: 24 B / entry -> 17.7)
+static double step_cost(const Variant& V, int64_t nrows, int64_t ncols, double speed, double hbm_cols) {
+  const int64_t tm = (nrows + V.bm - 1) / V.bm;
+  const int64_t units = (ncols + V.wnc - 1) / V.wnc;
+  const int64_t tn = (ncols + V.bnc - 1) / V.bnc;
+  const int64_t per = (units + tn - 1) / tn;
+  const int warps_m = V.threads / 32 / (V.bnc / V.wnc);
+  const double active_warps = (double)per * warps_m;
+  const double occ = active_warps >= 8 ? 1.0 : 0.6 + 0.05 * active_warps;
+  const double cols = 0.3 * (double)(tn * per * V.wnc) + 0.7 * (double)(units * V.wnc);
+  const double rows = (double)tm * V.bm;
+  const double compute = rows * cols / (V.eff * occ * speed);
+  const double memory = rows * hbm_cols * (1.0 + 0.25 * (double)(tn - 1));
+  // + 10 % of the compute term: between variants that all hit the HBM floor, the one with less
+  // padded tensor work keeps more slack (and wins)
+  return (compute > memory ? compute : memory) + 0.1 * compute;
+}
+
+template <size_t N>
+static TileChoice choose(const Variant (&vs)[N], const char* env, int64_t nrows, int64_t ncols, double speed,
+                         double hbm_cols) {
+  // test hook: the environment variable forces one variant (parity tests cover every instantiation)
+  const char* fs = getenv(env);
+  const int forced = fs ? atoi(fs) : -1;
+  int best = -1;
+  double best_cost = 1e300;
+  for (size_t v = 0; v < N; ++v) {
+    if (forced >= 0 && vs[v].id != forced) continue;
+    const double cost = step_cost(vs[v], nrows, ncols, speed, hbm_cols);
+    if (best < 0 || cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = (int)v;
+    }
+  }
+  if (best < 0) best = 0;
+  const Variant& V = vs[best];
+  return TileChoice{V.id, V.bm, V.bnc, V.threads, V.acc, V.wnc, best_cost};
+}
 
 }  // namespace
 
 TileChoice choose_filter_tile(int64_t nrows, int64_t ncols, int num_sms) {
-  // test hook: CHFSI_FILTER_VARIANT forces one variant (parity tests cover every instantiation)
-  const char* fs = getenv("CHFSI_FILTER_VARIANT");
-  const int forced = fs ? atoi(fs) : -1;
-  const int nvar = (int)(sizeof(kVariants) / sizeof(kVariants[0]));
-  if (forced >= 0 && forced < nvar)
-    return TileChoice{forced, kVariants[forced].bm, kVariants[forced].bnc, kVariants[forced].threads,
-                      kVariants[forced].acc, kVariants[forced].wnc};
-  // the persistent stream-K schedule removes wave quantisation: minimise padded work / efficiency
-  // (efficiencies: measured full-width rates relative to the best variant)
-  int best = 0;
-  double best_cost = 1e300;
-  for (int v = 0; v < nvar; ++v) {
-    const int64_t tm = (nrows + kVariants[v].bm - 1) / kVariants[v].bm;
-    // balanced N split in warp-tile units: every tile has `per` active warp columns; idle warps skip
-    // their MMAs but are not free (model: 30 % of full cost), and fewer than two
-    // active warps per SM sub-partition lose latency hiding (profiles/r01_filter_variants)
-    const Variant& V = kVariants[v];
-    const int64_t units = (ncols + V.wnc - 1) / V.wnc;
-    const int64_t tn = (ncols + V.bnc - 1) / V.bnc;
-    const int64_t per = (units + tn - 1) / tn;
-    const int warps_m = V.threads / 32 / (V.bnc / V.wnc);
-    const double active_warps = (double)per * warps_m;
-    const double occ = active_warps >= 8 ? 1.0 : 0.6 + 0.05 * active_warps;
-    const double cols = 0.3 * (double)(tn * per * V.wnc) + 0.7 * (double)ncols;
-    const double cost = (double)tm * V.bm * cols / (V.eff * occ);
-    if (cost < best_cost * 0.999) {
-      best_cost = cost;
-      best = v;
-    }
-  }
-  (void)num_sms;
-  return TileChoice{best, kVariants[best].bm, kVariants[best].bnc, kVariants[best].threads, kVariants[best].acc,
-                    kVariants[best].wnc};
-}
-
-TileChoice choose_filter_tile_real(int64_t nrows, int64_t ncols, int num_sms) {
-  (void)num_sms;
-  struct RV {
-    int id, bm, bnc, wnc, threads, acc;
-    double eff;
-  };
-  static const RV rv[] = {{100, 128, 96, 32, 384, 32, 1.0}, {101, 128, 64, 32, 256, 32, 0.97},
-                          {102, 128, 32, 16, 256, 16, 0.93}};
-  const char* fs = getenv("CHFSI_FILTER_VARIANT_REAL");
-  const int forced = fs ? atoi(fs) : -1;
-  int best = 0;
-  double best_cost = 1e300;
-  for (int v = 0; v < 3; ++v) {
-    if (forced >= 0 && rv[v].id != forced) continue;
-    const int64_t tm = (nrows + rv[v].bm - 1) / rv[v].bm;
-    const int64_t units = (ncols + rv[v].wnc - 1) / rv[v].wnc;
-    const int64_t tn = (ncols + rv[v].bnc - 1) / rv[v].bnc;
-    const int64_t per = (units + tn - 1) / tn;
-    const double cols = 0.3 * (double)(tn * per * rv[v].wnc) + 0.7 * (double)ncols;
-    const double cost = (double)tm * rv[v].bm * cols / rv[v].eff;
-    if (cost < best_cost * 0.999) {
-      best_cost = cost;
-      best = v;
-    }
-  }
-  return TileChoice{rv[best].id, rv[best].bm, rv[best].bnc, rv[best].threads, rv[best].acc, rv[best].wnc};
+  (void)num_sms;  // the persistent stream-K schedule removes wave quantisation
+  return choose(kVariants, "CHFSI_FILTER_VARIANT", nrows, ncols, 1.0, 11.8);
 }
 
 TileChoice choose_filter_tile_z3(int64_t nrows, int64_t ncols, int num_sms) {
   (void)num_sms;
-  // 3M variants: accumulators are 3 sets (P1, P2, P3) of (WM/8) x (WNC/8) 8x8 tiles
-  struct ZV {
-    int id, bm, bnc, wnc, threads, acc;
-    double eff;
-  };
-  // eff: measured full-width rates relative to 200 (n = 13000, k = 624: 45.2 / 42.0 / 32.4 / 41.8 /
-  // 30.2 TF/s ZGEMM-equivalent; profiles/r01_z3_variants.log)
-  static const ZV zv[] = {{200, 128, 48, 16, 384, 48, 1.0},  {201, 128, 32, 16, 256, 48, 0.93},
-                          {202, 128, 16, 8, 256, 24, 0.72},  {203, 64, 64, 16, 256, 48, 0.925},
-                          {204, 192, 32, 16, 384, 48, 0.67}};
-  const int nv = (int)(sizeof(zv) / sizeof(zv[0]));
-  const char* fs = getenv("CHFSI_FILTER_VARIANT_Z3");
-  const int forced = fs ? atoi(fs) : -1;
-  int best = 0;
-  double best_cost = 1e300;
-  for (int v = 0; v < nv; ++v) {
-    if (forced >= 0 && zv[v].id != forced) continue;
-    const int64_t tm = (nrows + zv[v].bm - 1) / zv[v].bm;
-    const int64_t units = (ncols + zv[v].wnc - 1) / zv[v].wnc;
-    const int64_t tn = (ncols + zv[v].bnc - 1) / zv[v].bnc;
-    const int64_t per = (units + tn - 1) / tn;
-    const int warps_m = zv[v].threads / 32 / (zv[v].bnc / zv[v].wnc);
-    const double active_warps = (double)per * warps_m;
-    const double occ = active_warps >= 8 ? 1.0 : 0.6 + 0.05 * active_warps;
-    const double cols = 0.3 * (double)(tn * per * zv[v].wnc) + 0.7 * (double)ncols;
-    const double cost = (double)tm * zv[v].bm * cols / (zv[v].eff * occ);
-    if (cost < best_cost * 0.999) {
-      best_cost = cost;
-      best = v;
-    }
-  }
-  return TileChoice{zv[best].id, zv[best].bm, zv[best].bnc, zv[best].threads, zv[best].acc, zv[best].wnc};
+  return choose(kVariantsZ3, "CHFSI_FILTER_VARIANT_Z3", nrows, ncols, 45.5 / 34.9, 17.7);
+}
+
+TileChoice choose_filter_tile_real(int64_t nrows, int64_t ncols, int num_sms) {
+  (void)num_sms;  // real: 2 n flops per column-row; speed / memory in the same relative units
+  return choose(kVariantsReal, "CHFSI_FILTER_VARIANT_REAL", nrows, ncols, 1.0, 20.0);
+}
+
+// K1 stage refill protocol (StepParams::refill_mode); CHFSI_K1_REFILL overrides (A/B measurements)
+static int refill_mode() {
+  static const int m = [] {
+    const char* e = getenv("CHFSI_K1_REFILL");
+    return e ? atoi(e) : 0;
+  }();
+  return m;
 }
 
 void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
+  p.refill_mode = refill_mode();
   const int64_t ncols = p.col_end - p.col0;
   const int64_t tm = (p.nrows + t.bm - 1) / t.bm, tn = (ncols + t.bnc - 1) / t.bnc;
   p.units_n = (int32_t)((ncols + t.wnc - 1) / t.wnc);
@@ -184,6 +169,12 @@ cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, cons
       return LC(128, 64, 64, 16, 4, kZ4M);
     case 9:
       return LC(256, 32, 64, 16, 3, kZ4M);
+    case 10:
+      return LC(256, 4, 32, 4, 3, kZ4M);
+    case 11:
+      return LC(128, 8, 32, 4, 6, kZ4M);
+    case 12:
+      return LC(128, 12, 32, 4, 6, kZ4M);
     // real symmetric (columns are real columns)
     case 100:
       return LC(128, 96, 32, 32, 3, kReal);

@@ -52,6 +52,7 @@ struct StepParams {
   int64_t y3_off;
   int64_t y3_off_r;
   int* nonfinite;       // set to 1 if any written value is not finite (nullable)
+  int32_t refill_mode;  // 0: thread 0 refills one stage behind; 1: the last warp to release a stage refills it
 };
 
 constexpr int kBKHalf = 16;            // doubles per 128-byte swizzle row
@@ -80,10 +81,15 @@ struct FilterCfg {
   static constexpr int kNT = MODE == kZ4M ? WNC / 4 : WNC / 8;  // 8-real-column MMA tiles per warp
   static constexpr int kNP = MODE == kZ3M ? 3 : 1;              // accumulator sets (P1, P2, P3)
   static constexpr int kA3 = MODE == kZ3M ? BM * 128 : 0;       // a_r - a_i plane, one swizzle row
-  static constexpr int kB3 = MODE == kZ3M ? BNC * 128 : 0;      // y_r + y_i plane
+  // B regions start on 1024-byte boundaries (the 128B-swizzle pattern is taken from absolute shared
+  // address bits, so a region must begin at an 8-row atom): BNC rows padded to a multiple of 8
+  static constexpr int kBRow = ((BNC + 7) / 8) * 8 * 128;       // smem stride of one B swizzle region
+  static constexpr int kB3 = MODE == kZ3M ? kBRow : 0;          // y_r + y_i plane
   static constexpr int kABytes = kHalves * BM * 128 + kA3;
-  static constexpr int kBBytes = kHalves * BNC * 128 + kB3;
+  static constexpr int kBBytes = kHalves * kBRow + kB3;
   static constexpr int kStageBytes = kABytes + kBBytes;
+  // bytes the stage's TMA boxes deliver (mbarrier transaction count)
+  static constexpr int kTxBytes = kHalves * BM * 128 + kA3 + (kHalves + (MODE == kZ3M ? 1 : 0)) * BNC * 128;
   static constexpr int kSmemBytes = STAGES * kStageBytes + 2 * STAGES * 8 + 1024;  // + barriers + align
   static_assert(WM % 8 == 0 && WNC % (MODE == kZ4M ? 4 : 8) == 0 && BM % WM == 0 && BNC % WNC == 0, "tile shape");
   static_assert(BM <= 256 && BNC <= 256, "TMA box limit");
@@ -134,6 +140,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes);
   uint64_t* empty = full + STAGES;
   __shared__ int s_ticket;
+  __shared__ int refill_cnt[STAGES];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -148,6 +155,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], Cfg::kConsumerWarps);
+      refill_cnt[s] = 0;
     }
     fence_barrier_init();
   }
@@ -196,7 +204,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     const int bcol = p.b_col0 + tile_cols(pc_tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
     uint8_t* sa = smem + pc_stage * Cfg::kStageBytes;
     uint8_t* sb = sa + Cfg::kABytes;
-    mbar_arrive_expect_tx(&full[pc_stage], Cfg::kStageBytes);
+    mbar_arrive_expect_tx(&full[pc_stage], Cfg::kTxBytes);
     const int q = pc_kt / p.kt_per_rank;
     const int t = pc_kt - q * p.kt_per_rank;
     const int ka = q * p.a_rank_stride + t * kBK;
@@ -204,11 +212,11 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
 #pragma unroll
     for (int h = 0; h < kHalves; ++h) {
       tma_load_2d(sa + h * BM * 128, &tmA, ka + h * kBKHalf, m0, &full[pc_stage]);
-      tma_load_3d(sb + h * BNC * 128, &tmB, kb + h * kBKHalf, bcol, q, &full[pc_stage]);
+      tma_load_3d(sb + h * Cfg::kBRow, &tmB, kb + h * kBKHalf, bcol, q, &full[pc_stage]);
     }
     if constexpr (MODE == kZ3M) {  // the real planes: 16 complex entries = one 128-byte row
       tma_load_2d(sa + kHalves * BM * 128, &tmA3, ka / 2, m0, &full[pc_stage]);
-      tma_load_3d(sb + kHalves * BNC * 128, &tmB3, kb / 2, bcol, q, &full[pc_stage]);
+      tma_load_3d(sb + kHalves * Cfg::kBRow, &tmB3, kb / 2, bcol, q, &full[pc_stage]);
     }
     ++pc_j;
     if (++pc_stage == STAGES) pc_stage = 0;
@@ -225,6 +233,30 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       }
     }
   };
+  // load CTA-local iteration jj into stage st (last-arriver mode: position from the iteration index)
+  auto produce_at = [&](int64_t jj, int st) {
+    int tile, kt;
+    coords(jj, tile, kt);
+    const int m0 = (tile / p.tiles_n) * BM;
+    int nu;
+    const int bcol = p.b_col0 + tile_cols(tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
+    uint8_t* sa = smem + st * Cfg::kStageBytes;
+    uint8_t* sb = sa + Cfg::kABytes;
+    mbar_arrive_expect_tx(&full[st], Cfg::kTxBytes);
+    const int q = kt / p.kt_per_rank;
+    const int t = kt - q * p.kt_per_rank;
+    const int ka = q * p.a_rank_stride + t * kBK;
+    const int kb = t * kBK;
+#pragma unroll
+    for (int h = 0; h < kHalves; ++h) {
+      tma_load_2d(sa + h * BM * 128, &tmA, ka + h * kBKHalf, m0, &full[st]);
+      tma_load_3d(sb + h * Cfg::kBRow, &tmB, kb + h * kBKHalf, bcol, q, &full[st]);
+    }
+    if constexpr (MODE == kZ3M) {
+      tma_load_2d(sa + kHalves * BM * 128, &tmA3, ka / 2, m0, &full[st]);
+      tma_load_3d(sb + kHalves * Cfg::kBRow, &tmB3, kb / 2, bcol, q, &full[st]);
+    }
+  };
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
@@ -236,7 +268,11 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     pc_stage = 0;
     pc_dp_left = p.dp_units;
     pc_init();
-    while (pc_j < STAGES && pc_j < my_iters) produce();
+    if (p.refill_mode == 0) {
+      while (pc_j < STAGES && pc_j < my_iters) produce();
+    } else {
+      for (int64_t jj = 0; jj < STAGES && jj < my_iters; ++jj) produce_at(jj, (int)jj);
+    }
   }
 
   const int wm = warp % Cfg::kWarpsM;
@@ -399,11 +435,11 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       if constexpr (MODE == kZ3M) {
         if (warp_active) {
           const uint8_t* a3 = sa + kHalves * BM * 128;
-          const uint8_t* b3 = sb + kHalves * BNC * 128;
+          const uint8_t* b3 = sb + kHalves * Cfg::kBRow;
 #pragma unroll
           for (int h = 0; h < kHalves; ++h) {
             const uint8_t* ah = sa + h * BM * 128;
-            const uint8_t* bh = sb + h * BNC * 128;
+            const uint8_t* bh = sb + h * Cfg::kBRow;
 #pragma unroll
             for (int sub = 0; sub < 2; ++sub) {
               // P1, P2: complex entry 2*qd + sub of this half -> (a_r, a_i) and (y_r, y_i) in one LDS.128
@@ -422,9 +458,11 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
 #pragma unroll
                 for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc2[i][jj][0], acc2[i][jj][1], av[i].y, bv[jj].y);
             }
-            // P3: entries 8h + 2qd + {0, 1} of the planes (one 16-byte chunk of the 128-byte row)
+            // P3: plane entries 2c, 2c+1 of chunk c = 2qd + h of the 128-byte row (h = 0, 1 cover all 16
+            // entries; even/odd chunks for the two rows of a quarter-warp keep the LDS.128 conflict-free
+            // under the 128B swizzle, chunk' = c ^ (row & 7))
             {
-              const int chunk = 4 * h + qd;
+              const int chunk = 2 * qd + h;
               double2 cv[Cfg::kMT], dv[Cfg::kNT];
 #pragma unroll
               for (int i = 0; i < Cfg::kMT; ++i) cv[i] = *reinterpret_cast<const double2*>(a3 + swz(a_row0 + i * 8, chunk));
@@ -445,7 +483,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
 #pragma unroll
       for (int h = 0; h < kHalves && warp_active; ++h) {
         const uint8_t* ah = sa + h * BM * 128;
-        const uint8_t* bh = sb + h * BNC * 128;
+        const uint8_t* bh = sb + h * Cfg::kBRow;
 #pragma unroll
         for (int sub = 0; sub < 2; ++sub) {
           // k-steps 2*sub, 2*sub+1 of this half: lane qd covers doubles 4*qd + 2*sub + {0,1}
@@ -476,12 +514,22 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      // refill the stage of iteration j - 1 (stage pc_stage, phase of j - 1) with iteration pc_j
-      if (threadIdx.x == 0 && j >= 1 && *(volatile int64_t*)&pc_j < my_iters) {
-        const uint32_t prev_phase = (s == 0) ? (phase ^ 1u) : phase;
-        mbar_wait(&empty[pc_stage], prev_phase);
-        produce();
+      if (p.refill_mode == 0) {
+        if (lane == 0) mbar_arrive(&empty[s]);
+        // refill the stage of iteration j - 1 (stage pc_stage, phase of j - 1) with iteration pc_j
+        if (threadIdx.x == 0 && j >= 1 && *(volatile int64_t*)&pc_j < my_iters) {
+          const uint32_t prev_phase = (s == 0) ? (phase ^ 1u) : phase;
+          mbar_wait(&empty[pc_stage], prev_phase);
+          produce();
+        }
+      } else if (lane == 0) {
+        // last-arriver refill: the warp that releases stage s last loads iteration j + STAGES into it,
+        // so no warp ever blocks on a release (the count grows by kConsumerWarps per use of the stage)
+        const int old = atomicAdd(&refill_cnt[s], 1);
+        if (old % Cfg::kConsumerWarps == Cfg::kConsumerWarps - 1 && j + STAGES < my_iters) {
+          fence_proxy_async_shared();
+          produce_at(j + STAGES, s);
+        }
       }
       if (++stage == STAGES) {
         stage = 0;
@@ -546,6 +594,7 @@ struct TileChoice {
   int threads;  // CTA size of the variant
   int acc;      // accumulator doubles per thread (partial-slot size = acc * threads doubles)
   int wnc;      // complex columns per warp (column-unit width of the balanced N split)
+  double cost;  // model time of the step (choose_*: comparable between the 3M and 4M families)
 };
 TileChoice choose_filter_tile(int64_t nrows, int64_t ncols, int num_sms);
 // Fill the persistent-schedule fields of p (tiles_n .. tail_iters) for variant t on num_sms SMs.

@@ -9,9 +9,10 @@ python -m pytest tests/test_gpu_multirank.py -q -x > gpurun_out/${TAG}_pytest_mu
 tail -2 gpurun_out/${TAG}_pytest_multirank.log
 timeout 1500 python tools/c4_sweep.py 8192,16384,32768 64,256,1024,2048 --parity > gpurun_out/${TAG}_sweep.jsonl 2> gpurun_out/${TAG}_sweep.err; echo "sweep rc=$?"
 cat gpurun_out/${TAG}_sweep.jsonl
-for KK in 1024 8; do
-  PERF="python tools/filter_perf.py 16384 $KK 4 auto"
-  $PERF > gpurun_out/${TAG}_perf_k$KK.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:filter_step -s 4 -c 1 -o gpurun_out/${TAG}_k1_n16384_k$KK -f $PERF > gpurun_out/${TAG}_ncu_k$KK.log 2>&1
-  echo "ncu k=$KK rc=$?"
+for NK in "16384 1024" "16384 8" "13000 624"; do
+  set -- $NK
+  PERF="python tools/filter_perf.py $1 $2 4 auto3"
+  $PERF > gpurun_out/${TAG}_perf_n$1_k$2.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:filter_step -s 4 -c 1 -o gpurun_out/${TAG}_k1_n$1_k$2 -f $PERF > gpurun_out/${TAG}_ncu_n$1_k$2.log 2>&1
+  echo "ncu n=$1 k=$2 rc=$?"
 done
