@@ -196,6 +196,9 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="allgather", choices=["allgather", "push"],
+                    help="N > 1: per-step operand exchange (pipelined in-place allgather, or the filter "
+                         "epilogue's peer push)")
     ap.add_argument("--zmul", type=int, default=3, choices=[3, 4],
                     help="complex filter arithmetic: 3 = Gauss 3M (default), 4 = 4M real embedding")
     ap.add_argument("--emulate-ranks", type=int, default=1,
@@ -355,6 +358,8 @@ def rank_main(args, cf, rank, world, local_rank, group):
     ctx = group.context(chfsi, local_rank, rank, world) if group else chfsi.Context(local_rank)
     ctx.set_complex_mult(args.zmul)
     ctx.reserve(n, nloc, k)
+    if world > 1 and args.exchange == "push":
+        ctx.set_exchange(1)  # collective: maps every rank's operand buffers
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -417,11 +422,13 @@ def rank_main(args, cf, rank, world, local_rank, group):
                        "eigenvalues/residuals read back per problem, the final block once"}
 
     # roofline of K1: FP64 DMMA-bound contraction; achieved from the filter calls' CUDA-event time
-    traffic = None
+    traffic, traffic_info = None, None
     tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            tj = json.load(open(tp))
+            traffic = tj.get("dram_bytes_per_launch")
+            traffic_info = {k: tj.get(k) for k in ("launch", "algorithmic_bytes_per_launch", "source")}
         except Exception:
             traffic = None
     # the tensor work K1 executes per complex multiply-add: 6 real flops (3M) or 8 (4M); `value` and
@@ -435,7 +442,7 @@ def rank_main(args, cf, rank, world, local_rank, group):
                 "flops_per_launch": flops * tensor_per_zmac / 8.0 / max(k1_launches, 1),
                 "achieved_def": (f"{tensor_per_zmac:g} n^2 sum(deg) (the real FP64 tensor flops of the {args.zmul}M "
                                  "complex product) over the timed problems / sum of CUDA-event times of the K1 launches"),
-                "achieved_zgemm_equivalent": k1_tf,
+                "achieved_zgemm_equivalent": k1_tf, "traffic_launch": traffic_info,
                 "peak_source": "measured FP64 DMMA peak (register-only DMMA loop, 1965 MHz), profiles/r01_fp64_peaks.txt"}
 
     cpu = None
@@ -459,6 +466,7 @@ def rank_main(args, cf, rank, world, local_rank, group):
                        "problems": f"{W} warm-up + {K} timed of the correlated sequence",
                        "parallelism": (f"1-D row panels over {world} emulated ranks on one GPU" if args.emulate_ranks > 1
                                        else f"1-D row panels over {world} GPU(s)" if world > 1 else "single GPU"),
+                       "exchange": args.exchange if world > 1 else None, "complex_mult": f"{args.zmul}M",
                        "l2": "inputs larger than L2 (H panel per problem >> 126 MB)"},
             "time_per_eigenproblem_s": ms / K / 1e3,
             "filter_kernel_tflops": filt_tf, "frac_of_peak": filt_tf * tensor_per_zmac / 8.0 / FP64_PEAK_TFLOPS,

@@ -83,6 +83,21 @@ int64_t chfsi_kernel_launches(chfsi_ctx ctx);
  * creation. Errors: CHFSI_ERR_ARG for a null ctx or mults not in {3, 4}. */
 chfsi_status chfsi_ctx_set_complex_mult(chfsi_ctx ctx, int32_t mults);
 
+/* nranks > 1 only, collective (every rank calls it): how the filter's next-step operand is exchanged
+ * (BASELINE.json north_star: Y is rebuilt each degree step across the row panels).
+ *  mode 0 (default): in-place allgather per column group on a communication stream, overlapped with the
+ *          next group's filter kernel (chfsi_ctx_set_pipeline).
+ *  mode 1: peer push. The filter kernel's epilogue stores this rank's rows of every still-active column
+ *          straight into every rank's next-step operand buffer through NVLink peer pointers (CUDA IPC
+ *          mappings between processes; plain pointers between the ranks of a local group), so the
+ *          exchange overlaps the MMAs tile by tile; one small barrier (a one-element NCCL allreduce, or
+ *          the local group's event barrier) separates consecutive steps.
+ * Mode 1 requires the workspace to be reserved first (chfsi_ctx_reserve with the largest n, nloc and
+ * block width to be used); the ranks' buffers are then pinned: a later chfsi_ctx_reserve or filter
+ * call needing a larger block returns CHFSI_ERR_ARG. Errors: CHFSI_ERR_ARG (null ctx, bad mode, no
+ * reservation), CHFSI_ERR_CUDA (IPC mapping failed), CHFSI_ERR_NCCL. No-op at nranks == 1. */
+chfsi_status chfsi_ctx_set_exchange(chfsi_ctx ctx, int32_t mode);
+
 /* nranks > 1 only: overlap of the per-step exchange with the filter's MMAs (BASELINE.json north_star
  * "Transfers overlap the next panel's MMA"; SURVEY 8(e) "Overlap"). The active columns of every filter
  * step are cut into G contiguous column groups of >= group_cols columns (G <= 16; group_cols = 0: one

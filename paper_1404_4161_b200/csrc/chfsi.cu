@@ -278,7 +278,7 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
 // >= pipe_group_cols wide (G = 1 at p == 1: nothing to overlap).
 static std::vector<int64_t> filter_groups(chfsi_ctx ctx, int64_t k) {
   int64_t G = 1;
-  if (ctx->nranks > 1 && ctx->pipe_group_cols > 0) G = std::max<int64_t>(1, std::min<int64_t>(k / ctx->pipe_group_cols, 16));
+  if (ctx->nranks > 1 && ctx->exchange == 0 && ctx->pipe_group_cols > 0) G = std::max<int64_t>(1, std::min<int64_t>(k / ctx->pipe_group_cols, 16));
   std::vector<int64_t> gb(G + 1);
   for (int64_t g = 0; g <= G; ++g) gb[g] = g * k / G;
   return gb;
@@ -327,8 +327,16 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
   if (!st) st = ensure(ctx, ctx->L1, sizeof(double) * cw * (size_t)ldl * k);
   if (!st) st = ensure(ctx, ctx->flag, 64);
   const int64_t ldp = (elem == 1 || z3) ? round_up(nloc, 2) : nloc;  // packed column stride (per plane)
-  if (p > 1 && !st) st = ensure(ctx, ctx->R0, sizeof(double) * cw * (size_t)ldp * p * k);
-  if (p > 1 && !st) st = ensure(ctx, ctx->R1, sizeof(double) * cw * (size_t)ldp * p * k);
+  const bool push = p > 1 && ctx->exchange == 1;
+  const size_t rbytes = sizeof(double) * cw * (size_t)ldp * p * k;
+  if (push && !st && rbytes > ctx->peer_R_bytes) {  // peers hold pointers into R0 / R1: no regrowth
+    set_err(ctx, "chfsi_filter: peer exchange needs " + std::to_string(rbytes) +
+                     " bytes of packed-operand workspace per buffer; chfsi_ctx_reserve a larger block before "
+                     "chfsi_ctx_set_exchange");
+    return CHFSI_ERR_ARG;
+  }
+  if (p > 1 && !st) st = ensure(ctx, ctx->R0, rbytes);
+  if (p > 1 && !st) st = ensure(ctx, ctx->R1, rbytes);
   if (!st) st = a_operand(ctx, &Hp, &ldh, n, nloc, elem);
   if (st) return st;
   const std::vector<int64_t> gb = filter_groups(ctx, k);
@@ -448,7 +456,15 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       sp.out = static_cast<double2*>(Y);
       sp.ld_out = ldy;
       if (p > 1 && ka_next > 0) {
-        sp.r_next = reinterpret_cast<double2*>(region(oth, g) + (size_t)cw * ldp * ka_next * ctx->rank);
+        const size_t chunk_off = (size_t)cw * ldp * p * gb[g] + (size_t)cw * ldp * ka_next * ctx->rank;
+        if (push) {  // this rank's chunk in every rank's next-step operand (NVLink peer stores)
+          for (int q = 0; q < p; ++q)
+            sp.r_dst[q] = reinterpret_cast<double2*>((oth ? ctx->peer_R1[q] : ctx->peer_R0[q]) + chunk_off);
+          sp.n_rdst = p;
+        } else {
+          sp.r_dst[0] = reinterpret_cast<double2*>(R[oth] + chunk_off);
+          sp.n_rdst = 1;
+        }
         sp.ld_r_next = z3 ? 3 * ldp / 2 : ldp;
         sp.y3_off_r = 2 * ldp;
       }
@@ -463,7 +479,10 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used + 1], ctx->stream));
       nev_used += 2;
       ctx->launches++;
-      if (p > 1 && ka_next > 0) {  // complete step i+1's operand of this group behind the next group's K1
+      if (push && ka_next > 0) {  // every rank's pushes of step i land before anyone's step i+1
+        st = comm_barrier(ctx, ctx->stream);
+        if (st) return st;
+      } else if (p > 1 && ka_next > 0) {  // complete step i+1's operand of this group behind the next group's K1
         CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->grp_k[g], ctx->stream));
         CHFSI_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm_stream, ctx->grp_k[g], 0));
         st = comm_allgather_inplace(ctx, region(oth, g), (size_t)cw * ldp * ka_next, ctx->comm_stream);
@@ -570,6 +589,11 @@ chfsi_status chfsi_ctx_create_local(chfsi_ctx* out, int32_t device, void* cuda_s
 chfsi_status chfsi_ctx_reserve(chfsi_ctx ctx, int64_t n, int64_t nloc, int64_t kmax) {
   if (!ctx || n < 1 || nloc < 1 || kmax < 1 || nloc > n) return CHFSI_ERR_ARG;
   cudaSetDevice(ctx->device);
+  if (ctx->exchange == 1 && ctx->nranks > 1 &&
+      sizeof(double) * 3 * (size_t)round_up(nloc, 2) * ctx->nranks * kmax > ctx->peer_R_bytes) {
+    set_err(ctx, "chfsi_ctx_reserve: the peer exchange is on; reserve before chfsi_ctx_set_exchange");
+    return CHFSI_ERR_ARG;  // peers hold pointers into R0 / R1
+  }
   const size_t ldl = (size_t)round_up(nloc, 2);
   const size_t blk = sizeof(double) * 3 * ldl * kmax;  // 3M column layout (the widest)
   chfsi_status st = CHFSI_OK;
@@ -613,6 +637,25 @@ int64_t chfsi_kernel_launches(chfsi_ctx ctx) { return ctx ? ctx->launches : 0; }
 chfsi_status chfsi_ctx_set_complex_mult(chfsi_ctx ctx, int32_t mults) {
   if (!ctx || (mults != 3 && mults != 4)) return CHFSI_ERR_ARG;
   ctx->zmul = mults;
+  return CHFSI_OK;
+}
+
+chfsi_status chfsi_ctx_set_exchange(chfsi_ctx ctx, int32_t mode) {
+  if (!ctx || (mode != 0 && mode != 1)) return CHFSI_ERR_ARG;
+  ctx->err.clear();
+  if (ctx->nranks == 1) {
+    ctx->exchange = mode;
+    return CHFSI_OK;
+  }
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return CHFSI_ERR_CUDA;
+  if (mode == 0) {
+    comm_close_peers(ctx);
+    ctx->exchange = 0;
+    return CHFSI_OK;
+  }
+  chfsi_status st = comm_open_peers(ctx);
+  if (st) return st;
+  ctx->exchange = 1;
   return CHFSI_OK;
 }
 

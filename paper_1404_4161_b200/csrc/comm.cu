@@ -10,7 +10,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "ctx.cuh"
@@ -87,7 +89,10 @@ chfsi_status comm_init(chfsi_ctx ctx) {
   return CHFSI_OK;
 }
 
+void comm_close_peers(chfsi_ctx ctx);
+
 void comm_destroy(chfsi_ctx ctx) {
+  comm_close_peers(ctx);
   if (ctx->comm && ctx->comm->scratch) cudaFree(ctx->comm->scratch);
   if (ctx->comm && ctx->comm->owns_comm && ctx->comm->comm) {
     auto destroy = reinterpret_cast<decltype(&ncclCommDestroy)>(dlsym(ctx->comm->lib, "ncclCommDestroy"));
@@ -199,6 +204,127 @@ chfsi_status comm_bcast(chfsi_ctx ctx, double* buf, size_t count, int root) {
   }
   return nccl_check(ctx, ctx->comm->bcast(buf, buf, count, ncclDouble, root, ctx->comm->comm, ctx->stream),
                     "ncclBroadcast");
+}
+
+chfsi_status comm_barrier(chfsi_ctx ctx, cudaStream_t st) {
+  if (ctx->nranks == 1) return CHFSI_OK;
+  if (!st) st = ctx->stream;
+  if (ctx->comm->local) {
+    lg_enter(ctx, nullptr, st);
+    lg_exit(ctx, st);
+    return CHFSI_OK;
+  }
+  if (!ctx->comm->scratch) CHFSI_CUDA_TRY(ctx, cudaMalloc(&ctx->comm->scratch, sizeof(double) * 8));
+  return nccl_check(ctx, ctx->comm->allreduce(ctx->comm->scratch, ctx->comm->scratch, 1, ncclDouble, ncclSum,
+                                              ctx->comm->comm, st),
+                    "ncclAllReduce (barrier)");
+}
+
+namespace {
+struct PeerInfo {
+  cudaIpcMemHandle_t h0, h1;
+  uint64_t bytes;
+  int32_t device;
+  int32_t pad;
+};
+}  // namespace
+
+chfsi_status comm_open_peers(chfsi_ctx ctx) {
+  const int P = ctx->nranks;
+  comm_close_peers(ctx);
+  ctx->peer_R0.assign(P, nullptr);
+  ctx->peer_R1.assign(P, nullptr);
+  const size_t mine = std::min(ctx->R0.bytes, ctx->R1.bytes);
+  if (!ctx->R0.ptr || !ctx->R1.ptr) {
+    set_err(ctx, "peer exchange: reserve the workspace first (chfsi_ctx_reserve)");
+    return CHFSI_ERR_ARG;
+  }
+  if (ctx->comm->local) {  // one process, one device: the group table holds every rank's pointers
+    chfsi_local_group g = ctx->comm->local;
+    {
+      std::lock_guard<std::mutex> lk(g->m);
+      if ((int)g->R0s.size() != P) {
+        g->R0s.assign(P, nullptr);
+        g->R1s.assign(P, nullptr);
+        g->Rbytes.assign(P, 0);
+      }
+      g->R0s[ctx->rank] = ctx->R0.ptr;
+      g->R1s[ctx->rank] = ctx->R1.ptr;
+      g->Rbytes[ctx->rank] = mine;
+    }
+    g->barrier();
+    size_t mn = mine;
+    for (int q = 0; q < P; ++q) {
+      ctx->peer_R0[q] = static_cast<double*>(g->R0s[q]);
+      ctx->peer_R1[q] = static_cast<double*>(g->R1s[q]);
+      mn = std::min(mn, g->Rbytes[q]);
+    }
+    g->barrier();
+    ctx->peer_R_bytes = mn;
+    return CHFSI_OK;
+  }
+  // separate processes: CUDA IPC handles of R0 / R1, gathered over the library's NCCL communicator
+  PeerInfo me{};
+  CHFSI_CUDA_TRY(ctx, cudaIpcGetMemHandle(&me.h0, ctx->R0.ptr));
+  CHFSI_CUDA_TRY(ctx, cudaIpcGetMemHandle(&me.h1, ctx->R1.ptr));
+  me.bytes = mine;
+  me.device = ctx->device;
+  const size_t chunk = (sizeof(PeerInfo) + 7) / 8;  // in doubles
+  double* d = nullptr;
+  CHFSI_CUDA_TRY(ctx, cudaMalloc(&d, sizeof(double) * chunk * P));
+  std::vector<PeerInfo> all(P);
+  chfsi_status st = CHFSI_OK;
+  if (cudaMemcpyAsync(d + chunk * ctx->rank, &me, sizeof(me), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
+    st = CHFSI_ERR_CUDA;
+  if (!st) st = comm_allgather_inplace(ctx, d, chunk, ctx->stream);
+  for (int q = 0; q < P && !st; ++q)
+    if (cudaMemcpyAsync(&all[q], d + chunk * q, sizeof(PeerInfo), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
+      st = CHFSI_ERR_CUDA;
+  if (!st && cudaStreamSynchronize(ctx->stream) != cudaSuccess) st = CHFSI_ERR_CUDA;
+  cudaFree(d);
+  if (st) {
+    set_err(ctx, "peer exchange: gathering the IPC handles failed");
+    return st;
+  }
+  size_t mn = mine;
+  for (int q = 0; q < P; ++q) {
+    mn = std::min<size_t>(mn, all[q].bytes);
+    if (q == ctx->rank) {
+      ctx->peer_R0[q] = static_cast<double*>(ctx->R0.ptr);
+      ctx->peer_R1[q] = static_cast<double*>(ctx->R1.ptr);
+      continue;
+    }
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, ctx->device, all[q].device);
+    if (can) {
+      cudaError_t e = cudaDeviceEnablePeerAccess(all[q].device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    }
+    void* p0 = nullptr;
+    void* p1 = nullptr;
+    if (cudaIpcOpenMemHandle(&p0, all[q].h0, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&p1, all[q].h1, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      if (p0) cudaIpcCloseMemHandle(p0);
+      comm_close_peers(ctx);
+      set_err(ctx, "peer exchange: cudaIpcOpenMemHandle failed for rank " + std::to_string(q));
+      return CHFSI_ERR_CUDA;
+    }
+    ctx->ipc_opened.push_back(p0);
+    ctx->ipc_opened.push_back(p1);
+    ctx->peer_R0[q] = static_cast<double*>(p0);
+    ctx->peer_R1[q] = static_cast<double*>(p1);
+  }
+  ctx->peer_R_bytes = mn;
+  return comm_barrier(ctx, ctx->stream);
+}
+
+void comm_close_peers(chfsi_ctx ctx) {
+  for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+  ctx->ipc_opened.clear();
+  ctx->peer_R0.clear();
+  ctx->peer_R1.clear();
+  ctx->peer_R_bytes = 0;
 }
 
 }  // namespace chfsi

@@ -23,6 +23,8 @@ struct chfsi_local_group_s {
   long generation = 0;
   std::vector<const void*> bufs;
   std::vector<cudaEvent_t> ready, done;
+  std::vector<void*> R0s, R1s;  // peer push: every rank's packed operand buffers (same device)
+  std::vector<size_t> Rbytes;
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
     const long gen = generation;
@@ -70,6 +72,13 @@ struct chfsi_ctx_s {
   // p > 1 filter pipelining (SURVEY 8(e) "Overlap"): the active block is cut into column groups of
   // >= pipe_group_cols columns; group g's allgather (comm_stream) overlaps group g+1's K1 (stream).
   // pipe_sm_reserve SMs are left out of K1's persistent grid for the collective's CTAs.
+  // p > 1 exchange of the filter's next-step operand: 0 = in-place allgather per column group on a
+  // communication stream; 1 = peer push (K1's epilogue stores this rank's chunk straight into every
+  // rank's buffer through peer pointers, then one small barrier per step)
+  int32_t exchange = 0;
+  std::vector<double*> peer_R0, peer_R1;  // exchange 1: rank q's R0 / R1 as addressed from here
+  size_t peer_R_bytes = 0;                // smallest R buffer over the ranks (no regrowth after)
+  std::vector<void*> ipc_opened;          // peer mappings to close (cudaIpcCloseMemHandle)
   int32_t pipe_group_cols = 128;
   int32_t pipe_sm_reserve = 0;
   cudaStream_t comm_stream = nullptr;
@@ -124,6 +133,12 @@ void comm_destroy(chfsi_ctx ctx);
 chfsi_status comm_allgather_inplace(chfsi_ctx ctx, double* buf, size_t count, cudaStream_t st = nullptr);
 chfsi_status comm_allreduce_sum(chfsi_ctx ctx, double* buf, size_t count);
 chfsi_status comm_bcast(chfsi_ctx ctx, double* buf, size_t count, int root);
+// every rank's work enqueued on `st` before the call is complete before any rank's later work on `st`
+// (NCCL: a one-element allreduce; local group: events + host barrier)
+chfsi_status comm_barrier(chfsi_ctx ctx, cudaStream_t st);
+// collective: make every rank's R0 / R1 addressable from every rank (exchange 1)
+chfsi_status comm_open_peers(chfsi_ctx ctx);
+void comm_close_peers(chfsi_ctx ctx);
 
 // internal (no status marshalling) versions of the public entry points, used by the solver
 chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,

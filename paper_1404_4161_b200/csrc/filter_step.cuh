@@ -45,7 +45,13 @@ struct StepParams {
   int64_t ld_next;
   double2* out;         // finished columns (caller's Y)
   int64_t ld_out;
-  double2* r_next;      // p > 1: this rank's chunk of the next step's packed B operand (nullable)
+  // p > 1: this rank's chunk of the next step's packed B operand. n_rdst = 1: the chunk in this rank's
+  // buffer (completed by an allgather); n_rdst = nranks (peer push): the chunk in every rank's buffer,
+  // stored through NVLink peer pointers by this epilogue, so the exchange overlaps the MMAs tile by
+  // tile and only a barrier remains between steps. n_rdst = 0: none.
+  static constexpr int kMaxRdst = 8;
+  double2* r_dst[kMaxRdst];
+  int32_t n_rdst;
   int64_t ld_r_next;
   // 3M mode: every B-operand column carries, after its 2*ld complex doubles, the real plane
   // y_r + y_i at double offset y3_off (state buffers) / y3_off_r (packed r_next) from the column start
@@ -320,7 +326,8 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       reinterpret_cast<double*>(p.out)[(int64_t)col * p.ld_out + r] = v;
     } else {
       reinterpret_cast<double*>(p.y_next)[(int64_t)col * p.ld_next + r] = v;
-      if (p.r_next) reinterpret_cast<double*>(p.r_next)[(int64_t)(col - p.fin_end) * p.ld_r_next + r] = v;
+      for (int q = 0; q < p.n_rdst; ++q)
+        reinterpret_cast<double*>(p.r_dst[q])[(int64_t)(col - p.fin_end) * p.ld_r_next + r] = v;
     }
   };
   // 3M: one complex output (vr, vi) of column col; also writes the y_r + y_i plane of the next operand
@@ -345,8 +352,8 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       double2* yn = p.y_next + (int64_t)col * p.ld_next;
       yn[r] = v;
       reinterpret_cast<double*>(yn)[p.y3_off + r] = vr + vi;
-      if (p.r_next) {
-        double2* rn = p.r_next + (int64_t)(col - p.fin_end) * p.ld_r_next;
+      for (int q = 0; q < p.n_rdst; ++q) {
+        double2* rn = p.r_dst[q] + (int64_t)(col - p.fin_end) * p.ld_r_next;
         rn[r] = v;
         reinterpret_cast<double*>(rn)[p.y3_off_r + r] = vr + vi;
       }
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
           p.out[(int64_t)col * p.ld_out + r] = v;
         } else {
           p.y_next[(int64_t)col * p.ld_next + r] = v;
-          if (p.r_next) p.r_next[(int64_t)(col - p.fin_end) * p.ld_r_next + r] = v;
+          for (int q = 0; q < p.n_rdst; ++q) p.r_dst[q][(int64_t)(col - p.fin_end) * p.ld_r_next + r] = v;
         }
       }
     }
@@ -585,6 +592,8 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     if (threadIdx.x == 0) p.tickets[u] = 0;  // ready for the next launch (stream ordered)
   }
   if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
+  // peer push: this thread's NVLink stores are ordered before the inter-step barrier's signal
+  if (p.n_rdst > 1) __threadfence_system();
 }
 
 // host launcher: picks the tile configuration for the step shape; returns cudaError_t

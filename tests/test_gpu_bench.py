@@ -35,3 +35,9 @@ def test_bench_emulated_ranks(P):
     d = bench("--emulate-ranks", str(P), "--no-e2e")
     assert d["emulated_ranks"] == P
     assert d["converged"] and d["max_resid_over_tol"] <= 1.0
+
+
+def test_bench_emulated_ranks_push():
+    d = bench("--emulate-ranks", "2", "--no-e2e", "--exchange", "push")
+    assert d["config"]["exchange"] == "push"
+    assert d["converged"] and d["max_resid_over_tol"] <= 1.0

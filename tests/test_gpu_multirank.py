@@ -18,9 +18,11 @@ def crand(rng, *shape):
     return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
 
 
-def run_ranks(chfsi, P, fn, group_cols=None):
+def run_ranks(chfsi, P, fn, group_cols=None, push=None):
     """Run fn(rank, ctx) for rank = 0..P-1 concurrently (one thread + one stream per rank).
-    group_cols: column-group width of the filter's comm/compute pipeline (chfsi_ctx_set_pipeline)."""
+    group_cols: column-group width of the filter's comm/compute pipeline (chfsi_ctx_set_pipeline).
+    push: (n, nloc, kmax) -> reserve that workspace and switch to the peer-push exchange (collective,
+    inside the rank threads)."""
     import torch
 
     torch.cuda.synchronize()
@@ -36,6 +38,9 @@ def run_ranks(chfsi, P, fn, group_cols=None):
     def work(r):
         try:
             with torch.cuda.stream(streams[r]):
+                if push is not None:
+                    ctxs[r].reserve(*push)
+                    ctxs[r].set_exchange(1)
                 out[r] = fn(r, ctxs[r])
                 streams[r].synchronize()
         except Exception as ex:  # pragma: no cover - surfaced below
@@ -61,11 +66,13 @@ def slabs(chfsi, H, P):
     return [chfsi.to_colmajor(np.asfortranarray(H[:, r * nloc:(r + 1) * nloc])) for r in range(P)], nloc
 
 
-@pytest.mark.parametrize("n,P,group_cols", [(512, 2, None), (600, 4, None), (256, 8, None), (512, 2, 8),
-                                             (600, 4, 10), (256, 8, 0)])
-def test_filter_multirank(gpu_lib, n, P, group_cols):
+@pytest.mark.parametrize("n,P,group_cols,push", [(512, 2, None, False), (600, 4, None, False), (256, 8, None, False),
+                                                  (512, 2, 8, False), (600, 4, 10, False), (256, 8, 0, False),
+                                                  (512, 2, None, True), (600, 4, None, True), (256, 8, None, True)])
+def test_filter_multirank(gpu_lib, n, P, group_cols, push):
     """group_cols: None = default (one group at k = 37), 8 / 10 = 4 / 3 column groups whose
-    allgathers overlap the next group's K1 on a separate stream, 0 = pipelining off."""
+    allgathers overlap the next group's K1 on a separate stream, 0 = pipelining off. push: the
+    filter epilogue stores each rank's rows into every rank's next-step operand (peer pointers)."""
     k = 37
     w = G.wy(n, int(0.9 * n), n + P)
     H = w.full()
@@ -80,7 +87,7 @@ def test_filter_multirank(gpu_lib, n, P, group_cols):
     def fn(r, ctx):
         return ctx.filter(Hs[r], Ys[r], deg, l1, c, e, n=n, row0=r * nloc)
 
-    mv = run_ranks(gpu_lib, P, fn, group_cols)
+    mv = run_ranks(gpu_lib, P, fn, group_cols, (n, n // P, k) if push else None)
     assert all(m == sum(deg) for m in mv)
     Y = np.concatenate([y.cpu().numpy() for y in Ys], axis=0)
     ctx1 = gpu_lib.Context(0)
@@ -142,8 +149,8 @@ def test_householder_fallback_multirank(gpu_lib):
     assert np.abs(Q.conj().T @ Q - np.eye(k)).max() <= 1e-13
 
 
-@pytest.mark.parametrize("P,group_cols", [(2, None), (4, None), (4, 12)])
-def test_solve_multirank_c0(gpu_lib, P, group_cols):
+@pytest.mark.parametrize("P,group_cols,push", [(2, None, False), (4, None, False), (4, 12, False), (4, None, True)])
+def test_solve_multirank_c0(gpu_lib, P, group_cols, push):
     cf = CONFIGS["c0"]
     n, nev, nex = cf["n"], cf["nev"], cf["nex"]
     w = G.wy(n, cf["nd"], cf["seed"])
@@ -156,7 +163,7 @@ def test_solve_multirank_c0(gpu_lib, P, group_cols):
         return ctx.solve_sequence(lambda ell: Hs[r], 1, Xs[r], nev, nex, cf["tol"], deg_cap=cf["cap"],
                                   seed=cf["seed"], n=n, row0=r * nloc)
 
-    out = run_ranks(gpu_lib, P, fn, group_cols)
+    out = run_ranks(gpu_lib, P, fn, group_cols, (n, n // P, nev + nex) if push else None)
     for o in out:
         assert o["status"] == 0
         assert np.max(np.abs(o["lam"][0] - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10

@@ -1,6 +1,7 @@
 #!/bin/bash
-# One gpurun call: GPU tests, the bench line, the ncu launch list of a short bench, one full ncu
-# capture of K1. Outputs land in gpurun_out/ (scratch); summaries are copied to profiles/ by hand.
+# One gpurun call: GPU tests, smoke, the bench line, the ncu launch list of a short bench, one full ncu
+# capture of K1 (c2 full-width step), the c3 bench line and the c1 ablations. Outputs land in
+# gpurun_out/ (scratch); summaries are copied to profiles/ by hand.
 set -u
 TAG=${1:-r01}
 mkdir -p gpurun_out
@@ -11,7 +12,10 @@ SHORT="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 $SHORT > gpurun_out/${TAG}_short_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $SHORT > gpurun_out/${TAG}_ncu_launches.log 2>&1
 echo "ncu launches rc=$?" >> gpurun_out/${TAG}_ncu_launches.log
-PERF="python tools/filter_perf.py 13000 624 4 auto"
+PERF="python tools/filter_perf.py 13000 624 4 auto3"
 $PERF > gpurun_out/${TAG}_perf_plain.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:filter_step -s 4 -c 1 -o gpurun_out/${TAG}_k1 -f $PERF > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/${TAG}_ncu_full.log
+python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_bench_c3.json 2> gpurun_out/${TAG}_bench_c3.err; echo "c3 rc=$?" >> gpurun_out/${TAG}_bench_c3.err
+python tools/ablation.py c1 5 16 > gpurun_out/${TAG}_ablation_c1.jsonl 2>&1; echo "ablation rc=$?" >> gpurun_out/${TAG}_ablation_c1.jsonl
+python bench.py --emulate-ranks 2 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_bench_emu2.json 2> gpurun_out/${TAG}_bench_emu2.err; echo "emu2 rc=$?" >> gpurun_out/${TAG}_bench_emu2.err
