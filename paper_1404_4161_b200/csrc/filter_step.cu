@@ -38,9 +38,15 @@ constexpr Variant kVariants[] = {
     {7, 128, 48, 16, 384, 32, 1.000},  // 12 warps, warp tile 32 x 16 (34.9 TF/s at n=13000, k=624)
     {8, 128, 64, 16, 256, 64, 0.900},  // 8 warps, warp tile 64 x 16 (measured slower; kept for sweeps)
     {9, 256, 32, 16, 256, 64, 0.970},  // 8 warps, warp tile 64 x 16, BM 256 (best at exact 32-column fits)
-    {10, 256, 4, 4, 256, 8, 0.800},    // narrow (HBM-bound) steps: 8 warps, warp tile 32 x 4
-    {11, 128, 8, 4, 256, 8, 0.800},    // narrow: 8 warps (4 x 2), warp tile 32 x 4
-    {12, 128, 12, 4, 384, 8, 0.800},   // narrow: 12 warps (4 x 3), warp tile 32 x 4
+    // narrow (HBM-bound) steps, warp tile 32 or 64 x 4 complex columns (no padding at k_a = 4, 8, 12);
+    // eff from n = 16384, 10 steps (profiles/r01_narrow_variants.log): k_a = 4: v10 6.60 ms (6.5 TB/s);
+    // k_a = 8: v13 6.99 ms, v14 7.80, v12 9.06, v11 9.83; k_a = 12: v14 9.63, v12 9.91
+    {10, 256, 4, 4, 256, 8, 0.800},    // 8 warps (8 x 1), warp tile 32 x 4
+    {11, 128, 8, 4, 256, 8, 0.600},    // 8 warps (4 x 2), warp tile 32 x 4
+    {12, 128, 12, 4, 384, 8, 0.700},   // 12 warps (4 x 3), warp tile 32 x 4
+    {13, 256, 8, 4, 512, 8, 0.850},    // 16 warps (8 x 2), warp tile 32 x 4
+    {14, 256, 12, 4, 384, 16, 0.820},  // 12 warps (4 x 3), warp tile 64 x 4
+    {15, 256, 8, 4, 256, 16, 0.750},   // 8 warps (4 x 2), warp tile 64 x 4
 };
 // 3M variants: accumulators are 3 sets (P1, P2, P3) of (WM/8) x (WNC/8) 8x8 tiles. eff: measured
 // full-width rates relative to 200 (n = 13000, k = 624: 45.5 / 42.0 / 32.4 / 41.8 / 30.2 TF/s
@@ -175,6 +181,12 @@ cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, cons
       return LC(128, 8, 32, 4, 6, kZ4M);
     case 12:
       return LC(128, 12, 32, 4, 6, kZ4M);
+    case 13:
+      return LC(256, 8, 32, 4, 3, kZ4M);
+    case 14:
+      return LC(256, 12, 64, 4, 3, kZ4M);
+    case 15:
+      return LC(256, 8, 64, 4, 3, kZ4M);
     // real symmetric (columns are real columns)
     case 100:
       return LC(128, 96, 32, 32, 3, kReal);

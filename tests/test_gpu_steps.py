@@ -213,6 +213,11 @@ def test_solve_c1_sequence(gpu_lib, ctx):
     nrm = np.abs(np.linalg.eigvalsh(Hl)).max()
     res = np.linalg.norm(Hl @ X - X * lam, axis=0) / nrm
     assert res.max() <= cf["tol"] * 1.01
+    # completeness ("the nev smallest"): Sylvester inertia of H - sigma I in the oracle
+    # (LDL^H), sigma just above the GPU's largest wanted eigenvalue
+    full = np.linalg.eigvalsh(Hl)
+    sigma = lam[-1] + min(1e-6, 0.5 * (full[nev] - full[nev - 1]))
+    assert O.count_below(Hl, sigma) == nev
     loops = [r["loops"] for r in out["reports"]]
     assert all(l <= loops[0] for l in loops[1:])  # reuse of the previous eigenvectors pays
 
