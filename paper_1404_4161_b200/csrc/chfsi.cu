@@ -189,7 +189,8 @@ static TileChoice pick_tile(int elem, bool z3_layout, int64_t nrows, int64_t nco
   }();
   if (ncols < min_cols) return t4;
   TileChoice t3 = choose_filter_tile_z3(nrows, ncols, sms);
-  if (t3.cost <= t4.cost) {
+  static const bool forced3 = getenv("CHFSI_FILTER_VARIANT_Z3") != nullptr;  // test / A-B hook
+  if (forced3 || t3.cost <= t4.cost) {
     *z3k = true;
     return t3;
   }
@@ -208,12 +209,12 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
   CUtensorMap tmA, tmA3;
   chfsi_status st = a_operand(ctx, &Hp, &ldh, n, nloc, elem);
   if (st) return st;
-  st = make_tmap_2d(ctx, &tmA, Hp, elem * n, nloc, elem * ldh, t.bm);
+  st = make_tmap_2d(ctx, &tmA, Hp, elem * n, nloc, elem * ldh, t.bm / t.cluster);
   if (st) return st;
   tmA3 = tmA;
   bool h3_built = false;
   if (z3) {
-    st = a3_operand(ctx, &tmA3, Hp, ldh, n, nloc, t.bm, &h3_built);
+    st = a3_operand(ctx, &tmA3, Hp, ldh, n, nloc, t.bm / t.cluster, &h3_built);
     if (st) return st;
   }
   Operand op;
@@ -407,15 +408,16 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       bool z3k = false;
       TileChoice t = pick_tile(elem, z3 && plane_ok[g], nloc, ka, sms, &z3k);
       if (!z3k) plane_ok[g] = 0;
-      if (t.bm != last_bm) {
-        st = make_tmap_2d(ctx, &tmA, Hp, elem * n, nloc, elem * ldh, t.bm);
+      const int abox = t.bm / t.cluster;  // A box rows (a CTA pair loads half the tile each)
+      if (abox != last_bm) {
+        st = make_tmap_2d(ctx, &tmA, Hp, elem * n, nloc, elem * ldh, abox);
         if (st) return st;
-        last_bm = t.bm;
+        last_bm = abox;
       }
-      if (z3k && t.bm != last_bm3) {
-        st = a3_operand(ctx, &tmA3, Hp, ldh, n, nloc, t.bm, &h3_built);
+      if (z3k && abox != last_bm3) {
+        st = a3_operand(ctx, &tmA3, Hp, ldh, n, nloc, abox, &h3_built);
         if (st) return st;
-        last_bm3 = t.bm;
+        last_bm3 = abox;
       }
       Operand op;
       if (p == 1)

@@ -7,24 +7,41 @@ namespace chfsi {
 
 namespace {
 
-template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M>
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1>
 cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3,
                        const CUtensorMap& tmB3, const StepParams& p, cudaStream_t stream) {
   using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>;
-  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, MODE>;
+  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, MODE, CL>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<p.grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tmA, tmB, tmA3, tmB3, p);
-  return cudaGetLastError();
+  if constexpr (CL == 1) {
+    kern<<<p.grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tmA, tmB, tmA3, tmB3, p);
+    return cudaGetLastError();
+  } else {  // p.grid counts clusters
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(p.grid * CL));
+    cfg.blockDim = dim3(Cfg::kThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmA3, tmB3, p);
+  }
 }
 
 struct Variant {
   int id, bm, bnc, wnc, threads, acc;
-  double eff;  // per-flop efficiency relative to the family's best full-width variant (measured)
+  double eff;       // per-flop efficiency relative to the family's best full-width variant (measured)
+  int cluster = 1;  // 2: CTA pairs multicasting the shared H tile
 };
 // 4M (real embedding) variants; ids are the launch_filter_step cases
 constexpr Variant kVariants[] = {
@@ -54,6 +71,7 @@ constexpr Variant kVariants[] = {
 constexpr Variant kVariantsZ3[] = {
     {200, 128, 48, 16, 384, 48, 1.0}, {201, 128, 32, 16, 256, 48, 0.93}, {202, 128, 16, 8, 256, 24, 0.72},
     {203, 64, 64, 16, 256, 48, 0.925}, {204, 192, 32, 16, 384, 48, 0.67},
+    {210, 128, 48, 16, 384, 48, 0.5, 2},  // z200 as multicast CTA pairs (A/B measurement; not chosen yet)
 };
 // real-symmetric variants
 constexpr Variant kVariantsReal[] = {
@@ -104,7 +122,7 @@ static TileChoice choose(const Variant (&vs)[N], const char* env, int64_t nrows,
   }
   if (best < 0) best = 0;
   const Variant& V = vs[best];
-  return TileChoice{V.id, V.bm, V.bnc, V.threads, V.acc, V.wnc, best_cost};
+  return TileChoice{V.id, V.cluster, V.bm, V.bnc, V.threads, V.acc, V.wnc, best_cost};
 }
 
 }  // namespace
@@ -136,11 +154,15 @@ static int refill_mode() {
 void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
   p.refill_mode = refill_mode();
   const int64_t ncols = p.col_end - p.col0;
-  const int64_t tm = (p.nrows + t.bm - 1) / t.bm, tn = (ncols + t.bnc - 1) / t.bnc;
+  const int64_t cl = t.cluster;
+  const int64_t tm = (p.nrows + t.bm - 1) / t.bm;
+  int64_t tn = (ncols + t.bnc - 1) / t.bnc;
+  tn = (tn + cl - 1) / cl * cl;  // pairs: an even number of N tiles (the balanced split spreads the units)
   p.units_n = (int32_t)((ncols + t.wnc - 1) / t.wnc);
-  const int64_t tiles = tm * tn;
+  const int64_t tiles = tm * (tn / cl);  // schedule tiles (pair tiles when cl = 2)
   const int64_t iters = tiles * p.num_kt;
-  const int64_t grid = iters < num_sms ? iters : num_sms;
+  const int64_t slots = num_sms / cl;    // schedule ids (clusters)
+  const int64_t grid = iters < slots ? iters : slots;
   p.tiles_n = (int32_t)tn;
   p.grid = (int32_t)grid;
   p.dp_units = (int32_t)(tiles / grid);
@@ -205,6 +227,8 @@ cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, cons
       return LC(64, 64, 32, 16, 4, kZ3M);
     case 204:
       return LC(192, 32, 32, 16, 2, kZ3M);
+    case 210:
+      return launch_cfg<128, 48, 32, 16, 3, kZ3M, 2>(tmA, tmB, tmA3, tmB3, p, stream);
     default:
       return cudaErrorInvalidValue;
   }

@@ -76,7 +76,7 @@ constexpr int kBK = kBKHalf * kHalves;  // real K per stage
 //         previous step's epilogue) are extra TMA operands, so the main loop has no FP64 add.
 constexpr int kReal = 0, kZ4M = 1, kZ3M = 2;
 
-template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M>
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1>
 struct FilterCfg {
   static constexpr bool kCplx = MODE != kReal;  // complex output columns
   static constexpr int kWarpsM = BM / WM;
@@ -130,12 +130,18 @@ __device__ __forceinline__ double xor_sign(double x, uint32_t mask) {
   return __hiloint2double(hi, __double2loint(x));
 }
 
-template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M>
+// CL = 2: CTA pairs (thread-block clusters of 2 along N). The pair shares one M tile: each CTA loads
+// half of every A box (rows [rank BM/2, (rank+1) BM/2) of H and of the plane) and multicasts it to both,
+// so the H tile crosses L2 -> SM once per pair and the pair advances in k in lockstep; the persistent /
+// stream-K schedule runs over pair tiles (tiles_n N tiles = tiles_n / 2 pair columns) and cluster ids.
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1>
 __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kThreads, 1)
     filter_step_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB3,
                        const StepParams p) {
   using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>;
+  static_assert(CL == 1 || CL == 2, "cluster of 1 or 2");
+  static_assert(BM % (8 * CL) == 0, "A box split");
   constexpr bool CPLX = MODE == kZ4M;  // the A' [B' B''] embedding
   constexpr int kNP = Cfg::kNP;
   constexpr int kAcc = kNP * Cfg::kMT * Cfg::kNT * 2;  // accumulator doubles per thread
@@ -150,7 +156,18 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t cta = blockIdx.x;
+  const int64_t cta = blockIdx.x / CL;        // schedule id (cluster id when CL = 2)
+  const int crank = (int)(blockIdx.x % CL);    // rank in the cluster (1-D grid, cluster dims (CL,1,1))
+  const int64_t pcta = blockIdx.x;             // physical CTA: owner of partial-accumulator slots
+  // schedule tile (pair tile when CL = 2) -> this CTA's output tile (m-major, tiles_n N tiles)
+  auto cta_tile = [&](int T) -> int {
+    if constexpr (CL == 1) {
+      return T;
+    } else {
+      const int tnp = p.tiles_n / CL;
+      return (T / tnp) * p.tiles_n + (T % tnp) * CL + crank;
+    }
+  };
   const int KT = p.num_kt;
   const int64_t t_beg = sk_start(cta, p.tail_iters, p.grid);
   const int64_t t_end = sk_start(cta + 1, p.tail_iters, p.grid);
@@ -160,12 +177,13 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], Cfg::kConsumerWarps);
+      mbar_init(&empty[s], Cfg::kConsumerWarps * CL);  // CL = 2: both CTAs release a stage
       refill_cnt[s] = 0;
     }
     fence_barrier_init();
   }
   __syncthreads();
+  if constexpr (CL == 2) cluster_sync();  // the peer's barriers exist before any multicast lands
 
   // CTA-local iteration j -> (tile, k-tile)
   auto coords = [&](int64_t j, int& tile, int& kt) {
@@ -204,26 +222,41 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       pc_kt = (int)(t_beg % KT);
     }
   };
-  auto produce = [&]() {  // load iteration pc_j into stage pc_stage, then advance the cursor
-    const int m0 = (pc_tile / p.tiles_n) * BM;
+  // load k-tile kt of schedule tile T into stage st
+  auto load_stage = [&](int T, int kt, int st) {
+    const int tile = cta_tile(T);
+    const int m0 = (tile / p.tiles_n) * BM;
     int nu;
-    const int bcol = p.b_col0 + tile_cols(pc_tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
-    uint8_t* sa = smem + pc_stage * Cfg::kStageBytes;
+    const int bcol = p.b_col0 + tile_cols(tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
+    uint8_t* sa = smem + st * Cfg::kStageBytes;
     uint8_t* sb = sa + Cfg::kABytes;
-    mbar_arrive_expect_tx(&full[pc_stage], Cfg::kTxBytes);
-    const int q = pc_kt / p.kt_per_rank;
-    const int t = pc_kt - q * p.kt_per_rank;
+    mbar_arrive_expect_tx(&full[st], Cfg::kTxBytes);  // CL = 2: includes the peer's multicast half
+    const int q = kt / p.kt_per_rank;
+    const int t = kt - q * p.kt_per_rank;
     const int ka = q * p.a_rank_stride + t * kBK;
     const int kb = t * kBK;
 #pragma unroll
     for (int h = 0; h < kHalves; ++h) {
-      tma_load_2d(sa + h * BM * 128, &tmA, ka + h * kBKHalf, m0, &full[pc_stage]);
-      tma_load_3d(sb + h * Cfg::kBRow, &tmB, kb + h * kBKHalf, bcol, q, &full[pc_stage]);
+      if constexpr (CL == 1) {
+        tma_load_2d(sa + h * BM * 128, &tmA, ka + h * kBKHalf, m0, &full[st]);
+      } else {
+        tma_load_2d_mc(sa + h * BM * 128 + crank * (BM / CL) * 128, &tmA, ka + h * kBKHalf, m0 + crank * (BM / CL),
+                       &full[st], (uint16_t)((1u << CL) - 1));
+      }
+      tma_load_3d(sb + h * Cfg::kBRow, &tmB, kb + h * kBKHalf, bcol, q, &full[st]);
     }
     if constexpr (MODE == kZ3M) {  // the real planes: 16 complex entries = one 128-byte row
-      tma_load_2d(sa + kHalves * BM * 128, &tmA3, ka / 2, m0, &full[pc_stage]);
-      tma_load_3d(sb + kHalves * Cfg::kBRow, &tmB3, kb / 2, bcol, q, &full[pc_stage]);
+      if constexpr (CL == 1) {
+        tma_load_2d(sa + kHalves * BM * 128, &tmA3, ka / 2, m0, &full[st]);
+      } else {
+        tma_load_2d_mc(sa + kHalves * BM * 128 + crank * (BM / CL) * 128, &tmA3, ka / 2, m0 + crank * (BM / CL),
+                       &full[st], (uint16_t)((1u << CL) - 1));
+      }
+      tma_load_3d(sb + kHalves * Cfg::kBRow, &tmB3, kb / 2, bcol, q, &full[st]);
     }
+  };
+  auto produce = [&]() {  // load iteration pc_j into stage pc_stage, then advance the cursor
+    load_stage(pc_tile, pc_kt, pc_stage);
     ++pc_j;
     if (++pc_stage == STAGES) pc_stage = 0;
     if (++pc_kt == KT) {
@@ -241,27 +274,9 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
   };
   // load CTA-local iteration jj into stage st (last-arriver mode: position from the iteration index)
   auto produce_at = [&](int64_t jj, int st) {
-    int tile, kt;
-    coords(jj, tile, kt);
-    const int m0 = (tile / p.tiles_n) * BM;
-    int nu;
-    const int bcol = p.b_col0 + tile_cols(tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
-    uint8_t* sa = smem + st * Cfg::kStageBytes;
-    uint8_t* sb = sa + Cfg::kABytes;
-    mbar_arrive_expect_tx(&full[st], Cfg::kTxBytes);
-    const int q = kt / p.kt_per_rank;
-    const int t = kt - q * p.kt_per_rank;
-    const int ka = q * p.a_rank_stride + t * kBK;
-    const int kb = t * kBK;
-#pragma unroll
-    for (int h = 0; h < kHalves; ++h) {
-      tma_load_2d(sa + h * BM * 128, &tmA, ka + h * kBKHalf, m0, &full[st]);
-      tma_load_3d(sb + h * Cfg::kBRow, &tmB, kb + h * kBKHalf, bcol, q, &full[st]);
-    }
-    if constexpr (MODE == kZ3M) {
-      tma_load_2d(sa + kHalves * BM * 128, &tmA3, ka / 2, m0, &full[st]);
-      tma_load_3d(sb + kHalves * Cfg::kBRow, &tmB3, kb / 2, bcol, q, &full[st]);
-    }
+    int T, kt;
+    coords(jj, T, kt);
+    load_stage(T, kt, st);
   };
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
@@ -418,8 +433,9 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
   int stage = 0;   // j % STAGES
   uint32_t phase = 0;  // (j / STAGES) & 1
   while (j < my_iters) {
-    int tile, kbeg;
-    coords(j, tile, kbeg);
+    int T, kbeg;
+    coords(j, T, kbeg);
+    const int tile = cta_tile(T);  // this CTA's output tile
     // this work unit: k-tiles [kbeg, kend) of `tile`
     int kend = KT;
     if (j >= dp_iters) {
@@ -521,8 +537,15 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
         }
       }
       __syncwarp();
-      if (p.refill_mode == 0) {
-        if (lane == 0) mbar_arrive(&empty[s]);
+      if (CL > 1 || p.refill_mode == 0) {
+        if (lane == 0) {
+          if constexpr (CL == 1) {
+            mbar_arrive(&empty[s]);
+          } else {  // release the stage in both CTAs: either may multicast into it next
+#pragma unroll
+            for (int q = 0; q < CL; ++q) mbar_arrive_cluster(&empty[s], (uint32_t)q);
+          }
+        }
         // refill the stage of iteration j - 1 (stage pc_stage, phase of j - 1) with iteration pc_j
         if (threadIdx.x == 0 && j >= 1 && *(volatile int64_t*)&pc_j < my_iters) {
           const uint32_t prev_phase = (s == 0) ? (phase ^ 1u) : phase;
@@ -549,10 +572,10 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       continue;
     }
     // ---- split tile: publish the partial accumulator; the last contributor finishes the tile ----
-    const int u = tile - p.tail_tile0;
+    const int u = T - p.tail_tile0;  // schedule (pair) tile of the stream-K tail
     const int64_t U0 = (int64_t)u * KT, U1 = U0 + KT;
     const int my_slot = (t_beg / KT == u) ? 0 : 1;
-    double* mine = p.partials + ((cta * 2 + my_slot) * kAcc) * (int64_t)Cfg::kThreads;
+    double* mine = p.partials + ((pcta * 2 + my_slot) * kAcc) * (int64_t)Cfg::kThreads;
 #pragma unroll
     for (int ps = 0; ps < kNP; ++ps)
 #pragma unroll
@@ -568,7 +591,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     int nseg = 0;
     for (int64_t c = c_lo; c <= c_hi; ++c)
       if (sk_start(c + 1, p.tail_iters, p.grid) > sk_start(c, p.tail_iters, p.grid)) ++nseg;
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&p.tickets[u], 1);
+    if (threadIdx.x == 0) s_ticket = atomicAdd(&p.tickets[u * CL + crank], 1);
     __syncthreads();
     if (s_ticket != nseg - 1) continue;  // not the last contributor
     __threadfence();
@@ -577,7 +600,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       const int64_t cs = sk_start(c, p.tail_iters, p.grid);
       if (sk_start(c + 1, p.tail_iters, p.grid) <= cs) continue;
       const int slot = (cs / KT == u) ? 0 : 1;
-      const double* src = p.partials + ((c * 2 + slot) * kAcc) * (int64_t)Cfg::kThreads;
+      const double* src = p.partials + (((c * CL + crank) * 2 + slot) * kAcc) * (int64_t)Cfg::kThreads;
 #pragma unroll
       for (int ps = 0; ps < kNP; ++ps)
 #pragma unroll
@@ -589,9 +612,11 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
               acc_ref(ps, i, jj, e) += __ldcg(src + (((ps * Cfg::kMT + i) * Cfg::kNT + jj) * 2 + e) * Cfg::kThreads + threadIdx.x);
     }
     epilogue(tile);
-    if (threadIdx.x == 0) p.tickets[u] = 0;  // ready for the next launch (stream ordered)
+    if (threadIdx.x == 0) p.tickets[u * CL + crank] = 0;  // ready for the next launch (stream ordered)
   }
   if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
+  // neither CTA of a pair leaves while the other may still multicast into it or arrive on its barriers
+  if constexpr (CL == 2) cluster_sync();
   // peer push: this thread's NVLink stores are ordered before the inter-step barrier's signal
   if (p.n_rdst > 1) __threadfence_system();
 }
@@ -599,6 +624,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
 // host launcher: picks the tile configuration for the step shape; returns cudaError_t
 struct TileChoice {
   int id;
+  int cluster;  // CTAs per thread-block cluster (2: A-multicast pairs)
   int bm, bnc;
   int threads;  // CTA size of the variant
   int acc;      // accumulator doubles per thread (partial-slot size = acc * threads doubles)
