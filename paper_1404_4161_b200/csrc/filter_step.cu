@@ -151,8 +151,18 @@ static int refill_mode() {
   return m;
 }
 
+// L2 prefetch distance of K1 (StepParams::l2_prefetch); CHFSI_K1_L2PF overrides (A/B measurements)
+static int l2_prefetch() {
+  static const int m = [] {
+    const char* e = getenv("CHFSI_K1_L2PF");
+    return e ? atoi(e) : 0;
+  }();
+  return m;
+}
+
 void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
   p.refill_mode = refill_mode();
+  p.l2_prefetch = l2_prefetch();
   const int64_t ncols = p.col_end - p.col0;
   const int64_t cl = t.cluster;
   const int64_t tm = (p.nrows + t.bm - 1) / t.bm;

@@ -59,6 +59,7 @@ struct StepParams {
   int64_t y3_off_r;
   int* nonfinite;       // set to 1 if any written value is not finite (nullable)
   int32_t refill_mode;  // 0: thread 0 refills one stage behind; 1: the last warp to release a stage refills it
+  int32_t l2_prefetch;  // > 0: with each stage load, prefetch into L2 the boxes this many iterations ahead
 };
 
 constexpr int kBKHalf = 16;            // doubles per 128-byte swizzle row
@@ -255,8 +256,31 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       tma_load_3d(sb + kHalves * Cfg::kBRow, &tmB3, kb / 2, bcol, q, &full[st]);
     }
   };
+  // L2 prefetch of the boxes of CTA-local iteration jj (issued p.l2_prefetch iterations ahead of its load)
+  auto prefetch_l2 = [&](int64_t jj) {
+    int T, kt;
+    coords(jj, T, kt);
+    const int tile = cta_tile(T);
+    const int m0 = (tile / p.tiles_n) * BM;
+    int nu;
+    const int bcol = p.b_col0 + tile_cols(tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
+    const int q = kt / p.kt_per_rank;
+    const int t = kt - q * p.kt_per_rank;
+    const int ka = q * p.a_rank_stride + t * kBK;
+    const int kb = t * kBK;
+#pragma unroll
+    for (int h = 0; h < kHalves; ++h) {
+      if (CL == 1 || crank == 0) tma_prefetch_l2_2d(&tmA, ka + h * kBKHalf, m0);
+      tma_prefetch_l2_3d(&tmB, kb + h * kBKHalf, bcol, q);
+    }
+    if constexpr (MODE == kZ3M) {
+      if (CL == 1 || crank == 0) tma_prefetch_l2_2d(&tmA3, ka / 2, m0);
+      tma_prefetch_l2_3d(&tmB3, kb / 2, bcol, q);
+    }
+  };
   auto produce = [&]() {  // load iteration pc_j into stage pc_stage, then advance the cursor
     load_stage(pc_tile, pc_kt, pc_stage);
+    if (p.l2_prefetch > 0 && pc_j + p.l2_prefetch < my_iters) prefetch_l2(pc_j + p.l2_prefetch);
     ++pc_j;
     if (++pc_stage == STAGES) pc_stage = 0;
     if (++pc_kt == KT) {
