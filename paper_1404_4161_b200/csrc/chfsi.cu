@@ -678,8 +678,8 @@ static chfsi_status filter_entry(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t
     set_err(ctx, "chfsi_filter: bad dimensions / leading dimensions / pointers");
     return CHFSI_ERR_ARG;
   }
-  if (ctx->nranks > 1 && (nloc * ctx->nranks != n || row0 != nloc * ctx->rank)) {
-    set_err(ctx, "chfsi_filter: nranks > 1 needs equal row panels (n = nranks * nloc, row0 = rank * nloc)");
+  if (nloc * ctx->nranks != n || row0 != nloc * ctx->rank) {
+    set_err(ctx, "chfsi_filter: row panels must be equal (n = nranks * nloc, row0 = rank * nloc; nranks == 1: nloc = n, row0 = 0)");
     return CHFSI_ERR_ARG;
   }
   if (2 * n > INT32_MAX / 2) {

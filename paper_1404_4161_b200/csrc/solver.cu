@@ -297,7 +297,7 @@ static chfsi_status solve_sequence_t(chfsi_ctx ctx, int64_t n, int64_t row0, int
   if (o.nev < 1 || o.nex < 0 || k > n || !(o.tol > 0) || o.deg0 < 1 || o.deg0 > o.deg_cap ||
       o.deg_cap > CHFSI_MAX_DEGREE || o.max_loops < 1 || o.lanczos_steps < 1 || o.fixed_degree < 0 ||
       o.fixed_degree > CHFSI_MAX_DEGREE ||
-      (ctx->nranks > 1 && (nloc * ctx->nranks != n || row0 != nloc * ctx->rank))) {
+      (nloc * ctx->nranks != n || row0 != nloc * ctx->rank)) {
     set_err(ctx, "chfsi_solve_sequence: bad options (need 0 < nev, nev + nex <= n, tol > 0, 1 <= deg0 <= cap <= 64)");
     return CHFSI_ERR_ARG;
   }

@@ -501,7 +501,7 @@ chfsi_status chfsi_lanczos_bounds(chfsi_ctx ctx, int64_t n, int64_t row0, int64_
   if (!ctx) return CHFSI_ERR_ARG;
   ctx->err.clear();
   if (n < 1 || nloc < 1 || row0 < 0 || row0 + nloc > n || ldh < n || !Hp || steps < 1 || !theta_min || !theta_max ||
-      !upper_bound || (ctx->nranks > 1 && (nloc * ctx->nranks != n || row0 != nloc * ctx->rank))) {
+      !upper_bound || (nloc * ctx->nranks != n || row0 != nloc * ctx->rank)) {
     set_err(ctx, "chfsi_lanczos_bounds: bad arguments");
     return CHFSI_ERR_ARG;
   }
@@ -514,7 +514,7 @@ chfsi_status chfsi_qr(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, void
   if (!ctx) return CHFSI_ERR_ARG;
   ctx->err.clear();
   if (n < 1 || nloc < 1 || row0 < 0 || row0 + nloc > n || ldy < nloc || k < 0 || k > n || nlocked < 0 ||
-      nlocked > k || (k > 0 && !Y) || (ctx->nranks > 1 && (nloc * ctx->nranks != n || row0 != nloc * ctx->rank))) {
+      nlocked > k || (k > 0 && !Y) || (nloc * ctx->nranks != n || row0 != nloc * ctx->rank)) {
     set_err(ctx, "chfsi_qr: bad arguments");
     return CHFSI_ERR_ARG;
   }
@@ -529,7 +529,7 @@ chfsi_status chfsi_rayleigh_ritz(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t
   ctx->err.clear();
   if (n < 1 || nloc < 1 || row0 < 0 || row0 + nloc > n || ldh < n || ldq < nloc || k < 0 || k > n ||
       (k > 0 && (!Hp || !Q || !ritz)) || (resid && !(normH > 0)) ||
-      (ctx->nranks > 1 && (nloc * ctx->nranks != n || row0 != nloc * ctx->rank))) {
+      (nloc * ctx->nranks != n || row0 != nloc * ctx->rank)) {
     set_err(ctx, "chfsi_rayleigh_ritz: bad arguments");
     return CHFSI_ERR_ARG;
   }

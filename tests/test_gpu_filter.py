@@ -180,3 +180,13 @@ def test_filter_3m_matches_4m_and_oracle(gpu_lib, n, k):
     Yo, _ = O.chebyshev_filter(Gm, Y0[:, cols], [deg[j] for j in cols], iv["lambda1"], c, e)
     for mults in (3, 4):
         assert colrel(out[mults][:, cols], Yo).max() <= 1e-11
+
+
+def test_filter_rejects_partial_panel_on_one_rank(gpu_lib, ctx):
+    """nranks == 1 owns every row: a panel with nloc < n or row0 != 0 is CHFSI_ERR_ARG (the B operand of
+    a single rank is its own state, so a partial panel would read rows it does not hold)."""
+    n = 64
+    H = gpu_lib.to_colmajor(np.eye(n))
+    Y = gpu_lib.to_colmajor(np.ones((n // 2, 2)))
+    with pytest.raises(gpu_lib.ChfsiError, match="ERR_ARG"):
+        ctx.filter(H[:, : n // 2], Y, [1, 1], -2.0, 0.0, 1.0, n=n, row0=0)
