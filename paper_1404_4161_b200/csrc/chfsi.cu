@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -390,6 +391,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
   st = ensure_events(ctx, ctx->k1_events, (size_t)2 * (mk + 1) * G, cudaEventDefault);
   if (st) return st;
   int nev_used = 0;
+  std::vector<std::pair<int, int>> launch_log;  // (active columns, variant) per K1 launch
   std::vector<char> plane_ok(G, 1);  // group's B operand carries a current 3M plane
   int64_t s = 0;  // active start s_i = #{j : deg[j] <= i}
   for (int i = 0; i < mk; ++i) {
@@ -478,6 +480,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       if (p > 1) CHFSI_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->grp_ag[g], 0));
       CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used], ctx->stream));
       CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, z3k ? tmA3 : tmA, op.tm3, sp, ctx->stream));
+      launch_log.emplace_back((int)ka, t.id);
       CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used + 1], ctx->stream));
       nev_used += 2;
       ctx->launches++;
@@ -498,11 +501,15 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     CHFSI_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   }
   CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  static const bool k1_log = getenv("CHFSI_K1_LOG") != nullptr;  // per-launch trace (diagnostics)
   for (int q = 0; q < nev_used; q += 2) {
     float ms = 0;
     CHFSI_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->k1_events[q], ctx->k1_events[q + 1]));
     ctx->k1_seconds += ms * 1e-3;
     ctx->k1_launches++;
+    if (k1_log)
+      fprintf(stderr, "k1 rank %d n %lld nloc %lld ka %d variant %d ms %.4f\n", ctx->rank, (long long)n,
+              (long long)nloc, launch_log[q / 2].first, launch_log[q / 2].second, ms);
   }
   if (check_finite) {
     int h = 0;

@@ -10,6 +10,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ctx.cuh"
 #include "small_kernels.cuh"
 #include "supporting.cuh"
@@ -33,6 +35,7 @@ struct PhaseTimer {
   double acc[8] = {0};
   explicit PhaseTimer(cudaStream_t s) : st(s) {}
   ~PhaseTimer() {
+    for (; nvtx_depth > 0; --nvtx_depth) nvtxRangePop();  // ranges left open by an error return
     for (auto e : pool) cudaEventDestroy(e);
   }
   cudaEvent_t ev() {
@@ -43,7 +46,11 @@ struct PhaseTimer {
     }
     return pool[used++];
   }
-  std::pair<cudaEvent_t, cudaEvent_t> begin() {
+  // NVTX range per phase (header-only NVTX3: free unless a profiler is attached)
+  int nvtx_depth = 0;
+  std::pair<cudaEvent_t, cudaEvent_t> begin(const char* name) {
+    nvtxRangePushA(name);
+    ++nvtx_depth;
     cudaEvent_t a = ev(), b = ev();
     cudaEventRecord(a, st);
     return {a, b};
@@ -51,6 +58,8 @@ struct PhaseTimer {
   void end(int phase, std::pair<cudaEvent_t, cudaEvent_t> p) {
     cudaEventRecord(p.second, st);
     pending.push_back({phase, p});
+    nvtxRangePop();
+    --nvtx_depth;
   }
   void flush() {  // call after a stream synchronisation
     for (auto& q : pending) {
@@ -76,7 +85,7 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
   const int64_t nev = o.nev, k = (int64_t)o.nev + o.nex;
   rep = chfsi_report{};
   PhaseTimer tm(ctx->stream);
-  auto t_all = tm.begin();
+  auto t_all = tm.begin("chfsi: eigenproblem");
   const size_t blk = sizeof(double) * 2 * (size_t)nloc * k;
   TRY(ensure(ctx, ctx->ya, blk));
   TRY(ensure(ctx, ctx->xl, blk));
@@ -112,7 +121,7 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
 
   // Alg 1 l3: Lanczos upper bound beta (R17) and ||H||_est (R8)
   double tmin, tmax, beta;
-  auto t0 = tm.begin();
+  auto t0 = tm.begin("chfsi: lanczos");
   TRY(lanczos_t<Scal>(ctx, n, row0, nloc, Hp, ldh, o.lanczos_steps, seed, &tmin, &tmax, &beta));
   tm.end(T_LANCZOS, t0);
   const double normH = std::max(std::fabs(tmin), std::fabs(tmax));
@@ -127,11 +136,11 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
   double lam1, alpha;
   if (!have_prev) {  // R11: start block -> QR -> RR seeds (lambda_1, alpha)
     int32_t fb = 0;
-    auto t1 = tm.begin();
+    auto t1 = tm.begin("chfsi: qr (start)");
     TRY(qr_t<Scal>(ctx, n, nloc, nullptr, nloc, 0, Ya, nloc, k, &fb));
     tm.end(T_QR, t1);
     rep.qr_fallbacks += fb;
-    auto t2 = tm.begin();
+    auto t2 = tm.begin("chfsi: rayleigh-ritz (start)");
     TRY(rr_t<Scal>(ctx, n, row0, nloc, Hp, ldh, Ya, nloc, k, normH, mu.data(), nullptr));
     tm.end(T_RR, t2);
     rep.matvecs_total += k;
@@ -154,7 +163,7 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
     for (int64_t j = 0; j < ka; ++j) ms[j] = m[perm[j]];
     TRY(gather(Ya, perm, T, nloc));
     // Alg 1 l5: the Chebyshev filter (Alg 2)
-    auto t3 = tm.begin();
+    auto t3 = tm.begin("chfsi: filter");
     const double k1s = ctx->k1_seconds;
     const int64_t k1n = ctx->k1_launches;
     TRY(filter_impl(ctx, n, row0, nloc, Hp, ldh, T, nloc, ka, ms.data(), lam1, c, e, true, elem));
@@ -168,18 +177,18 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
     rep.filter_flops += (elem == 2 ? 8.0 : 2.0) * (double)n * (double)n * (double)mv;
     // Alg 1 l6: orthonormalise [locked | filtered] (R14, R15)
     int32_t fb = 0;
-    auto t4 = tm.begin();
+    auto t4 = tm.begin("chfsi: qr");
     TRY(qr_t<Scal>(ctx, n, nloc, XL, nloc, nl, T, nloc, ka, &fb));
     tm.end(T_QR, t4);
     rep.qr_fallbacks += fb;
     // Alg 1 l7-9 (+ residuals, R8): Rayleigh-Ritz on the active block (R16)
-    auto t5 = tm.begin();
+    auto t5 = tm.begin("chfsi: rayleigh-ritz");
     TRY(rr_t<Scal>(ctx, n, row0, nloc, Hp, ldh, T, nloc, ka, normH, mu.data(), res.data()));
     tm.end(T_RR, t5);
     rep.matvecs_total += ka;
     rep.loops++;
     // Alg 1 l10 (R7): lock wanted Ritz positions with r <= tol, leftmost in locking order
-    auto t6 = tm.begin();
+    auto t6 = tm.begin("chfsi: lock + degrees");
     const int64_t want = nev - nl;
     std::vector<int> lock_cols, keep_cols;
     std::vector<double> mu2, res2;

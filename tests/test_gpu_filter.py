@@ -121,10 +121,14 @@ def test_filter_ld_and_panel_views(gpu_lib, ctx):
     Hbig = gpu_lib.colmajor(n + 6, n + 3)
     Hbig[:n, :n].copy_(torch.as_tensor(H))
     Ybig = gpu_lib.colmajor(n + 10, k)
+    Ybig.fill_(complex(1234.5, -6789.25))  # guard band: rows n..n+9 of every column must stay untouched
     Ybig[:n].copy_(torch.as_tensor(Y0))
+    Hguard = Hbig.clone()
     ctx.filter(Hbig[:n, :n], Ybig[:n], deg, l1, c, e)
     Yo, _ = O.chebyshev_filter(H, Y0, deg, l1, c, e)
     assert colrel(Ybig[:n].cpu().numpy(), Yo).max() <= 1e-11
+    assert bool((Ybig[n:] == complex(1234.5, -6789.25)).all())  # no write outside the caller's view
+    assert torch.equal(Hbig, Hguard)  # H is read-only
 
 
 def test_filter_errors(gpu_lib, ctx):
@@ -190,3 +194,20 @@ def test_filter_rejects_partial_panel_on_one_rank(gpu_lib, ctx):
     Y = gpu_lib.to_colmajor(np.ones((n // 2, 2)))
     with pytest.raises(gpu_lib.ChfsiError, match="ERR_ARG"):
         ctx.filter(H[:, : n // 2], Y, [1, 1], -2.0, 0.0, 1.0, n=n, row0=0)
+
+
+@pytest.mark.parametrize("deg_kind", ["all_one", "all_max", "one_and_max"])
+def test_filter_degree_extremes(gpu_lib, ctx, deg_kind):
+    """Degree edge cases of Alg 2: every column finishing at step 1 (only the a3 step, no recurrence),
+    every column at CHFSI_MAX_DEGREE = 64, and both in one block (a 1-step column next to 63 more steps of
+    a 64-step one) -- against the closed form on a diagonal H (App. A, <= 1e-13)."""
+    rng = np.random.default_rng(11)
+    n, k = 173, 11
+    d = np.sort(rng.uniform(-2.0, 40.0, n))
+    deg = {"all_one": [1] * k, "all_max": [64] * k, "one_and_max": [1] * 5 + [64] * 6}[deg_kind]
+    Y0 = crand(rng, n, k)
+    l1, a, b = -2.3, -1.2, 40.5
+    c, e = (a + b) / 2, (b - a) / 2
+    Y = run_filter(gpu_lib, ctx, np.diag(d.astype(complex)), Y0, deg, l1, c, e)
+    Yc = O.filter_diag_closed(d, Y0, deg, l1, c, e)
+    assert colrel(Y, Yc).max() <= 1e-13
