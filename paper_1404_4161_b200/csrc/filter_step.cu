@@ -73,9 +73,12 @@ constexpr Variant kVariantsZ3[] = {
     {203, 64, 64, 16, 256, 48, 0.925}, {204, 192, 32, 16, 384, 48, 0.67},
     {210, 128, 48, 16, 384, 48, 0.5, 2},  // z200 as multicast CTA pairs (A/B measurement; not chosen yet)
 };
-// real-symmetric variants
+// real-symmetric variants (columns are real columns; kNT = WNC / 8). eff relative to 103 (n = 13000,
+// k = 624: 33.6 / 32.1 / 31.7 / 29.2 / 32.9 / 32.6 TF/s for 103 / 100 / 101 / 102 / 104 / 105;
+// profiles/r01_real_variants.log)
 constexpr Variant kVariantsReal[] = {
-    {100, 128, 96, 32, 384, 32, 1.0}, {101, 128, 64, 32, 256, 32, 0.97}, {102, 128, 32, 16, 256, 16, 0.93},
+    {100, 128, 96, 32, 384, 32, 0.955}, {101, 128, 64, 32, 256, 32, 0.94}, {102, 128, 32, 16, 256, 16, 0.87},
+    {103, 192, 64, 32, 384, 32, 1.0},   {104, 128, 64, 16, 512, 16, 0.98}, {105, 128, 48, 16, 384, 16, 0.97},
 };
 
 // Model time of one step of `ncols` active columns over `nrows` rows for variant V, in units of a
@@ -226,6 +229,12 @@ cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, cons
       return LC(128, 64, 32, 32, 4, kReal);
     case 102:
       return LC(128, 32, 32, 16, 5, kReal);
+    case 103:
+      return LC(192, 64, 32, 32, 3, kReal);
+    case 104:
+      return LC(128, 64, 32, 16, 4, kReal);
+    case 105:
+      return LC(128, 48, 32, 16, 5, kReal);
     // complex 3M (columns are complex columns)
     case 200:
       return LC(128, 48, 32, 16, 3, kZ3M);
