@@ -7,11 +7,11 @@ namespace chfsi {
 
 namespace {
 
-template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1>
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int OCC = 1>
 cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3,
                        const CUtensorMap& tmB3, const StepParams& p, cudaStream_t stream) {
   using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>;
-  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, MODE, CL>;
+  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, MODE, CL, OCC>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
@@ -42,6 +42,7 @@ struct Variant {
   int id, bm, bnc, wnc, threads, acc;
   double eff;       // per-flop efficiency relative to the family's best full-width variant (measured)
   int cluster = 1;  // 2: CTA pairs multicasting the shared H tile
+  int occ = 1;      // CTAs per SM
 };
 // 4M (real embedding) variants; ids are the launch_filter_step cases
 constexpr Variant kVariants[] = {
@@ -72,6 +73,7 @@ constexpr Variant kVariantsZ3[] = {
     {200, 128, 48, 16, 384, 48, 1.0}, {201, 128, 32, 16, 256, 48, 0.93}, {202, 128, 16, 8, 256, 24, 0.72},
     {203, 64, 64, 16, 256, 48, 0.925}, {204, 192, 32, 16, 384, 48, 0.67},
     {210, 128, 48, 16, 384, 48, 0.5, 2},  // z200 as multicast CTA pairs (A/B measurement; not chosen yet)
+    {206, 64, 48, 16, 192, 48, 0.5, 1, 2},  // 6 warps, 2 stages, 2 CTAs per SM (A/B measurement)
 };
 // real-symmetric variants (columns are real columns; kNT = WNC / 8). eff relative to 103 (n = 13000,
 // k = 624: 33.6 / 32.1 / 31.7 / 29.2 / 32.9 / 32.6 TF/s for 103 / 100 / 101 / 102 / 104 / 105;
@@ -125,7 +127,7 @@ static TileChoice choose(const Variant (&vs)[N], const char* env, int64_t nrows,
   }
   if (best < 0) best = 0;
   const Variant& V = vs[best];
-  return TileChoice{V.id, V.cluster, V.bm, V.bnc, V.threads, V.acc, V.wnc, best_cost};
+  return TileChoice{V.id, V.cluster, V.occ, V.bm, V.bnc, V.threads, V.acc, V.wnc, best_cost};
 }
 
 }  // namespace
@@ -174,7 +176,7 @@ void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
   p.units_n = (int32_t)((ncols + t.wnc - 1) / t.wnc);
   const int64_t tiles = tm * (tn / cl);  // schedule tiles (pair tiles when cl = 2)
   const int64_t iters = tiles * p.num_kt;
-  const int64_t slots = num_sms / cl;    // schedule ids (clusters)
+  const int64_t slots = (int64_t)num_sms * t.occ / cl;  // schedule ids (clusters)
   const int64_t grid = iters < slots ? iters : slots;
   p.tiles_n = (int32_t)tn;
   p.grid = (int32_t)grid;
@@ -183,7 +185,9 @@ void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
   p.tail_iters = (tiles - p.tail_tile0) * p.num_kt;
 }
 
-size_t filter_partials_doubles(const TileChoice& t, int num_sms) { return (size_t)2 * num_sms * t.acc * t.threads; }
+size_t filter_partials_doubles(const TileChoice& t, int num_sms) {
+  return (size_t)2 * num_sms * t.occ * t.acc * t.threads;
+}
 
 cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, const CUtensorMap& tmB,
                                const CUtensorMap& tmA3, const CUtensorMap& tmB3, const StepParams& p,
@@ -248,6 +252,8 @@ cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, cons
       return LC(192, 32, 32, 16, 2, kZ3M);
     case 210:
       return launch_cfg<128, 48, 32, 16, 3, kZ3M, 2>(tmA, tmB, tmA3, tmB3, p, stream);
+    case 206:
+      return launch_cfg<64, 48, 32, 16, 2, kZ3M, 1, 2>(tmA, tmB, tmA3, tmB3, p, stream);
     default:
       return cudaErrorInvalidValue;
   }

@@ -135,8 +135,10 @@ __device__ __forceinline__ double xor_sign(double x, uint32_t mask) {
 // half of every A box (rows [rank BM/2, (rank+1) BM/2) of H and of the plane) and multicasts it to both,
 // so the H tile crosses L2 -> SM once per pair and the pair advances in k in lockstep; the persistent /
 // stream-K schedule runs over pair tiles (tiles_n N tiles = tiles_n / 2 pair columns) and cluster ids.
-template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1>
-__global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kThreads, 1)
+// OCC: CTAs resident per SM (the persistent grid is OCC x SM count; 2 lets one CTA's MMAs cover the
+// other's TMA waits)
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int OCC = 1>
+__global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kThreads, OCC)
     filter_step_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB3,
                        const StepParams p) {
@@ -649,6 +651,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
 struct TileChoice {
   int id;
   int cluster;  // CTAs per thread-block cluster (2: A-multicast pairs)
+  int occ;      // CTAs resident per SM (persistent grid = occ x SMs)
   int bm, bnc;
   int threads;  // CTA size of the variant
   int acc;      // accumulator doubles per thread (partial-slot size = acc * threads doubles)
