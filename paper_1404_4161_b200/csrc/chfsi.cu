@@ -190,7 +190,7 @@ static TileChoice pick_tile(int elem, bool z3_layout, int64_t nrows, int64_t nco
   }();
   if (ncols < min_cols) return t4;
   TileChoice t3 = choose_filter_tile_z3(nrows, ncols, sms);
-  static const bool forced3 = getenv("CHFSI_FILTER_VARIANT_Z3") != nullptr;  // test / A-B hook
+  const bool forced3 = getenv("CHFSI_FILTER_VARIANT_Z3") != nullptr;  // test / A-B hook (read per call)
   if (forced3 || t3.cost <= t4.cost) {
     *z3k = true;
     return t3;

@@ -1,4 +1,5 @@
 // filter_step.cu -- instantiations and launcher of K1 (see filter_step.cuh).
+#include <atomic>
 #include <cstdlib>
 
 #include "filter_step.cuh"
@@ -12,11 +13,16 @@ cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUt
                        const CUtensorMap& tmB3, const StepParams& p, cudaStream_t stream) {
   using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>;
   auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, MODE, CL, OCC>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  // the opt-in shared-memory size is a per-device function attribute: set it once per device (contexts
+  // on several host threads may launch the same instantiation concurrently)
+  static std::atomic<uint64_t> attr_devices{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_devices.load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_devices.fetch_or(bit, std::memory_order_release);
   }
   if constexpr (CL == 1) {
     kern<<<p.grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tmA, tmB, tmA3, tmB3, p);
