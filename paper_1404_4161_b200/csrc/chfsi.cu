@@ -304,9 +304,11 @@ static chfsi_status ensure_comm_stream(chfsi_ctx ctx, size_t groups) {
 }
 
 // Alg 2 on this rank's rows. One K1 launch per (step, column group). At p > 1 the packed
-// B operand of group g lives at R + elem*ldp*p*gb[g] with layout [rank][ka_g][ldp]; the epilogue of
-// step i writes this rank's chunk of step i+1's operand, and an in-place allgather on the comm stream
-// completes it while K1 runs on the next group ("Overlap").
+// B operand of group g lives at R + cw*ldp*p*gb[g] with layout [rank][ka_g][cw*ldp] (cw = 3 in the 3M
+// column layout); the epilogue of step i writes this rank's chunk of step i+1's operand, and an in-place
+// allgather on the comm stream completes it while K1 runs on the next group ("Overlap") --
+// or, with the peer exchange, the epilogue writes the chunk into every rank's buffer and a barrier
+// separates the steps (one group).
 chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,
                          void* Y, int64_t ldy, int64_t k, const int32_t* deg, double lambda1, double c, double e,
                          bool check_finite, int elem) {
