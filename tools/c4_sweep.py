@@ -25,6 +25,19 @@ HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if o
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 
 
+def roofline_time_ms(n, deg):
+    """T* = sum over steps of max(tensor time, H-stream time) for the arithmetic the
+    library picks per step: 3M (6 n^2 k_a tensor flops, 24 B of H per entry) at >= 28 active columns,
+    4M (8 n^2 k_a, 16 B) below; peaks: the measured FP64 DMMA rate and HBM copy bandwidth."""
+    deg = sorted(deg)
+    t = 0.0
+    for i in range(max(deg)):
+        ka = sum(1 for m in deg if m > i)
+        fl, by = (6.0 * n * n * ka, 24.0 * n * n) if ka >= 28 else (8.0 * n * n * ka, 16.0 * n * n)
+        t += max(fl / (PEAK * 1e12), by / (HBM * 1e9))
+    return 1e3 * t
+
+
 def timed(ctx, H, Y0, deg, l1, c, e, reps=2):
     Y = chfsi.colmajor(*Y0.shape)
     best = 1e30
@@ -88,7 +101,9 @@ def main():
                 tfac = 1.0 if k < 28 else 0.75
                 row = {"n": n, "k": k, "degrees": label, "ms": ms, "tflops": flops / ms / 1e9,
                        "tensor_tflops": tfac * flops / ms / 1e9,
-                       "frac_of_fp64_peak": tfac * flops / ms / 1e9 / PEAK, "gen_s": gen_s}
+                       "frac_of_fp64_peak": tfac * flops / ms / 1e9 / PEAK,
+                       "roofline_ms": roofline_time_ms(n, deg), "frac_of_roofline": roofline_time_ms(n, deg) / ms,
+                       "gen_s": gen_s}
                 if k <= 12:  # HBM-bound: H streamed once per step
                     steps = max(deg)
                     row["hbm_gbs_H_stream"] = 16.0 * n * n * steps / ms / 1e6
