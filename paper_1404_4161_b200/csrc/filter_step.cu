@@ -57,7 +57,7 @@ constexpr Variant kVariants[] = {
     {2, 128, 64, 32, 256, 64, 0.940},  // 8 warps, warp tile 32 x 32
     {3, 64, 32, 16, 128, 32, 0.700},   // 4 warps
     {4, 128, 64, 16, 512, 32, 0.950},  // 16 warps (4 per SMSP), warp tile 32 x 16
-    {5, 128, 16, 16, 256, 16, 0.800},  // 8 warps, warp tile 16 x 16 (narrow blocks)
+    {5, 128, 16, 16, 256, 16, 0.900},  // 8 warps, warp tile 16 x 16 (narrow blocks; best at k_a = 16)
     {6, 128, 32, 8, 512, 16, 0.960},   // 16 warps, warp tile 32 x 8
     {7, 128, 48, 16, 384, 32, 1.000},  // 12 warps, warp tile 32 x 16 (34.9 TF/s at n=13000, k=624)
     {8, 128, 64, 16, 256, 64, 0.900},  // 8 warps, warp tile 64 x 16 (measured slower; kept for sweeps)
@@ -80,6 +80,8 @@ constexpr Variant kVariantsZ3[] = {
     {203, 64, 64, 16, 256, 48, 0.925}, {204, 192, 32, 16, 384, 48, 0.67},
     {210, 128, 48, 16, 384, 48, 0.5, 2},  // z200 as multicast CTA pairs (A/B measurement; not chosen yet)
     {206, 64, 48, 16, 192, 48, 0.5, 1, 2},  // 6 warps, 2 stages, 2 CTAs per SM (A/B measurement)
+    {207, 64, 64, 16, 512, 24, 0.963},      // 16 warps, warp tile 16 x 16, 4 stages (k_a = 64, 128, 256)
+    {208, 128, 32, 8, 512, 24, 0.94},       // 16 warps, warp tile 32 x 8, 3 stages (k_a = 32, 160)
 };
 // real-symmetric variants (columns are real columns; kNT = WNC / 8). eff relative to 103 (n = 13000,
 // k = 624: 33.6 / 32.1 / 31.7 / 29.2 / 32.9 / 32.6 TF/s for 103 / 100 / 101 / 102 / 104 / 105;
@@ -91,24 +93,29 @@ constexpr Variant kVariantsReal[] = {
 
 // Model time of one step of `ncols` active columns over `nrows` rows for variant V, in units of a
 // full-efficiency 4M column-row (8 n flops at 34.9 TF/s):
-//  compute: the balanced N split gives every N tile `per` warp-column units; active warps compute
-//           whole units (padding inside a unit is real work), idle warps skip their MMAs but are not
-//           free (30 %), fewer than two active warps per SM sub-partition lose latency hiding;
+//  compute: the balanced N split gives the N tiles `per` or `per - 1` warp-column units; the persistent
+//           schedule hands out whole tiles (stream-K splits by k-iterations, not by work), so every
+//           tile is charged as the widest one (tn x per units) -- uneven splits cost their imbalance;
+//           active warps in a tile cover latency as g(warps): >= 12 -> 1, 8..11 -> 0.85, 4..7 -> 0.6,
+//           relative to the variant's own warp count (its measured eff already includes that);
 //           `speed` = the family's best full-width rate relative to 4M (3M: 45.5 / 34.9)
 //  memory:  H streamed once per step per N tile column (re-reads mostly from L2: +25 % per extra N
 //           tile), `hbm_cols` = the column count at which the family's compute time equals its H
 //           stream at ~5.9 TB/s (4M: 16 B / entry -> 11.8; 3M: 24 B / entry -> 17.7)
+// Calibrated on profiles/r01_mid_width_variants.log and r01_narrow_variants.log.
+static double warp_cover(int warps) { return warps >= 12 ? 1.0 : warps >= 8 ? 0.85 : warps >= 4 ? 0.6 : 0.4; }
+
 static double step_cost(const Variant& V, int64_t nrows, int64_t ncols, double speed, double hbm_cols) {
   const int64_t tm = (nrows + V.bm - 1) / V.bm;
   const int64_t units = (ncols + V.wnc - 1) / V.wnc;
   const int64_t tn = (ncols + V.bnc - 1) / V.bnc;
   const int64_t per = (units + tn - 1) / tn;
-  const int warps_m = V.threads / 32 / (V.bnc / V.wnc);
-  const double active_warps = (double)per * warps_m;
-  const double occ = active_warps >= 8 ? 1.0 : 0.6 + 0.05 * active_warps;
-  const double cols = 0.3 * (double)(tn * per * V.wnc) + 0.7 * (double)(units * V.wnc);
+  const int warps = V.threads / 32;
+  const int warps_m = warps / (V.bnc / V.wnc);
+  const double cover = warp_cover((int)per * warps_m) / warp_cover(warps);
+  const double cols = (double)(tn * per * V.wnc);
   const double rows = (double)tm * V.bm;
-  const double compute = rows * cols / (V.eff * occ * speed);
+  const double compute = rows * cols / (V.eff * cover * speed);
   const double memory = rows * hbm_cols * (1.0 + 0.25 * (double)(tn - 1));
   // + 10 % of the compute term: between variants that all hit the HBM floor, the one with less
   // padded tensor work keeps more slack (and wins)
@@ -258,6 +265,10 @@ cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, cons
       return LC(192, 32, 32, 16, 2, kZ3M);
     case 210:
       return launch_cfg<128, 48, 32, 16, 3, kZ3M, 2>(tmA, tmB, tmA3, tmB3, p, stream);
+    case 207:
+      return LC(64, 64, 16, 16, 4, kZ3M);
+    case 208:
+      return LC(128, 32, 32, 8, 3, kZ3M);
     case 206:
       return launch_cfg<64, 48, 32, 16, 2, kZ3M, 1, 2>(tmA, tmB, tmA3, tmB3, p, stream);
     default:
