@@ -51,7 +51,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 chfsi_status make_tmap_2d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64_t kreal, int64_t rows,
-                          int64_t ld_doubles, int box_rows) {
+                          int64_t ld_doubles, int box_rows, int box_inner) {
   auto enc = get_encode();
   if (!enc) {
     set_err(ctx, "cuTensorMapEncodeTiled unavailable");
@@ -59,10 +59,11 @@ chfsi_status make_tmap_2d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64
   }
   cuuint64_t dims[2] = {(cuuint64_t)kreal, (cuuint64_t)std::max<int64_t>(rows, 1)};
   cuuint64_t strides[1] = {(cuuint64_t)(ld_doubles * 8)};
-  cuuint32_t box[2] = {(cuuint32_t)kBKHalf, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle sw = box_inner * 8 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_err(ctx, "cuTensorMapEncodeTiled(2d) failed: " + std::to_string((int)r));
@@ -72,7 +73,7 @@ chfsi_status make_tmap_2d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64
 }
 
 chfsi_status make_tmap_3d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64_t kreal, int64_t cols,
-                          int64_t chunks, int64_t ld_doubles, int64_t chunk_doubles, int box_cols) {
+                          int64_t chunks, int64_t ld_doubles, int64_t chunk_doubles, int box_cols, int box_inner) {
   auto enc = get_encode();
   if (!enc) {
     set_err(ctx, "cuTensorMapEncodeTiled unavailable");
@@ -81,10 +82,11 @@ chfsi_status make_tmap_3d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64
   cuuint64_t dims[3] = {(cuuint64_t)kreal, (cuuint64_t)std::max<int64_t>(cols, 1),
                         (cuuint64_t)std::max<int64_t>(chunks, 1)};
   cuuint64_t strides[2] = {(cuuint64_t)(ld_doubles * 8), (cuuint64_t)(std::max<int64_t>(chunk_doubles, ld_doubles) * 8)};
-  cuuint32_t box[3] = {(cuuint32_t)kBKHalf, (cuuint32_t)box_cols, 1};
+  cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_cols, 1};
   cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapSwizzle sw = box_inner * 8 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_err(ctx, "cuTensorMapEncodeTiled(3d) failed: " + std::to_string((int)r));
@@ -122,7 +124,8 @@ struct Operand {
 //  p == 1: buf = local state (rows = n), column coordinate = absolute column.
 //  p > 1 : buf = packed [rank][kcols - col0][cs] operand (rows = nloc), coordinate = column - col0.
 static chfsi_status b_operand(chfsi_ctx ctx, Operand* op, const double* buf, int64_t rows, int64_t ld,
-                              int64_t kcols, int64_t col0, int nranks, int box_cols, int elem, int cw, bool z3) {
+                              int64_t kcols, int64_t col0, int nranks, int box_cols, int elem, int cw, bool z3,
+                              int kh = 2) {
   const int64_t cs = cw * ld;
   const int64_t cols = nranks == 1 ? kcols : kcols - col0;
   op->b_col0 = nranks == 1 ? (int32_t)col0 : 0;
@@ -131,7 +134,7 @@ static chfsi_status b_operand(chfsi_ctx ctx, Operand* op, const double* buf, int
     op->tm3 = op->tm;  // unused outside 3M
     return st;
   }
-  return make_tmap_3d(ctx, &op->tm3, buf + 2 * ld, rows, cols, nranks, cs, cs * cols, box_cols);
+  return make_tmap_3d(ctx, &op->tm3, buf + 2 * ld, rows, cols, nranks, cs, cs * cols, box_cols, 8 * kh);
 }
 
 // The A operand (H panel) through TMA needs a 16-byte row stride: real data with an odd ldh is first
@@ -162,7 +165,7 @@ chfsi_status h3_prepare(chfsi_ctx ctx, const void* Hp, int64_t ldh, int64_t n, i
 }
 
 static chfsi_status a3_operand(chfsi_ctx ctx, CUtensorMap* m, const void* Hp, int64_t ldh, int64_t n, int64_t nloc,
-                               int box_rows, bool* built) {
+                               int box_rows, bool* built, int kh = 2) {
   if (!*built) {
     if (ctx->h3_pin != Hp) {
       chfsi_status st = h3_prepare(ctx, Hp, ldh, n, nloc);
@@ -170,7 +173,7 @@ static chfsi_status a3_operand(chfsi_ctx ctx, CUtensorMap* m, const void* Hp, in
     }
     *built = true;
   }
-  return make_tmap_2d(ctx, m, ctx->h3.ptr, n, nloc, ctx->h3_ld, box_rows);
+  return make_tmap_2d(ctx, m, ctx->h3.ptr, n, nloc, ctx->h3_ld, box_rows, 8 * kh);
 }
 
 // Tile variant and arithmetic of one launch. With the 3M column layout available (z3_layout) the
@@ -215,7 +218,7 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
   tmA3 = tmA;
   bool h3_built = false;
   if (z3) {
-    st = a3_operand(ctx, &tmA3, Hp, ldh, n, nloc, t.bm / t.cluster, &h3_built);
+    st = a3_operand(ctx, &tmA3, Hp, ldh, n, nloc, t.bm / t.cluster, &h3_built, t.kh);
     if (st) return st;
   }
   Operand op;
@@ -250,12 +253,13 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
     bsrc = static_cast<const double*>(ctx->L0.ptr);
     bld = ldl;
   }
-  st = b_operand(ctx, &op, bsrc, p == 1 ? n : nloc, bld, k, 0, p, t.bnc, elem, cw, z3);
+  st = b_operand(ctx, &op, bsrc, p == 1 ? n : nloc, bld, k, 0, p, t.bnc, elem, cw, z3, t.kh);
   if (st) return st;
   StepParams sp{};
   sp.nrows = nloc;
   const int64_t kr = p == 1 ? elem * n : elem * nloc;
-  sp.kt_per_rank = (int32_t)((kr + kBK - 1) / kBK);
+  const int64_t kbk = 16 * t.kh;  // real K per stage of the variant
+  sp.kt_per_rank = (int32_t)((kr + kbk - 1) / kbk);
   sp.num_kt = sp.kt_per_rank * p;
   sp.a_rank_stride = (int32_t)(elem * nloc);
   sp.col0 = 0;
@@ -418,21 +422,22 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
         if (st) return st;
         last_bm = abox;
       }
-      if (z3k && abox != last_bm3) {
-        st = a3_operand(ctx, &tmA3, Hp, ldh, n, nloc, abox, &h3_built);
+      if (z3k && abox * 4 + t.kh != last_bm3) {  // the plane box depends on the rows and the stage depth
+        st = a3_operand(ctx, &tmA3, Hp, ldh, n, nloc, abox, &h3_built, t.kh);
         if (st) return st;
-        last_bm3 = abox;
+        last_bm3 = abox * 4 + t.kh;
       }
       Operand op;
       if (p == 1)
-        st = b_operand(ctx, &op, reinterpret_cast<const double*>(L[cur]), n, ldl, k, c0, 1, t.bnc, elem, cw, z3k);
+        st = b_operand(ctx, &op, reinterpret_cast<const double*>(L[cur]), n, ldl, k, c0, 1, t.bnc, elem, cw, z3k, t.kh);
       else
-        st = b_operand(ctx, &op, region(cur, g), nloc, ldp, ce, c0, p, t.bnc, elem, cw, z3k);
+        st = b_operand(ctx, &op, region(cur, g), nloc, ldp, ce, c0, p, t.bnc, elem, cw, z3k, t.kh);
       if (st) return st;
       StepParams sp{};
       sp.nrows = nloc;
       const int64_t kr = p == 1 ? elem * n : elem * nloc;
-      sp.kt_per_rank = (int32_t)((kr + kBK - 1) / kBK);
+      const int64_t kbk = 16 * t.kh;  // real K per stage of the variant
+      sp.kt_per_rank = (int32_t)((kr + kbk - 1) / kbk);
       sp.num_kt = sp.kt_per_rank * p;
       sp.a_rank_stride = (int32_t)(elem * nloc);
       sp.col0 = (int32_t)c0;

@@ -120,10 +120,11 @@ void set_err(chfsi_ctx ctx, const std::string& msg);
 // TMA descriptors (FLOAT64, 128B swizzle, OOB -> zero fill)
 //  A: real K-major matrix of `rows` rows with `kreal` doubles each, row stride ld_doubles; box (16, box_rows)
 //  B: 3-D (kreal, cols, chunks) with column stride ld_doubles and chunk stride chunk_doubles
+//  box_inner = 16 doubles (one 128-byte swizzle row) unless given; 8 doubles selects the 64B swizzle
 chfsi_status make_tmap_2d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64_t kreal, int64_t rows,
-                          int64_t ld_doubles, int box_rows);
+                          int64_t ld_doubles, int box_rows, int box_inner = 16);
 chfsi_status make_tmap_3d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64_t kreal, int64_t cols,
-                          int64_t chunks, int64_t ld_doubles, int64_t chunk_doubles, int box_cols);
+                          int64_t chunks, int64_t ld_doubles, int64_t chunk_doubles, int box_cols, int box_inner = 16);
 
 // Communication (comm.cu). With nranks == 1 every collective is a no-op / local copy.
 chfsi_status comm_init(chfsi_ctx ctx);

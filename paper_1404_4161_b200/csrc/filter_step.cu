@@ -8,11 +8,11 @@ namespace chfsi {
 
 namespace {
 
-template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int OCC = 1>
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int OCC = 1, int KH = 2>
 cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3,
                        const CUtensorMap& tmB3, const StepParams& p, cudaStream_t stream) {
-  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>;
-  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, MODE, CL, OCC>;
+  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE, CL, KH>;
+  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, MODE, CL, OCC, KH>;
   // the opt-in shared-memory size is a per-device function attribute: set it once per device (contexts
   // on several host threads may launch the same instantiation concurrently)
   static std::atomic<uint64_t> attr_devices{0};
@@ -49,6 +49,7 @@ struct Variant {
   double eff;       // per-flop efficiency relative to the family's best full-width variant (measured)
   int cluster = 1;  // 2: CTA pairs multicasting the shared H tile
   int occ = 1;      // CTAs per SM
+  int kh = 2;       // 128-byte swizzle rows per stage (1: half stages)
 };
 // 4M (real embedding) variants; ids are the launch_filter_step cases
 constexpr Variant kVariants[] = {
@@ -82,6 +83,9 @@ constexpr Variant kVariantsZ3[] = {
     {206, 64, 48, 16, 192, 48, 0.5, 1, 2},  // 6 warps, 2 stages, 2 CTAs per SM (A/B measurement)
     {207, 64, 64, 16, 512, 24, 0.963},      // 16 warps, warp tile 16 x 16, 4 stages (k_a = 64, 128, 256)
     {208, 128, 32, 8, 512, 24, 0.94},       // 16 warps, warp tile 32 x 8, 3 stages (k_a = 32, 160)
+    {209, 128, 48, 16, 384, 48, 0.5},       // z200 with 2 stages (pipeline-depth probe, never chosen)
+    {220, 128, 48, 16, 384, 48, 0.5, 1, 1, 1},   // z200 in 6 half stages (A/B measurement)
+    {227, 64, 64, 16, 512, 24, 0.5, 1, 1, 1},    // z207 in 8 half stages (A/B measurement)
 };
 // real-symmetric variants (columns are real columns; kNT = WNC / 8). eff relative to 103 (n = 13000,
 // k = 624: 33.6 / 32.1 / 31.7 / 29.2 / 32.9 / 32.6 TF/s for 103 / 100 / 101 / 102 / 104 / 105;
@@ -140,7 +144,7 @@ static TileChoice choose(const Variant (&vs)[N], const char* env, int64_t nrows,
   }
   if (best < 0) best = 0;
   const Variant& V = vs[best];
-  return TileChoice{V.id, V.cluster, V.occ, V.bm, V.bnc, V.threads, V.acc, V.wnc, best_cost};
+  return TileChoice{V.id, V.cluster, V.occ, V.kh, V.bm, V.bnc, V.threads, V.acc, V.wnc, best_cost};
 }
 
 }  // namespace
@@ -265,6 +269,12 @@ cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, cons
       return LC(192, 32, 32, 16, 2, kZ3M);
     case 210:
       return launch_cfg<128, 48, 32, 16, 3, kZ3M, 2>(tmA, tmB, tmA3, tmB3, p, stream);
+    case 220:
+      return launch_cfg<128, 48, 32, 16, 6, kZ3M, 1, 1, 1>(tmA, tmB, tmA3, tmB3, p, stream);
+    case 227:
+      return launch_cfg<64, 64, 16, 16, 8, kZ3M, 1, 1, 1>(tmA, tmB, tmA3, tmB3, p, stream);
+    case 209:
+      return LC(128, 48, 32, 16, 2, kZ3M);
     case 207:
       return LC(64, 64, 16, 16, 4, kZ3M);
     case 208:

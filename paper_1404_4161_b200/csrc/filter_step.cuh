@@ -62,9 +62,7 @@ struct StepParams {
   int32_t l2_prefetch;  // > 0: with each stage load, prefetch into L2 the boxes this many iterations ahead
 };
 
-constexpr int kBKHalf = 16;            // doubles per 128-byte swizzle row
-constexpr int kHalves = 2;             // two swizzle rows per stage -> 32 real K per stage
-constexpr int kBK = kBKHalf * kHalves;  // real K per stage
+constexpr int kBKHalf = 16;            // doubles per 128-byte swizzle row (one TMA box of the interleaved operands)
 
 // MODE (the arithmetic of one step):
 //  kReal: real symmetric (BNC, WNC count real columns, a plain real GEMM);
@@ -77,7 +75,10 @@ constexpr int kBK = kBKHalf * kHalves;  // real K per stage
 //         previous step's epilogue) are extra TMA operands, so the main loop has no FP64 add.
 constexpr int kReal = 0, kZ4M = 1, kZ3M = 2;
 
-template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1>
+// KH: 128-byte swizzle rows of the interleaved operands per stage (2: 16 complex K entries per stage; 1:
+// half stages of 8 entries -- twice as many, finer-grained stages in the same shared memory, so a stage
+// is refilled sooner after it is released; the 3M planes then use 64-byte rows with the 64B swizzle)
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int KH = 2>
 struct FilterCfg {
   static constexpr bool kCplx = MODE != kReal;  // complex output columns
   static constexpr int kWarpsM = BM / WM;
@@ -87,16 +88,20 @@ struct FilterCfg {
   static constexpr int kMT = WM / 8;   // 8-row MMA tiles per warp
   static constexpr int kNT = MODE == kZ4M ? WNC / 4 : WNC / 8;  // 8-real-column MMA tiles per warp
   static constexpr int kNP = MODE == kZ3M ? 3 : 1;              // accumulator sets (P1, P2, P3)
-  static constexpr int kA3 = MODE == kZ3M ? BM * 128 : 0;       // a_r - a_i plane, one swizzle row
+  static constexpr int kKH = KH;
+  static constexpr int kBKs = kBKHalf * KH;                     // real K doubles per stage
+  static constexpr int kPlaneRow = 64 * KH;                     // bytes of one plane row per stage
+  static constexpr int kA3 = MODE == kZ3M ? BM * kPlaneRow : 0;  // a_r - a_i plane
   // B regions start on 1024-byte boundaries (the 128B-swizzle pattern is taken from absolute shared
   // address bits, so a region must begin at an 8-row atom): BNC rows padded to a multiple of 8
   static constexpr int kBRow = ((BNC + 7) / 8) * 8 * 128;       // smem stride of one B swizzle region
-  static constexpr int kB3 = MODE == kZ3M ? kBRow : 0;          // y_r + y_i plane
-  static constexpr int kABytes = kHalves * BM * 128 + kA3;
-  static constexpr int kBBytes = kHalves * kBRow + kB3;
+  static constexpr int kB3 = MODE == kZ3M ? ((BNC + 7) / 8) * 8 * kPlaneRow : 0;  // y_r + y_i plane
+  static constexpr int kABytes = KH * BM * 128 + kA3;
+  static constexpr int kBBytes = KH * kBRow + kB3;
   static constexpr int kStageBytes = kABytes + kBBytes;
   // bytes the stage's TMA boxes deliver (mbarrier transaction count)
-  static constexpr int kTxBytes = kHalves * BM * 128 + kA3 + (kHalves + (MODE == kZ3M ? 1 : 0)) * BNC * 128;
+  static constexpr int kTxBytes = KH * BM * 128 + kA3 + KH * BNC * 128 + (MODE == kZ3M ? BNC * kPlaneRow : 0);
+  static_assert(kStageBytes % 1024 == 0, "stages must start on 128B-swizzle atoms");
   static constexpr int kSmemBytes = STAGES * kStageBytes + 2 * STAGES * 8 + 1024;  // + barriers + align
   static_assert(WM % 8 == 0 && WNC % (MODE == kZ4M ? 4 : 8) == 0 && BM % WM == 0 && BNC % WNC == 0, "tile shape");
   static_assert(BM <= 256 && BNC <= 256, "TMA box limit");
@@ -105,6 +110,11 @@ struct FilterCfg {
 // 128B swizzle: 16-byte chunk c of row r lives at chunk (c ^ (r & 7)) (buffer 1024-byte aligned).
 __device__ __forceinline__ uint32_t swz(int row, int chunk) {
   return static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+// 64B swizzle (64-byte rows): 16-byte chunk c of row r lives at chunk c ^ ((r >> 1) & 3) (512-byte atoms)
+__device__ __forceinline__ uint32_t swz64(int row, int chunk) {
+  return static_cast<uint32_t>(row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4));
 }
 
 // first iteration of CTA c in the stream-K tail (balanced integer split)
@@ -137,13 +147,16 @@ __device__ __forceinline__ double xor_sign(double x, uint32_t mask) {
 // stream-K schedule runs over pair tiles (tiles_n N tiles = tiles_n / 2 pair columns) and cluster ids.
 // OCC: CTAs resident per SM (the persistent grid is OCC x SM count; 2 lets one CTA's MMAs cover the
 // other's TMA waits)
-template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int OCC = 1>
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int OCC = 1, int KH = 2>
 __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kThreads, OCC)
     filter_step_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB3,
                        const StepParams p) {
-  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>;
+  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE, CL, KH>;
   static_assert(CL == 1 || CL == 2, "cluster of 1 or 2");
+  static_assert(KH == 2 || (KH == 1 && MODE == kZ3M), "half stages are built for the 3M planes");
+  constexpr int kHalves = KH;
+  constexpr int kBK = Cfg::kBKs;
   static_assert(BM % (8 * CL) == 0, "A box split");
   constexpr bool CPLX = MODE == kZ4M;  // the A' [B' B''] embedding
   constexpr int kNP = Cfg::kNP;
@@ -252,7 +265,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       if constexpr (CL == 1) {
         tma_load_2d(sa + kHalves * BM * 128, &tmA3, ka / 2, m0, &full[st]);
       } else {
-        tma_load_2d_mc(sa + kHalves * BM * 128 + crank * (BM / CL) * 128, &tmA3, ka / 2, m0 + crank * (BM / CL),
+        tma_load_2d_mc(sa + kHalves * BM * 128 + crank * (BM / CL) * Cfg::kPlaneRow, &tmA3, ka / 2, m0 + crank * (BM / CL),
                        &full[st], (uint16_t)((1u << CL) - 1));
       }
       tma_load_3d(sb + kHalves * Cfg::kBRow, &tmB3, kb / 2, bcol, q, &full[st]);
@@ -507,16 +520,25 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
 #pragma unroll
                 for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc2[i][jj][0], acc2[i][jj][1], av[i].y, bv[jj].y);
             }
-            // P3: plane entries 2c, 2c+1 of chunk c = 2qd + h of the 128-byte row (h = 0, 1 cover all 16
-            // entries; even/odd chunks for the two rows of a quarter-warp keep the LDS.128 conflict-free
-            // under the 128B swizzle, chunk' = c ^ (row & 7))
+            // P3: plane entries 2c, 2c+1 of chunk c. KH = 2: c = 2qd + h of the 128-byte row (h = 0, 1
+            // cover all 16 entries; even/odd chunks for the two rows of a quarter-warp keep the LDS.128
+            // conflict-free under the 128B swizzle, c' = c ^ (row & 7)). KH = 1: c = qd of the 64-byte row
+            // (64B swizzle: c' = c ^ ((row >> 1) & 3); rows g, g+1 of a quarter-warp land in opposite
+            // 64-byte halves of the bank space -> conflict-free)
             {
-              const int chunk = 2 * qd + h;
               double2 cv[Cfg::kMT], dv[Cfg::kNT];
+              if constexpr (KH == 2) {
+                const int chunk = 2 * qd + h;
 #pragma unroll
-              for (int i = 0; i < Cfg::kMT; ++i) cv[i] = *reinterpret_cast<const double2*>(a3 + swz(a_row0 + i * 8, chunk));
+                for (int i = 0; i < Cfg::kMT; ++i) cv[i] = *reinterpret_cast<const double2*>(a3 + swz(a_row0 + i * 8, chunk));
 #pragma unroll
-              for (int jj = 0; jj < Cfg::kNT; ++jj) dv[jj] = *reinterpret_cast<const double2*>(b3 + swz(b_row0 + jj * 8, chunk));
+                for (int jj = 0; jj < Cfg::kNT; ++jj) dv[jj] = *reinterpret_cast<const double2*>(b3 + swz(b_row0 + jj * 8, chunk));
+              } else {
+#pragma unroll
+                for (int i = 0; i < Cfg::kMT; ++i) cv[i] = *reinterpret_cast<const double2*>(a3 + swz64(a_row0 + i * 8, qd));
+#pragma unroll
+                for (int jj = 0; jj < Cfg::kNT; ++jj) dv[jj] = *reinterpret_cast<const double2*>(b3 + swz64(b_row0 + jj * 8, qd));
+              }
 #pragma unroll
               for (int i = 0; i < Cfg::kMT; ++i)
 #pragma unroll
@@ -652,6 +674,7 @@ struct TileChoice {
   int id;
   int cluster;  // CTAs per thread-block cluster (2: A-multicast pairs)
   int occ;      // CTAs resident per SM (persistent grid = occ x SMs)
+  int kh;       // 128-byte swizzle rows per stage (real K per stage = 16 kh doubles)
   int bm, bnc;
   int threads;  // CTA size of the variant
   int acc;      // accumulator doubles per thread (partial-slot size = acc * threads doubles)

@@ -12,7 +12,7 @@ from gen.configs import C4_INTERVAL, CONFIGS, c4_ramp
 
 pytestmark = pytest.mark.gpu
 # 3M variants (the default complex arithmetic, ids 200..204) and the 4M real-embedding variants (0..9)
-VARIANTS = ["200", "201", "202", "203", "204", "206", "207", "208", "210", "0", "1", "2", "3", "4", "5", "6", "7", "8", "9", "10", "11", "12", "13", "14", "15"]
+VARIANTS = ["200", "201", "202", "203", "204", "206", "207", "208", "210", "220", "227", "0", "1", "2", "3", "4", "5", "6", "7", "8", "9", "10", "11", "12", "13", "14", "15"]
 
 
 def crand(rng, *shape):
