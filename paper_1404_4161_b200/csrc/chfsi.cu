@@ -154,13 +154,20 @@ static chfsi_status a_operand(chfsi_ctx ctx, const void** Hp, int64_t* ldh, int6
 // 3M: the plane Re H - Im H of the panel (nloc rows x n, row stride ld3), rebuilt unless the solver
 // pinned it for this panel (ctx->h3_pin == Hp for the duration of one eigenproblem).
 chfsi_status h3_prepare(chfsi_ctx ctx, const void* Hp, int64_t ldh, int64_t n, int64_t nloc) {
-  const int64_t ld3 = round_up(n, 2);
+  // K layout of the plane: one rank -> n entries; p ranks -> p chunks of nloc entries, each padded to an
+  // even count (TMA boxes of the plane start on 16-byte boundaries for every rank chunk)
+  const int p = ctx->nranks;
+  const int64_t chunk = p > 1 ? nloc : n, ldk = p > 1 ? round_up(nloc, 2) : n;
+  const int64_t klen = p > 1 ? p * ldk : n;
+  const int64_t ld3 = round_up(klen, 2);
   chfsi_status st = ensure(ctx, ctx->h3, sizeof(double) * (size_t)ld3 * nloc);
   if (st) return st;
   CHFSI_CUDA_TRY(ctx, launch_h3_plane(n, nloc, static_cast<const double2*>(Hp), ldh, static_cast<double*>(ctx->h3.ptr),
-                                      ld3, ctx->stream));
+                                      ld3, chunk, ldk, ctx->stream));
   ctx->launches++;
   ctx->h3_ld = ld3;
+  ctx->h3_klen = klen;
+  ctx->h3_rank_stride = p > 1 ? ldk : 0;
   return CHFSI_OK;
 }
 
@@ -173,7 +180,7 @@ static chfsi_status a3_operand(chfsi_ctx ctx, CUtensorMap* m, const void* Hp, in
     }
     *built = true;
   }
-  return make_tmap_2d(ctx, m, ctx->h3.ptr, n, nloc, ctx->h3_ld, box_rows, 8 * kh);
+  return make_tmap_2d(ctx, m, ctx->h3.ptr, ctx->h3_klen, nloc, ctx->h3_ld, box_rows, 8 * kh);
 }
 
 // Tile variant and arithmetic of one launch. With the 3M column layout available (z3_layout) the
@@ -262,6 +269,7 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
   sp.kt_per_rank = (int32_t)((kr + kbk - 1) / kbk);
   sp.num_kt = sp.kt_per_rank * p;
   sp.a_rank_stride = (int32_t)(elem * nloc);
+  sp.a3_rank_stride = (int32_t)round_up(nloc, 2);
   sp.col0 = 0;
   sp.col_end = (int32_t)k;
   sp.fin_end = (int32_t)k;
@@ -440,6 +448,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       sp.kt_per_rank = (int32_t)((kr + kbk - 1) / kbk);
       sp.num_kt = sp.kt_per_rank * p;
       sp.a_rank_stride = (int32_t)(elem * nloc);
+      sp.a3_rank_stride = (int32_t)round_up(nloc, 2);
       sp.col0 = (int32_t)c0;
       sp.col_end = (int32_t)ce;
       sp.fin_end = (int32_t)fin;
@@ -621,7 +630,8 @@ chfsi_status chfsi_ctx_reserve(chfsi_ctx ctx, int64_t n, int64_t nloc, int64_t k
     if (!st) st = ensure(ctx, ctx->R0, rb);
     if (!st) st = ensure(ctx, ctx->R1, rb);
   }
-  if (!st && ctx->zmul == 3) st = ensure(ctx, ctx->h3, sizeof(double) * (size_t)round_up(n, 2) * nloc);
+  if (!st && ctx->zmul == 3)  // the plane, with the rank chunks padded to even lengths at p > 1
+    st = ensure(ctx, ctx->h3, sizeof(double) * (size_t)round_up(ctx->nranks * round_up(nloc, 2), 2) * nloc);
   return st;
 }
 

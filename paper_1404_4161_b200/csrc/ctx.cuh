@@ -90,6 +90,8 @@ struct chfsi_ctx_s {
   int zmul = 3;
   chfsi::DevBuf h3;
   int64_t h3_ld = 0;
+  int64_t h3_klen = 0;         // K extent of the plane (n, or p chunks of nloc padded to even)
+  int64_t h3_rank_stride = 0;  // K offset between rank chunks of the plane (p > 1)
   const void* h3_pin = nullptr;
 
   // workspace

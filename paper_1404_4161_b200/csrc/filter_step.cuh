@@ -18,6 +18,7 @@ struct StepParams {
   int32_t num_kt;       // k-tiles per output tile (32 real = 16 complex contraction entries each)
   int32_t kt_per_rank;  // k-tiles per rank chunk of the B operand (== num_kt when p == 1)
   int32_t a_rank_stride;  // real-K offset between rank chunks in A (2 * nloc_per_rank)
+  int32_t a3_rank_stride;  // 3M: K offset between rank chunks in the Re H - Im H plane (nloc rounded up to even)
   int32_t col0;         // first active complex column s_i
   int32_t col_end;      // k (one past the last active column)
   int32_t fin_end;      // columns [col0, fin_end) finish at this step and go to `out`
@@ -251,6 +252,9 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     const int t = kt - q * p.kt_per_rank;
     const int ka = q * p.a_rank_stride + t * kBK;
     const int kb = t * kBK;
+    // plane K coordinate: rank chunks of the plane start on even entries (a3_rank_stride = nloc rounded
+    // up to even) -- a TMA box starting 8 bytes off a 16-byte boundary traps
+    const int ka3 = q * p.a3_rank_stride + t * (kBK / 2);
 #pragma unroll
     for (int h = 0; h < kHalves; ++h) {
       if constexpr (CL == 1) {
@@ -263,9 +267,9 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     }
     if constexpr (MODE == kZ3M) {  // the real planes: 16 complex entries = one 128-byte row
       if constexpr (CL == 1) {
-        tma_load_2d(sa + kHalves * BM * 128, &tmA3, ka / 2, m0, &full[st]);
+        tma_load_2d(sa + kHalves * BM * 128, &tmA3, ka3, m0, &full[st]);
       } else {
-        tma_load_2d_mc(sa + kHalves * BM * 128 + crank * (BM / CL) * Cfg::kPlaneRow, &tmA3, ka / 2, m0 + crank * (BM / CL),
+        tma_load_2d_mc(sa + kHalves * BM * 128 + crank * (BM / CL) * Cfg::kPlaneRow, &tmA3, ka3, m0 + crank * (BM / CL),
                        &full[st], (uint16_t)((1u << CL) - 1));
       }
       tma_load_3d(sb + kHalves * Cfg::kBRow, &tmB3, kb / 2, bcol, q, &full[st]);
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       tma_prefetch_l2_3d(&tmB, kb + h * kBKHalf, bcol, q);
     }
     if constexpr (MODE == kZ3M) {
-      if (CL == 1 || crank == 0) tma_prefetch_l2_2d(&tmA3, ka / 2, m0);
+      if (CL == 1 || crank == 0) tma_prefetch_l2_2d(&tmA3, q * p.a3_rank_stride + t * (kBK / 2), m0);
       tma_prefetch_l2_3d(&tmB3, kb / 2, bcol, q);
     }
   };

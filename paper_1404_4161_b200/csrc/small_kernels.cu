@@ -33,12 +33,20 @@ __global__ void hemv_kernel(int64_t n, int64_t nloc, const double2* __restrict__
   if (lane == 0) w[r] = make_double2(sr, si);
 }
 
+// K entry q of chunk c = q / chunk lands at c * ldk + q % chunk (ldk >= chunk; the gaps are zero)
 __global__ void h3_plane_kernel(int64_t n, int64_t nloc, const double2* __restrict__ Hp, int64_t ldh,
-                                double* __restrict__ H3, int64_t ld3) {
+                                double* __restrict__ H3, int64_t ld3, int64_t chunk, int64_t ldk) {
   const int64_t r = blockIdx.y;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-    const double2 h = __ldcs(Hp + r * ldh + q);
-    H3[r * ld3 + q] = h.x - h.y;
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nchunks * ldk;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / ldk, o = i - c * ldk, q = c * chunk + o;
+    double v = 0.0;
+    if (o < chunk && q < n) {
+      const double2 h = __ldcs(Hp + r * ldh + q);
+      v = h.x - h.y;
+    }
+    H3[r * ld3 + i] = v;
   }
 }
 
@@ -397,10 +405,11 @@ cudaError_t launch_orth_err(int64_t k, const double* G, int64_t ldg, double* out
 }
 
 cudaError_t launch_h3_plane(int64_t n, int64_t nloc, const double2* Hp, int64_t ldh, double* H3, int64_t ld3,
-                            cudaStream_t st) {
+                            int64_t chunk, int64_t ldk, cudaStream_t st) {
   if (n <= 0 || nloc <= 0) return cudaSuccess;
-  const unsigned bx = (unsigned)std::min<int64_t>((n + 255) / 256, 16);
-  h3_plane_kernel<<<dim3(bx, (unsigned)nloc), 256, 0, st>>>(n, nloc, Hp, ldh, H3, ld3);
+  const int64_t len = (n + chunk - 1) / chunk * ldk;
+  const unsigned bx = (unsigned)std::min<int64_t>((len + 255) / 256, 16);
+  h3_plane_kernel<<<dim3(bx, (unsigned)nloc), 256, 0, st>>>(n, nloc, Hp, ldh, H3, ld3, chunk, ldk);
   return cudaGetLastError();
 }
 

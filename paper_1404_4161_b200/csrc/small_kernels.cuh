@@ -33,10 +33,12 @@ cudaError_t launch_scale(int64_t rows, double2* x, double s, cudaStream_t st);
 // G[i,j] for i<k: make identity minus G, return max |entry| into out[0] via atomicMax on the bit pattern
 cudaError_t launch_orth_err(int64_t k, const double2* G, int64_t ldg, double* out, cudaStream_t st);
 
-// 3M filter operands. H3[r * ld3 + q] = Re Hp[q, r] - Im Hp[q, r] for the nloc local
-// rows r (K-major like the interleaved A operand; HBM-bound, 24 bytes per entry)
+// 3M filter operands. H3[r * ld3 + c * ldk + o] = Re Hp[q, r] - Im Hp[q, r] for the
+// nloc local rows r and K entries q = c * chunk + o (the rank chunks of the contraction, each padded to
+// ldk >= chunk with zeros; chunk = ldk = n on one rank). K-major like the interleaved A operand;
+// HBM-bound, 24 bytes per entry.
 cudaError_t launch_h3_plane(int64_t n, int64_t nloc, const double2* Hp, int64_t ldh, double* H3, int64_t ld3,
-                            cudaStream_t st);
+                            int64_t chunk, int64_t ldk, cudaStream_t st);
 // extended column layout of a B operand: dst + j * cs holds column j of X as rows complex values,
 // followed at double offset y3_off by the plane Re X[:, j] + Im X[:, j] (cs, y3_off in doubles)
 cudaError_t launch_pack_y3(int64_t rows, int64_t cols, const double2* X, int64_t ldx, double* dst, int64_t cs,

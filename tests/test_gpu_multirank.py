@@ -68,11 +68,13 @@ def slabs(chfsi, H, P):
 
 @pytest.mark.parametrize("n,P,group_cols,push", [(512, 2, None, False), (600, 4, None, False), (256, 8, None, False),
                                                   (512, 2, 8, False), (600, 4, 10, False), (256, 8, 0, False),
-                                                  (512, 2, None, True), (600, 4, None, True), (256, 8, None, True)])
+                                                  (512, 2, None, True), (600, 4, None, True), (256, 8, None, True),
+                                                  (1000, 8, None, False), (1000, 8, 8, False), (1000, 8, None, True)])
 def test_filter_multirank(gpu_lib, n, P, group_cols, push):
     """group_cols: None = default (one group at k = 37), 8 / 10 = 4 / 3 column groups whose
     allgathers overlap the next group's K1 on a separate stream, 0 = pipelining off. push: the
-    filter epilogue stores each rank's rows into every rank's next-step operand (peer pointers)."""
+    filter epilogue stores each rank's rows into every rank's next-step operand (peer pointers).
+    n = 1000 over 8 ranks gives odd panels (nloc = 125, like c2's 1625 at p = 8)."""
     k = 37
     w = G.wy(n, int(0.9 * n), n + P)
     H = w.full()
