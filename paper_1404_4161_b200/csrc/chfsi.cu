@@ -137,17 +137,40 @@ static chfsi_status b_operand(chfsi_ctx ctx, Operand* op, const double* buf, int
   return make_tmap_3d(ctx, &op->tm3, buf + 2 * ld, rows, cols, nranks, cs, cs * cols, box_cols, 8 * kh);
 }
 
-// The A operand (H panel) through TMA needs a 16-byte row stride: real data with an odd ldh is first
-// copied into a workspace with an even leading dimension.
-static chfsi_status a_operand(chfsi_ctx ctx, const void** Hp, int64_t* ldh, int64_t n, int64_t nloc, int elem) {
-  if ((elem * *ldh * 8) % 16 == 0) return CHFSI_OK;
-  const int64_t ld2 = round_up(n, 2);
+// The A operand (H panel) through TMA: every box must start on a 16-byte boundary. Complex data always
+// does (16-byte elements). Real data is re-strided into a workspace when the panel's leading dimension
+// is odd, or when p > 1 and nloc is odd (rank chunk q of the contraction starts at row q nloc): there
+// each rank chunk is padded to an even length with zero rows. *kchunk = the K offset (elements) between
+// rank chunks, *klen = the K extent of the operand.
+static chfsi_status a_operand(chfsi_ctx ctx, const void** Hp, int64_t* ldh, int64_t n, int64_t nloc, int elem,
+                              int64_t* kchunk, int64_t* klen) {
+  const int p = ctx->nranks;
+  *kchunk = nloc;
+  *klen = n;
+  const bool odd_ld = (elem * *ldh * 8) % 16 != 0;
+  const bool odd_chunks = elem == 1 && p > 1 && (nloc % 2) != 0;
+  if (!odd_ld && !odd_chunks) return CHFSI_OK;
+  const int64_t ldk = odd_chunks ? round_up(nloc, 2) : nloc;
+  const int64_t len = odd_chunks ? p * ldk : n;
+  const int64_t ld2 = round_up(len, 2);
   chfsi_status st = ensure(ctx, ctx->hpad, sizeof(double) * elem * (size_t)ld2 * nloc);
   if (st) return st;
-  CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(ctx->hpad.ptr, 8 * elem * ld2, *Hp, 8 * elem * *ldh, 8 * elem * n, nloc,
-                                        cudaMemcpyDeviceToDevice, ctx->stream));
-  *Hp = ctx->hpad.ptr;
+  double* dst = static_cast<double*>(ctx->hpad.ptr);
+  const char* src = static_cast<const char*>(*Hp);
+  if (odd_chunks) {
+    CHFSI_CUDA_TRY(ctx, cudaMemsetAsync(dst, 0, sizeof(double) * elem * (size_t)ld2 * nloc, ctx->stream));
+    for (int q = 0; q < p; ++q)
+      CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(dst + (size_t)elem * q * ldk, 8 * elem * ld2, src + 8 * elem * q * nloc,
+                                            8 * elem * *ldh, 8 * elem * nloc, nloc, cudaMemcpyDeviceToDevice,
+                                            ctx->stream));
+  } else {
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(dst, 8 * elem * ld2, src, 8 * elem * *ldh, 8 * elem * n, nloc,
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  *Hp = dst;
   *ldh = ld2;
+  *kchunk = ldk;
+  *klen = len;
   return CHFSI_OK;
 }
 
@@ -218,9 +241,10 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
   const int cw = z3 ? 3 : elem;
   const size_t eb = 8 * (size_t)elem;
   CUtensorMap tmA, tmA3;
-  chfsi_status st = a_operand(ctx, &Hp, &ldh, n, nloc, elem);
+  int64_t kchunk, klen;
+  chfsi_status st = a_operand(ctx, &Hp, &ldh, n, nloc, elem, &kchunk, &klen);
   if (st) return st;
-  st = make_tmap_2d(ctx, &tmA, Hp, elem * n, nloc, elem * ldh, t.bm / t.cluster);
+  st = make_tmap_2d(ctx, &tmA, Hp, elem * klen, nloc, elem * ldh, t.bm / t.cluster);
   if (st) return st;
   tmA3 = tmA;
   bool h3_built = false;
@@ -268,7 +292,7 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
   const int64_t kbk = 16 * t.kh;  // real K per stage of the variant
   sp.kt_per_rank = (int32_t)((kr + kbk - 1) / kbk);
   sp.num_kt = sp.kt_per_rank * p;
-  sp.a_rank_stride = (int32_t)(elem * nloc);
+  sp.a_rank_stride = (int32_t)(elem * kchunk);
   sp.a3_rank_stride = (int32_t)round_up(nloc, 2);
   sp.col0 = 0;
   sp.col_end = (int32_t)k;
@@ -353,7 +377,8 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
   }
   if (p > 1 && !st) st = ensure(ctx, ctx->R0, rbytes);
   if (p > 1 && !st) st = ensure(ctx, ctx->R1, rbytes);
-  if (!st) st = a_operand(ctx, &Hp, &ldh, n, nloc, elem);
+  int64_t kchunk = nloc, klen = n;
+  if (!st) st = a_operand(ctx, &Hp, &ldh, n, nloc, elem, &kchunk, &klen);
   if (st) return st;
   const std::vector<int64_t> gb = filter_groups(ctx, k);
   const int G = (int)gb.size() - 1;
@@ -426,7 +451,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       if (!z3k) plane_ok[g] = 0;
       const int abox = t.bm / t.cluster;  // A box rows (a CTA pair loads half the tile each)
       if (abox != last_bm) {
-        st = make_tmap_2d(ctx, &tmA, Hp, elem * n, nloc, elem * ldh, abox);
+        st = make_tmap_2d(ctx, &tmA, Hp, elem * klen, nloc, elem * ldh, abox);
         if (st) return st;
         last_bm = abox;
       }
@@ -447,7 +472,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       const int64_t kbk = 16 * t.kh;  // real K per stage of the variant
       sp.kt_per_rank = (int32_t)((kr + kbk - 1) / kbk);
       sp.num_kt = sp.kt_per_rank * p;
-      sp.a_rank_stride = (int32_t)(elem * nloc);
+      sp.a_rank_stride = (int32_t)(elem * kchunk);
       sp.a3_rank_stride = (int32_t)round_up(nloc, 2);
       sp.col0 = (int32_t)c0;
       sp.col_end = (int32_t)ce;

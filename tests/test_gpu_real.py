@@ -61,12 +61,15 @@ def test_filter_real_diag_closed_form(gpu_lib):
     assert (np.linalg.norm(Y - Yc, axis=0) / np.linalg.norm(Yc, axis=0)).max() <= 1e-13
 
 
-def test_filter_real_multirank(gpu_lib):
+@pytest.mark.parametrize("n,P", [(640, 4), (1000, 8), (1002, 2)])
+def test_filter_real_multirank(gpu_lib, n, P):
+    """Emulated ranks; (1000, 8) and (1002, 2) have odd panels (nloc = 125, 501): the real A operand's
+    rank chunks then start on odd doubles (the library re-strides the panel)."""
     import threading
 
     import torch
 
-    n, P, k = 640, 4, 21
+    k = 21
     H = real_sym(n, 11)
     rng = np.random.default_rng(5)
     deg = sorted(rng.integers(1, 15, k).tolist())
@@ -134,3 +137,44 @@ def test_solve_real_known_spectrum_and_vs_oracle(gpu_lib):
     ro = O.chfsi_solve(H.astype(complex), X0.astype(complex), nev, nex, 1e-10, 20, seed=3)
     assert np.max(np.abs(got - ro["lam"]) / np.abs(ro["lam"])) <= 1e-10
     assert out["reports"][0]["filter_flops"] == pytest.approx(2.0 * n * n * out["reports"][0]["matvecs_filter"])
+
+
+def test_solve_real_multirank_odd_panels(gpu_lib):
+    """Real-symmetric ChFSI over 2 emulated ranks with odd panels (nloc = 255): every step of the path
+    (Lanczos, filter on the re-strided A operand, QR, Rayleigh-Ritz) on row panels, against the known
+    spectrum of H = Q diag(lambda) Q^T."""
+    import threading
+
+    import torch
+
+    n, P, nev, nex = 510, 2, 16, 8
+    H, lam = real_known(n, 470, 9)
+    X0 = np.asfortranarray(np.random.default_rng(2).standard_normal((n, nev + nex)))
+    nloc = n // P
+    g = gpu_lib.LocalGroup(P)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    ctxs = [gpu_lib.Context(0, stream=streams[r], local_group=g, rank=r) for r in range(P)]
+    Hs = [gpu_lib.to_colmajor(np.asfortranarray(H[:, r * nloc:(r + 1) * nloc]), real=True) for r in range(P)]
+    Xs = [gpu_lib.to_colmajor(np.asfortranarray(X0[r * nloc:(r + 1) * nloc]), real=True) for r in range(P)]
+    torch.cuda.synchronize()
+    outs, errs = [None] * P, []
+
+    def work(r):
+        try:
+            with torch.cuda.stream(streams[r]):
+                outs[r] = ctxs[r].solve_sequence(lambda ell: Hs[r], 1, Xs[r], nev, nex, 1e-10, deg_cap=20, seed=3,
+                                                 real=True, n=n, row0=r * nloc)
+                streams[r].synchronize()
+        except Exception as ex:
+            errs.append(ex)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    torch.cuda.synchronize()
+    [cx.close() for cx in ctxs]
+    g.close()
+    assert not errs, errs
+    for o in outs:
+        assert o["status"] == 0
+        assert np.max(np.abs(o["lam"][0] - lam[:nev]) / np.abs(lam[:nev])) <= 1e-10
