@@ -172,3 +172,24 @@ def test_solve_multirank_c0(gpu_lib, P, group_cols, push):
     X = np.concatenate([x.cpu().numpy() for x in Xs], axis=0)[:, :nev]
     res = np.linalg.norm(H @ X - X * out[0]["lam"][0], axis=0) / HNORM
     assert res.max() <= cf["tol"]
+
+
+@pytest.mark.parametrize("push", [False, True])
+def test_solve_multirank_odd_panels_3m(gpu_lib, push):
+    """Complex ChFSI over 2 emulated ranks with odd panels (nloc = 255) and a block wide enough for the
+    3M kernel (k = 32): filter, H Q of Rayleigh-Ritz and the 3M plane all on odd rank chunks."""
+    n, P, nev, nex = 510, 2, 24, 8
+    w = G.wy(n, 470, 21)
+    H = w.full()
+    X0 = G.start_basis(n, nev + nex, 21)
+    Hs, nloc = slabs(gpu_lib, H, P)
+    Xs = [gpu_lib.to_colmajor(X0[r * nloc:(r + 1) * nloc]) for r in range(P)]
+
+    def fn(r, ctx):
+        return ctx.solve_sequence(lambda ell: Hs[r], 1, Xs[r], nev, nex, 1e-10, deg_cap=20, seed=21, n=n,
+                                  row0=r * nloc)
+
+    out = run_ranks(gpu_lib, P, fn, None, (n, nloc, nev + nex) if push else None)
+    for o in out:
+        assert o["status"] == 0
+        assert np.max(np.abs(o["lam"][0] - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
