@@ -50,9 +50,12 @@ struct Sc<cuDoubleComplex> {
   static T one() { return {1.0, 0.0}; }
   static T zero() { return {0.0, 0.0}; }
   static T mone() { return {-1.0, 0.0}; }
-  static cublasStatus_t gemm(cublasHandle_t h, cublasOperation_t a, cublasOperation_t b, int m, int n, int k,
+  // the n k^2-class products of QR / Rayleigh-Ritz: cuBLAS ZGEMM, or its Gauss 3M form (ZGEMM3M) when the
+  // context runs the filter in 3M (the same arithmetic, 25 % fewer real multiplications)
+  static cublasStatus_t gemm(chfsi_ctx ctx, cublasOperation_t a, cublasOperation_t b, int m, int n, int k,
                              const T* al, const T* A, int lda, const T* B, int ldb, const T* be, T* C, int ldc) {
-    return cublasZgemm(h, a, b, m, n, k, al, A, lda, B, ldb, be, C, ldc);
+    if (ctx->zmul == 3) return cublasZgemm3m(ctx->cublas, a, b, m, n, k, al, A, lda, B, ldb, be, C, ldc);
+    return cublasZgemm(ctx->cublas, a, b, m, n, k, al, A, lda, B, ldb, be, C, ldc);
   }
   static cublasStatus_t gemv(cublasHandle_t h, cublasOperation_t a, int m, int n, const T* al, const T* A, int lda,
                              const T* x, const T* be, T* y) {
@@ -99,9 +102,9 @@ struct Sc<double> {
   static T one() { return 1.0; }
   static T zero() { return 0.0; }
   static T mone() { return -1.0; }
-  static cublasStatus_t gemm(cublasHandle_t h, cublasOperation_t a, cublasOperation_t b, int m, int n, int k,
+  static cublasStatus_t gemm(chfsi_ctx ctx, cublasOperation_t a, cublasOperation_t b, int m, int n, int k,
                              const T* al, const T* A, int lda, const T* B, int ldb, const T* be, T* C, int ldc) {
-    return cublasDgemm(h, a, b, m, n, k, al, A, lda, B, ldb, be, C, ldc);
+    return cublasDgemm(ctx->cublas, a, b, m, n, k, al, A, lda, B, ldb, be, C, ldc);
   }
   static cublasStatus_t gemv(cublasHandle_t h, cublasOperation_t a, int m, int n, const T* al, const T* A, int lda,
                              const T* x, const T* be, T* y) {
@@ -147,7 +150,7 @@ static chfsi_status gram(chfsi_ctx ctx, int64_t K, int64_t m, int64_t n, const v
                          int64_t ldb, void* C, int64_t ldc) {
   using S = Sc<T>;
   const T one = S::one(), zero = S::zero();
-  CUBLAS_TRY(ctx, S::gemm(ctx->cublas, S::opH, CUBLAS_OP_N, (int)m, (int)n, (int)K, &one, static_cast<const T*>(A),
+  CUBLAS_TRY(ctx, S::gemm(ctx, S::opH, CUBLAS_OP_N, (int)m, (int)n, (int)K, &one, static_cast<const T*>(A),
                           (int)lda, static_cast<const T*>(B), (int)ldb, &zero, static_cast<T*>(C), (int)ldc));
   if (ctx->nranks > 1) {
     if (ldc != m) {
@@ -354,7 +357,7 @@ chfsi_status qr_t(chfsi_ctx ctx, int64_t n, int64_t nloc, const void* XL, int64_
   if (nl > 0) {
     for (int pass = 0; pass < 2; ++pass) {
       TRY(gram<T>(ctx, nloc, nl, ka, XL, ldxl, Y, ldy, G, nl));
-      CUBLAS_TRY(ctx, S::gemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)nl, &mone, Xt, (int)ldxl, G,
+      CUBLAS_TRY(ctx, S::gemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)nl, &mone, Xt, (int)ldxl, G,
                               (int)nl, &one, Yt, (int)ldy));
     }
   }
@@ -431,10 +434,10 @@ chfsi_status rr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const vo
   }
   TRY(comm_bcast(ctx, reinterpret_cast<double*>(G), (size_t)S::elem * ka * ka, 0));
   TRY(comm_bcast(ctx, dmu, (size_t)ka, 0));
-  CUBLAS_TRY(ctx, S::gemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)ka, &one, Qt, (int)ldq, G,
+  CUBLAS_TRY(ctx, S::gemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)ka, &one, Qt, (int)ldq, G,
                           (int)ka, &zero, Yr, (int)nloc));
   if (resid) {
-    CUBLAS_TRY(ctx, S::gemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)ka, &one, W, (int)nloc, G,
+    CUBLAS_TRY(ctx, S::gemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)ka, &one, W, (int)nloc, G,
                             (int)ka, &zero, HY, (int)nloc));
     CHFSI_CUDA_TRY(ctx, launch_resid2(nloc, ka, reinterpret_cast<const D*>(HY), nloc, reinterpret_cast<const D*>(Yr),
                                       nloc, dmu, dr, ctx->stream));
