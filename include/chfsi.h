@@ -186,7 +186,8 @@ chfsi_status chfsi_back_transform(chfsi_ctx ctx, int64_t n, const void* L, int64
                                   int64_t ldx, int64_t k);
 
 typedef struct {
-  int32_t nev, nex;      /* wanted eigenpairs and extra buffer columns, k = nev + nex <= n */
+  int32_t nev, nex;      /* wanted eigenpairs and extra buffer columns, k = nev + nex <= n; nex >= 1
+                            (the filter interval starts at the largest of the k current values, R4) */
   int32_t deg0;          /* starting degree of each problem's first loop (R12; default 8) */
   int32_t deg_cap;       /* degree cap (default 40), <= CHFSI_MAX_DEGREE */
   int32_t max_loops;     /* default 50 */

@@ -303,11 +303,14 @@ static chfsi_status solve_sequence_t(chfsi_ctx ctx, int64_t n, int64_t row0, int
   }
   const chfsi_opts& o = *opts;
   const int64_t k = (int64_t)o.nev + o.nex;
-  if (o.nev < 1 || o.nex < 0 || k > n || !(o.tol > 0) || o.deg0 < 1 || o.deg0 > o.deg_cap ||
+  // nex >= 1: the filter interval starts at the largest of the k current values (R4), so without a
+  // buffer vector it would start at the last wanted Ritz value and never separate it from the unwanted
+  if (o.nev < 1 || o.nex < 1 || k > n || !(o.tol > 0) || o.deg0 < 1 || o.deg0 > o.deg_cap ||
       o.deg_cap > CHFSI_MAX_DEGREE || o.max_loops < 1 || o.lanczos_steps < 1 || o.fixed_degree < 0 ||
       o.fixed_degree > CHFSI_MAX_DEGREE ||
       (nloc * ctx->nranks != n || row0 != nloc * ctx->rank)) {
-    set_err(ctx, "chfsi_solve_sequence: bad options (need 0 < nev, nev + nex <= n, tol > 0, 1 <= deg0 <= cap <= 64)");
+    set_err(ctx, "chfsi_solve_sequence: bad options (need nev >= 1, nex >= 1, nev + nex <= n, tol > 0, "
+                 "1 <= deg0 <= cap <= 64)");
     return CHFSI_ERR_ARG;
   }
   cudaSetDevice(ctx->device);

@@ -193,3 +193,24 @@ def test_solve_multirank_odd_panels_3m(gpu_lib, push):
     for o in out:
         assert o["status"] == 0
         assert np.max(np.abs(o["lam"][0] - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
+
+
+@pytest.mark.parametrize("push", [False, True])
+def test_filter_multirank_tiny_panels(gpu_lib, push):
+    """Panels smaller than one K tile (n = 64 over 8 ranks: nloc = 8 rows, 16 real K per rank chunk) and
+    a single column, against the oracle."""
+    n, P = 64, 8
+    w = G.wy(n, 56, 5)
+    H = w.full()
+    rng = np.random.default_rng(3)
+    for k, deg in ((1, [7]), (30, sorted(rng.integers(1, 12, 30).tolist()))):
+        Y0 = crand(rng, n, k)
+        l1, a, b = w.lam[0] - 0.05, w.lam[min(k, n - 1)], 45.0
+        c, e = (a + b) / 2, (b - a) / 2
+        Hs, nloc = slabs(gpu_lib, H, P)
+        Ys = [gpu_lib.to_colmajor(Y0[r * nloc:(r + 1) * nloc]) for r in range(P)]
+        run_ranks(gpu_lib, P, lambda r, ctx: ctx.filter(Hs[r], Ys[r], deg, l1, c, e, n=n, row0=r * nloc), None,
+                  (n, nloc, k) if push else None)
+        Y = np.concatenate([y.cpu().numpy() for y in Ys], axis=0)
+        Yo, _ = O.chebyshev_filter(H, Y0, deg, l1, c, e)
+        assert (np.linalg.norm(Y - Yo, axis=0) / np.linalg.norm(Yo, axis=0)).max() <= 1e-11

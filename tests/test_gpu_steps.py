@@ -288,3 +288,23 @@ def test_library_owned_nccl_communicator(gpu_lib):
     ctx.close()
     assert out["status"] == 0
     assert np.max(np.abs(out["lam"][0] - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
+
+
+def test_solve_without_buffer_vectors(gpu_lib, ctx):
+    """nex = 0 is rejected (ERR_ARG): the filter interval starts at the largest of the k current values
+    (reading R4), which without a buffer vector is the last wanted Ritz value itself -- it would never be
+    separated from the damped interval. A small buffer (nex = 8 at the degree cap 40) converges."""
+    cf = CONFIGS["c0"]
+    n, nev = cf["n"], 40
+    w = G.wy(n, cf["nd"], cf["seed"])
+    H = w.full()
+    Hd = gpu_lib.to_colmajor(H)
+    with pytest.raises(gpu_lib.ChfsiError, match="ERR_ARG"):
+        ctx.solve_sequence(lambda ell: Hd, 1, gpu_lib.to_colmajor(G.start_basis(n, nev, cf["seed"])), nev, 0,
+                           cf["tol"], deg_cap=cf["cap"], seed=cf["seed"])
+    Xd = gpu_lib.to_colmajor(G.start_basis(n, nev + 8, cf["seed"]))
+    out = ctx.solve_sequence(lambda ell: Hd, 1, Xd, nev, 8, cf["tol"], deg_cap=40, seed=cf["seed"], max_loops=200)
+    assert out["status"] == 0
+    assert np.max(np.abs(out["lam"][0] - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
+    X = Xd.cpu().numpy()[:, :nev]
+    assert (np.linalg.norm(H @ X - X * out["lam"][0], axis=0) / HNORM).max() <= cf["tol"]
