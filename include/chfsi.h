@@ -92,7 +92,7 @@ chfsi_status chfsi_ctx_set_complex_mult(chfsi_ctx ctx, int32_t mults);
  *          mappings between processes; plain pointers between the ranks of a local group), so the
  *          exchange overlaps the MMAs tile by tile; one small barrier (a one-element NCCL allreduce, or
  *          the local group's event barrier) separates consecutive steps.
- * Mode 1 requires the workspace to be reserved first (chfsi_ctx_reserve with the largest n, nloc and
+ * Mode 1 supports up to 8 ranks (one 8-GPU NVSwitch box) and requires the workspace to be reserved first (chfsi_ctx_reserve with the largest n, nloc and
  * block width to be used); the ranks' buffers are then pinned: a later chfsi_ctx_reserve or filter
  * call needing a larger block returns CHFSI_ERR_ARG. Errors: CHFSI_ERR_ARG (null ctx, bad mode, no
  * reservation), CHFSI_ERR_CUDA (IPC mapping failed), CHFSI_ERR_NCCL. No-op at nranks == 1. */

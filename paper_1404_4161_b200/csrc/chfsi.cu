@@ -704,6 +704,10 @@ chfsi_status chfsi_ctx_set_exchange(chfsi_ctx ctx, int32_t mode) {
     ctx->exchange = 0;
     return CHFSI_OK;
   }
+  if (ctx->nranks > StepParams::kMaxRdst) {  // one peer pointer per rank travels in the kernel parameters
+    set_err(ctx, "chfsi_ctx_set_exchange: the peer push supports at most 8 ranks (one NVLink domain box)");
+    return CHFSI_ERR_ARG;
+  }
   chfsi_status st = comm_open_peers(ctx);
   if (st) return st;
   ctx->exchange = 1;

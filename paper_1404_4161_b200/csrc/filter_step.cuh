@@ -3,11 +3,16 @@
 // TMA-staged, 128B-swizzled shared-memory tiles, with the three-term-recurrence axpby, the degree
 // masking and the finished-column store in the epilogue (no separate elementwise pass).
 //
-// Complex -> real embedding: Hp (n x nloc, complex, column-major) is read as a real
-// K-major matrix A' (nloc rows, K' = 2n), Y_i as real K-major columns B' = (re, im, re, im, ...).
-// The imaginary output column uses B''_j = (im, -re, im, -re, ...) built in registers from the same
-// shared tile (swap + sign), so C = A' [B' B''] has (Re, Im) of output (r, j) in one thread's
-// accumulator pair:  Re = sum a_q c_q + b_q d_q,  Im = sum a_q d_q - b_q c_q  for conj(h) * y.
+// Complex arithmetic, MODE below:
+//  3M (default): P1 = sum Re h Re y, P2 = sum Im h Im y, P3 = sum (Re h - Im h)(Re y + Im y) from the
+//    interleaved tiles plus two TMA-staged real planes; Re = P1 + P2, Im = P3 - P1 + P2 for conj(h) y.
+//  4M: Hp (n x nloc, complex, column-major) is read as a real K-major matrix A' (nloc rows, K' = 2n),
+//    Y_i as real K-major columns B' = (re, im, re, im, ...). The imaginary output column uses
+//    B''_j = (im, -re, im, -re, ...) built in registers from the same shared tile (swap + sign), so
+//    C = A' [B' B''] has (Re, Im) of output (r, j) in one thread's accumulator pair.
+// Schedule: persistent CTAs (data-parallel tiles, then stream-K over the remaining k-iterations),
+// thread 0 of each CTA issues the TMA loads; optional thread-block clusters (CL = 2, multicast H tile),
+// 2 CTAs per SM (OCC = 2) and half stages (KH = 1) exist as measured alternatives.
 #pragma once
 #include "common.cuh"
 
