@@ -164,27 +164,7 @@ TileChoice choose_filter_tile_real(int64_t nrows, int64_t ncols, int num_sms) {
   return choose(kVariantsReal, "CHFSI_FILTER_VARIANT_REAL", nrows, ncols, 1.0, 20.0);
 }
 
-// K1 stage refill protocol (StepParams::refill_mode); CHFSI_K1_REFILL overrides (A/B measurements)
-static int refill_mode() {
-  static const int m = [] {
-    const char* e = getenv("CHFSI_K1_REFILL");
-    return e ? atoi(e) : 0;
-  }();
-  return m;
-}
-
-// L2 prefetch distance of K1 (StepParams::l2_prefetch); CHFSI_K1_L2PF overrides (A/B measurements)
-static int l2_prefetch() {
-  static const int m = [] {
-    const char* e = getenv("CHFSI_K1_L2PF");
-    return e ? atoi(e) : 0;
-  }();
-  return m;
-}
-
 void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
-  p.refill_mode = refill_mode();
-  p.l2_prefetch = l2_prefetch();
   const int64_t ncols = p.col_end - p.col0;
   const int64_t cl = t.cluster;
   const int64_t tm = (p.nrows + t.bm - 1) / t.bm;

@@ -64,8 +64,6 @@ struct StepParams {
   int64_t y3_off;
   int64_t y3_off_r;
   int* nonfinite;       // set to 1 if any written value is not finite (nullable)
-  int32_t refill_mode;  // 0: thread 0 refills one stage behind; 1: the last warp to release a stage refills it
-  int32_t l2_prefetch;  // > 0: with each stage load, prefetch into L2 the boxes this many iterations ahead
 };
 
 constexpr int kBKHalf = 16;            // doubles per 128-byte swizzle row (one TMA box of the interleaved operands)
@@ -174,7 +172,6 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes);
   uint64_t* empty = full + STAGES;
   __shared__ int s_ticket;
-  __shared__ int refill_cnt[STAGES];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -200,7 +197,6 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], Cfg::kConsumerWarps * CL);  // CL = 2: both CTAs release a stage
-      refill_cnt[s] = 0;
     }
     fence_barrier_init();
   }
@@ -280,31 +276,8 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       tma_load_3d(sb + kHalves * Cfg::kBRow, &tmB3, kb / 2, bcol, q, &full[st]);
     }
   };
-  // L2 prefetch of the boxes of CTA-local iteration jj (issued p.l2_prefetch iterations ahead of its load)
-  auto prefetch_l2 = [&](int64_t jj) {
-    int T, kt;
-    coords(jj, T, kt);
-    const int tile = cta_tile(T);
-    const int m0 = (tile / p.tiles_n) * BM;
-    int nu;
-    const int bcol = p.b_col0 + tile_cols(tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
-    const int q = kt / p.kt_per_rank;
-    const int t = kt - q * p.kt_per_rank;
-    const int ka = q * p.a_rank_stride + t * kBK;
-    const int kb = t * kBK;
-#pragma unroll
-    for (int h = 0; h < kHalves; ++h) {
-      if (CL == 1 || crank == 0) tma_prefetch_l2_2d(&tmA, ka + h * kBKHalf, m0);
-      tma_prefetch_l2_3d(&tmB, kb + h * kBKHalf, bcol, q);
-    }
-    if constexpr (MODE == kZ3M) {
-      if (CL == 1 || crank == 0) tma_prefetch_l2_2d(&tmA3, q * p.a3_rank_stride + t * (kBK / 2), m0);
-      tma_prefetch_l2_3d(&tmB3, kb / 2, bcol, q);
-    }
-  };
   auto produce = [&]() {  // load iteration pc_j into stage pc_stage, then advance the cursor
     load_stage(pc_tile, pc_kt, pc_stage);
-    if (p.l2_prefetch > 0 && pc_j + p.l2_prefetch < my_iters) prefetch_l2(pc_j + p.l2_prefetch);
     ++pc_j;
     if (++pc_stage == STAGES) pc_stage = 0;
     if (++pc_kt == KT) {
@@ -320,12 +293,6 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       }
     }
   };
-  // load CTA-local iteration jj into stage st (last-arriver mode: position from the iteration index)
-  auto produce_at = [&](int64_t jj, int st) {
-    int T, kt;
-    coords(jj, T, kt);
-    load_stage(T, kt, st);
-  };
   if (threadIdx.x == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
@@ -337,11 +304,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     pc_stage = 0;
     pc_dp_left = p.dp_units;
     pc_init();
-    if (p.refill_mode == 0) {
-      while (pc_j < STAGES && pc_j < my_iters) produce();
-    } else {
-      for (int64_t jj = 0; jj < STAGES && jj < my_iters; ++jj) produce_at(jj, (int)jj);
-    }
+    while (pc_j < STAGES && pc_j < my_iters) produce();
   }
 
   const int wm = warp % Cfg::kWarpsM;
@@ -594,29 +557,19 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
         }
       }
       __syncwarp();
-      if (CL > 1 || p.refill_mode == 0) {
-        if (lane == 0) {
-          if constexpr (CL == 1) {
-            mbar_arrive(&empty[s]);
-          } else {  // release the stage in both CTAs: either may multicast into it next
+      if (lane == 0) {
+        if constexpr (CL == 1) {
+          mbar_arrive(&empty[s]);
+        } else {  // release the stage in both CTAs: either may multicast into it next
 #pragma unroll
-            for (int q = 0; q < CL; ++q) mbar_arrive_cluster(&empty[s], (uint32_t)q);
-          }
+          for (int q = 0; q < CL; ++q) mbar_arrive_cluster(&empty[s], (uint32_t)q);
         }
-        // refill the stage of iteration j - 1 (stage pc_stage, phase of j - 1) with iteration pc_j
-        if (threadIdx.x == 0 && j >= 1 && *(volatile int64_t*)&pc_j < my_iters) {
-          const uint32_t prev_phase = (s == 0) ? (phase ^ 1u) : phase;
-          mbar_wait(&empty[pc_stage], prev_phase);
-          produce();
-        }
-      } else if (lane == 0) {
-        // last-arriver refill: the warp that releases stage s last loads iteration j + STAGES into it,
-        // so no warp ever blocks on a release (the count grows by kConsumerWarps per use of the stage)
-        const int old = atomicAdd(&refill_cnt[s], 1);
-        if (old % Cfg::kConsumerWarps == Cfg::kConsumerWarps - 1 && j + STAGES < my_iters) {
-          fence_proxy_async_shared();
-          produce_at(j + STAGES, s);
-        }
+      }
+      // refill the stage of iteration j - 1 (stage pc_stage, phase of j - 1) with iteration pc_j
+      if (threadIdx.x == 0 && j >= 1 && *(volatile int64_t*)&pc_j < my_iters) {
+        const uint32_t prev_phase = (s == 0) ? (phase ^ 1u) : phase;
+        mbar_wait(&empty[pc_stage], prev_phase);
+        produce();
       }
       if (++stage == STAGES) {
         stage = 0;
