@@ -167,6 +167,34 @@ __global__ void scale_kernel(int64_t rows, double2* x, double s) {
   }
 }
 
+// Lanczos step on the device (no host round trip): beta = sqrt(||w||^2), v_next = w / beta (nullable),
+// alpha = Re(coef_j) (nullable); beta and alpha land in the step's slots of the device arrays
+template <typename D>
+__global__ void lanczos_next_kernel(int64_t rows, const D* __restrict__ w, D* __restrict__ vn, const double* nrm2,
+                                    const D* coef_j, double* beta_out, double* alpha_out) {
+  const double beta = sqrt(*nrm2);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *beta_out = beta;
+    if (alpha_out) {
+      if constexpr (sizeof(D) == 16) {
+        *alpha_out = reinterpret_cast<const double2*>(coef_j)->x;
+      } else {
+        *alpha_out = *reinterpret_cast<const double*>(coef_j);
+      }
+    }
+  }
+  if (!vn) return;
+  const double s = 1.0 / beta;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    if constexpr (sizeof(D) == 16) {
+      const double2 a = reinterpret_cast<const double2*>(w)[r];
+      reinterpret_cast<double2*>(vn)[r] = make_double2(a.x * s, a.y * s);
+    } else {
+      reinterpret_cast<double*>(vn)[r] = reinterpret_cast<const double*>(w)[r] * s;
+    }
+  }
+}
+
 __global__ void orth_err_kernel(int64_t k, const double2* G, int64_t ldg, unsigned long long* out) {
   const int64_t j = blockIdx.y;
   double m = 0;
@@ -418,6 +446,18 @@ cudaError_t launch_pack_y3(int64_t rows, int64_t cols, const double2* X, int64_t
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   const unsigned bx = (unsigned)std::min<int64_t>((rows + 255) / 256, 64);
   pack_y3_kernel<<<dim3(bx, (unsigned)cols), 256, 0, st>>>(rows, X, ldx, dst, cs, y3_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lanczos_next(int64_t rows, const double2* w, double2* vn, const double* nrm2, const double2* coef_j,
+                                double* beta_out, double* alpha_out, cudaStream_t st) {
+  lanczos_next_kernel<double2><<<grid1(rows, 256), 256, 0, st>>>(rows, w, vn, nrm2, coef_j, beta_out, alpha_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lanczos_next(int64_t rows, const double* w, double* vn, const double* nrm2, const double* coef_j,
+                                double* beta_out, double* alpha_out, cudaStream_t st) {
+  lanczos_next_kernel<double><<<grid1(rows, 256), 256, 0, st>>>(rows, w, vn, nrm2, coef_j, beta_out, alpha_out);
   return cudaGetLastError();
 }
 

@@ -44,6 +44,14 @@ cudaError_t launch_h3_plane(int64_t n, int64_t nloc, const double2* Hp, int64_t 
 cudaError_t launch_pack_y3(int64_t rows, int64_t cols, const double2* X, int64_t ldx, double* dst, int64_t cs,
                            int64_t y3_off, cudaStream_t st);
 
+// one Lanczos step finished on the device: beta = sqrt(*nrm2), vn = w / beta (vn nullable), alpha =
+// Re(*coef_j) (alpha_out nullable); *beta_out, *alpha_out written (device) -- the host reads all steps'
+// scalars once
+cudaError_t launch_lanczos_next(int64_t rows, const double2* w, double2* vn, const double* nrm2, const double2* coef_j,
+                                double* beta_out, double* alpha_out, cudaStream_t st);
+cudaError_t launch_lanczos_next(int64_t rows, const double* w, double* vn, const double* nrm2, const double* coef_j,
+                                double* beta_out, double* alpha_out, cudaStream_t st);
+
 // ---- real-symmetric (NEXT-3) counterparts, same semantics on double data ----
 cudaError_t launch_hemv(int64_t n, int64_t nloc, const double* Hp, int64_t ldh, const double* v, double* w,
                         cudaStream_t st);

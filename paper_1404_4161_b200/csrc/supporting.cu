@@ -208,14 +208,15 @@ chfsi_status lanczos_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
   const int p = ctx->nranks;
   const int64_t ldv = nloc;
   TRY(ensure(ctx, ctx->lz, sizeof(D) * ((size_t)ldv * (steps + 1) + (size_t)n + (size_t)nloc)));
-  TRY(ensure(ctx, ctx->small3, sizeof(double) * 2 * (size_t)(steps + 8)));
+  TRY(ensure(ctx, ctx->small3, sizeof(double) * (2 * (size_t)(steps + 8) + 2 * (size_t)steps + 8)));
   D* V = static_cast<D*>(ctx->lz.ptr);
   D* vfull = V + (size_t)ldv * (steps + 1);
   D* w = vfull + n;
   D* coef = static_cast<D*>(ctx->small3.ptr);
   double* nrm = static_cast<double*>(ctx->small3.ptr) + 2 * (steps + 2);
+  double* dalpha = nrm + 8;             // alpha_j, beta_j of every step stay on the device until the end
+  double* dbeta = dalpha + steps;
   std::vector<double> al(steps), be(steps);
-  std::vector<T> hcoef(steps + 2);
   for (int restart = 0; restart <= 3; ++restart) {
     CHFSI_CUDA_TRY(ctx, launch_random_block(nloc, 1, row0, seed, (4ull << 16) | (uint64_t)restart, 0, V, ldv,
                                             ctx->stream));
@@ -228,10 +229,10 @@ chfsi_status lanczos_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
     CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     CHFSI_CUDA_TRY(ctx, launch_scale(nloc, V, 1.0 / std::sqrt(h), ctx->stream));
     ctx->launches++;
-    double hest = 0;
-    bool broke = false;
-    int j = 0;
-    for (; j < steps; ++j) {
+    // the steps run without host round trips: beta_j = ||w||, v_{j+1} = w / beta_j and alpha_j are formed
+    // on the device; the breakdown test (beta_j < 1e-14 ||T||_est) runs on the host afterwards, and a
+    // breakdown discards the (then meaningless) later steps and restarts
+    for (int j = 0; j < steps; ++j) {
       D* vj = V + (size_t)j * ldv;
       const D* vin = vj;
       if (p > 1) {
@@ -246,30 +247,29 @@ chfsi_status lanczos_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
         CUBLAS_TRY(ctx, S::gemv(ctx->cublas, S::opH, (int)nloc, j + 1, &one, reinterpret_cast<const T*>(V), (int)ldv,
                                 reinterpret_cast<const T*>(w), &zero, reinterpret_cast<T*>(coef)));
         TRY(comm_allreduce_sum(ctx, reinterpret_cast<double*>(coef), (size_t)S::elem * (j + 1)));
-        if (pass == 0) {
-          CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(hcoef.data(), coef, sizeof(T) * (j + 1), cudaMemcpyDeviceToHost,
+        if (pass == 0)  // alpha_j = Re(v_j^H H v_j) from the first pass
+          CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(dalpha + j, coef + j, sizeof(double), cudaMemcpyDeviceToDevice,
                                               ctx->stream));
-        }
         CUBLAS_TRY(ctx, S::gemv(ctx->cublas, CUBLAS_OP_N, (int)nloc, j + 1, &mone, reinterpret_cast<const T*>(V),
                                 (int)ldv, reinterpret_cast<const T*>(coef), &one, reinterpret_cast<T*>(w)));
       }
       CHFSI_CUDA_TRY(ctx, launch_colnorm2(nloc, 1, w, nloc, nrm, ctx->stream));
       ctx->launches++;
       TRY(comm_allreduce_sum(ctx, nrm, 1));
-      CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&h, nrm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-      CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-      al[j] = S::re(hcoef[j]);  // alpha_j = Re(v_j^H H v_j)
-      be[j] = std::sqrt(h);
+      D* vn = j + 1 < steps ? V + (size_t)(j + 1) * ldv : nullptr;
+      CHFSI_CUDA_TRY(ctx, launch_lanczos_next(nloc, w, vn, nrm, nullptr, dbeta + j, nullptr, ctx->stream));
+      ctx->launches++;
+    }
+    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(al.data(), dalpha, sizeof(double) * steps, cudaMemcpyDeviceToHost, ctx->stream));
+    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(be.data(), dbeta, sizeof(double) * steps, cudaMemcpyDeviceToHost, ctx->stream));
+    CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    double hest = 0;
+    bool broke = false;
+    for (int j = 0; j < steps; ++j) {
       hest = std::max(hest, std::fabs(al[j]) + be[j] + (j > 0 ? be[j - 1] : 0.0));
-      if (j + 1 < steps) {
-        if (be[j] < 1e-14 * hest) {
-          broke = true;
-          break;
-        }
-        D* vn = V + (size_t)(j + 1) * ldv;
-        CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(vn, w, sizeof(D) * nloc, cudaMemcpyDeviceToDevice, ctx->stream));
-        CHFSI_CUDA_TRY(ctx, launch_scale(nloc, vn, 1.0 / be[j], ctx->stream));
-        ctx->launches++;
+      if (j + 1 < steps && be[j] < 1e-14 * hest) {
+        broke = true;
+        break;
       }
     }
     if (broke) continue;

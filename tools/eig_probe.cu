@@ -47,15 +47,27 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int alg = 0; alg < 2; ++alg) {
+  // 64-bit generic API (cusolverDnXsyevd) with the same matrix
+  cusolverDnParams_t xp;
+  cusolverDnCreateParams(&xp);
+  size_t xdev = 0, xhost = 0;
+  cusolverDnXsyevd_bufferSize(h, xp, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, k, CUDA_C_64F, dA, k, CUDA_R_64F,
+                              dW, CUDA_C_64F, &xdev, &xhost);
+  void* xwork = nullptr;
+  cudaMalloc(&xwork, xdev > 0 ? xdev : 1);
+  std::vector<char> hwork(xhost > 0 ? xhost : 1);
+  for (int alg = 0; alg < 3; ++alg) {
     float best = 1e30f;
     for (int rep = 0; rep < 5; ++rep) {
       cudaMemcpy(dA, dG, sizeof(cuDoubleComplex) * k * k, cudaMemcpyDeviceToDevice);
       cudaEventRecord(e0);
       if (alg == 0)
         cusolverDnZheevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, k, dA, k, dW, work, lwd, info);
-      else
+      else if (alg == 1)
         cusolverDnZheevj(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, k, dA, k, dW, work, lwj, info, params);
+      else
+        cusolverDnXsyevd(h, xp, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, k, CUDA_C_64F, dA, k, CUDA_R_64F, dW,
+                         CUDA_C_64F, xwork, xdev, hwork.data(), xhost, info);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -71,7 +83,7 @@ int main(int argc, char** argv) {
       cusolverDnXsyevjGetResidual(h, params, &res);
     }
     printf("{\"k\": %d, \"coupling\": %g, \"alg\": \"%s\", \"ms\": %.3f, \"info\": %d, \"sweeps\": %d, \"residual\": %.3g}\n",
-           k, coupling, alg == 0 ? "zheevd" : "zheevj", best, hinfo, sweeps, res);
+           k, coupling, alg == 0 ? "zheevd" : alg == 1 ? "zheevj" : "Xsyevd", best, hinfo, sweeps, res);
   }
   return 0;
 }
