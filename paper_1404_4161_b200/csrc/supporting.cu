@@ -5,6 +5,7 @@
 // n^2 k contractions (H Q) run on the K1 kernel; n k^2 / k^3 pieces are plain library calls
 // (cuBLAS ZGEMM/ZTRSM, cuSOLVER ZPOTRF/ZHEEVD/ZGEQRF/ZUNGQR); small reductions are the library's
 // own kernels (small_kernels.cu). Every k x k reduction across ranks is an NCCL allreduce.
+#include <cstdio>
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -425,6 +426,24 @@ chfsi_status rr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const vo
   TRY(gram<T>(ctx, nloc, ka, ka, Q, ldq, W, nloc, G, ka));
   CHFSI_CUDA_TRY(ctx, launch_hermitize(ka, reinterpret_cast<D*>(G), ka, ctx->stream));
   ctx->launches++;
+  // diagnostics (CHFSI_RR_LOG): how far the projected matrix is from diagonal (relative Frobenius mass of
+  // the off-diagonal part), the quantity a Jacobi-type eigensolver would have to remove
+  static const bool rr_log = getenv("CHFSI_RR_LOG") != nullptr;
+  if (rr_log && ctx->rank == 0) {
+    std::vector<T> hg((size_t)ka * ka);
+    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(hg.data(), G, sizeof(T) * hg.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    double off = 0, tot = 0, offmax = 0;
+    for (int64_t j = 0; j < ka; ++j)
+      for (int64_t i = 0; i < ka; ++i) {
+        const T& g = hg[(size_t)j * ka + i];
+        double a2;
+        if constexpr (S::elem == 2) a2 = g.x * g.x + g.y * g.y; else a2 = g * g;
+        tot += a2;
+        if (i != j) off += a2, offmax = std::max(offmax, std::sqrt(a2));
+      }
+    fprintf(stderr, "rr k %lld offdiag_rel %.3e offdiag_max %.3e\n", (long long)ka, std::sqrt(off / tot), offmax);
+  }
   // small dense eigensolve: once, on rank 0, broadcast (identical bits on every rank)
   if (ctx->rank == 0) {
     int lw = 0;
