@@ -63,3 +63,31 @@ def test_solve_c2_first_problem(gpu_lib, c2):
     sample = [0, 1, nev // 2, nev - 2, nev - 1]
     res = O.residuals(H, X[:, sample], lam[sample], HNORM)  # ||H x - lam x|| / ||H||_2, naive
     assert res.max() <= cf["tol"]
+
+
+def test_filter_c3_full_width(gpu_lib):
+    """c3 size (n = 30000, k = 1440 = 1200 + 240, degree cap 40): the filter on H^(1) against the
+    compact-WY closed form on every column (App. A) and the oracle's Alg 2 on two sampled columns."""
+    cf = CONFIGS["c3"]
+    n, k = cf["n"], cf["nev"] + cf["nex"]
+    w = G.wy(n, cf["nd"], cf["seed"])
+    rng = np.random.default_rng(3)
+    deg = sorted(rng.integers(1, cf["cap"] + 1, k).tolist())
+    Y0 = G.start_basis(n, k, cf["seed"])
+    l1, a, b = w.lam[0] - 0.02, w.lam[k], 48.0
+    c, e = (a + b) / 2, (b - a) / 2
+    ctx = gpu_lib.Context(0)
+    H = w.full()
+    Hd = gpu_lib.to_colmajor(H)
+    Yd = gpu_lib.to_colmajor(Y0)
+    assert ctx.filter(Hd, Yd, deg, l1, c, e) == sum(deg)
+    Y = Yd.cpu().numpy()
+    del Hd, Yd
+    ctx.close()
+    Yc = O.filter_wy_closed(w, Y0, deg, l1, c, e)
+    rel = np.linalg.norm(Y - Yc, axis=0) / np.linalg.norm(Yc, axis=0)
+    assert rel.max() <= 1e-11, (rel.max(), int(np.argmax(rel)))
+    cols = [0, k - 1]
+    Yo, _ = O.chebyshev_filter(H, Y0[:, cols], [deg[j] for j in cols], l1, c, e)
+    rel = np.linalg.norm(Y[:, cols] - Yo, axis=0) / np.linalg.norm(Yo, axis=0)
+    assert rel.max() <= 1e-11
