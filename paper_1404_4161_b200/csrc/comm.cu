@@ -214,7 +214,10 @@ chfsi_status comm_barrier(chfsi_ctx ctx, cudaStream_t st) {
     lg_exit(ctx, st);
     return CHFSI_OK;
   }
-  if (!ctx->comm->scratch) CHFSI_CUDA_TRY(ctx, cudaMalloc(&ctx->comm->scratch, sizeof(double) * 8));
+  if (!ctx->comm->scratch) {  // one zeroed word: the barrier reduces zeros (the value is never read)
+    CHFSI_CUDA_TRY(ctx, cudaMalloc(&ctx->comm->scratch, sizeof(double) * 8));
+    CHFSI_CUDA_TRY(ctx, cudaMemsetAsync(ctx->comm->scratch, 0, sizeof(double) * 8, st));
+  }
   return nccl_check(ctx, ctx->comm->allreduce(ctx->comm->scratch, ctx->comm->scratch, 1, ncclDouble, ncclSum,
                                               ctx->comm->comm, st),
                     "ncclAllReduce (barrier)");
