@@ -98,7 +98,7 @@ chfsi_status make_tmap_3d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64
 static inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 chfsi_status sk_workspace(chfsi_ctx ctx, const TileChoice& t, StepParams& p) {
-  const size_t tick_bytes = 4096;  // >= num_sms ints
+  const size_t tick_bytes = sizeof(int) * kMaxTailTickets;  // >= tail tiles x cluster ranks (schedule_filter_step)
   const size_t need = tick_bytes + sizeof(double) * filter_partials_doubles(t, ctx->num_sms);
   void* old = ctx->sk.ptr;
   chfsi_status st = ensure(ctx, ctx->sk, need);

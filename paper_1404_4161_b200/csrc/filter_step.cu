@@ -177,7 +177,17 @@ void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
   const int64_t grid = iters < slots ? iters : slots;
   p.tiles_n = (int32_t)tn;
   p.grid = (int32_t)grid;
-  p.dp_units = (int32_t)(tiles / grid);
+  int64_t dp = tiles / grid;
+  const int64_t rem = tiles - dp * grid;
+  // Small remainder: the rem tail tiles would each be split over grid / rem contributors, and the last
+  // of them sums all their partial accumulators serially (measured: 74 contributors cost 133 us on a
+  // 1.5 ms step). Folding one data-parallel wave into the stream-K tail gives every CTA 1..1.5 tiles of
+  // tail work, so a tail tile has at most two contributors (DP + "two-tile" stream-K hybrid).
+  // CHFSI_SK_HYBRID=0 turns it off (A/B and test hook, read per call).
+  const char* hy = getenv("CHFSI_SK_HYBRID");
+  const bool hybrid = !(hy && hy[0] == '0');
+  if (hybrid && dp >= 1 && rem > 0 && 2 * rem < grid && (rem + grid) * cl <= kMaxTailTickets) --dp;
+  p.dp_units = (int32_t)dp;
   p.tail_tile0 = (int32_t)(p.dp_units * grid);
   p.tail_iters = (tiles - p.tail_tile0) * p.num_kt;
 }

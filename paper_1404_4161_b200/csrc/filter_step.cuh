@@ -18,6 +18,9 @@
 
 namespace chfsi {
 
+// stream-K tickets in the workspace (one int per tail tile and cluster rank)
+constexpr int64_t kMaxTailTickets = 1024;
+
 struct StepParams {
   int64_t nrows;        // output rows (nloc)
   int32_t num_kt;       // k-tiles per output tile (32 real = 16 complex contraction entries each)

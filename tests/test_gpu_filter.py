@@ -211,3 +211,34 @@ def test_filter_degree_extremes(gpu_lib, ctx, deg_kind):
     Y = run_filter(gpu_lib, ctx, np.diag(d.astype(complex)), Y0, deg, l1, c, e)
     Yc = O.filter_diag_closed(d, Y0, deg, l1, c, e)
     assert colrel(Y, Yc).max() <= 1e-13
+
+
+@pytest.mark.parametrize("env,vid,mults", [("CHFSI_FILTER_VARIANT_Z3", "200", 3), ("CHFSI_FILTER_VARIANT", "7", 4)])
+def test_filter_stream_k_hybrid_schedule(gpu_lib, ctx, env, vid, mults):
+    """Persistent schedule with a small stream-K remainder: n = 2000, k = 480 under a 128 x 48 tile is
+    16 x 10 = 160 tiles on 148 CTAs (remainder 12 < 148 / 2). The default schedule folds one
+    data-parallel wave into the stream-K tail (12 + 148 tail tiles, at most two contributors each);
+    CHFSI_SK_HYBRID=0 keeps the plain split (12 tail tiles over all 148 CTAs). Both within the filter
+    tolerance of the compact-WY closed form (App. A) and of each other (they only re-associate the k sum)."""
+    n, k = 2000, 480
+    w = G.wy(n, int(0.9 * n), 31)
+    H = w.full()
+    rng = np.random.default_rng(31)
+    deg = sorted(rng.integers(2, 9, k).tolist())
+    Y0 = crand(rng, n, k)
+    l1, a, b = w.lam[0] - 0.05, w.lam[k], 45.0
+    c, e = (a + b) / 2, (b - a) / 2
+    ctx.set_complex_mult(mults)
+    out = {}
+    os.environ[env] = vid
+    try:
+        for hy in ("1", "0"):
+            os.environ["CHFSI_SK_HYBRID"] = hy
+            out[hy] = run_filter(gpu_lib, ctx, H, Y0, deg, l1, c, e)
+    finally:
+        os.environ.pop(env, None)
+        os.environ.pop("CHFSI_SK_HYBRID", None)
+    Yc = O.filter_wy_closed(w, Y0, deg, l1, c, e)
+    for hy in ("1", "0"):
+        assert colrel(out[hy], Yc).max() <= 1e-11
+    assert colrel(out["1"], out["0"]).max() <= 1e-13
