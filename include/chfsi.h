@@ -184,6 +184,28 @@ chfsi_status chfsi_reduce_generalized(chfsi_ctx ctx, int64_t n, void* A, int64_t
  * result is B-orthonormal when X is orthonormal. Single rank only. */
 chfsi_status chfsi_back_transform(chfsi_ctx ctx, int64_t n, const void* L, int64_t ldl, void* X,
                                   int64_t ldx, int64_t k);
+/* Row-panel form of chfsi_reduce_generalized for any nranks >= 1 (collective: every rank
+ * calls it with its own panel; nloc * nranks == n, row0 == rank * nloc, as for chfsi_filter).
+ * Ap (in/out, device n x nloc, lda >= n): in, the column slab A[:, row0:row0+nloc]; out, the slab
+ * Hp = H[:, row0:row0+nloc] of H = L^{-1} A L^{-H}, ready for chfsi_filter / chfsi_solve_sequence with
+ * the same (n, row0, nloc). The assembled H is Hermitian bit for bit across the ranks (R13).
+ * Bp (in, device n x nloc, ldb >= n): the column slab B[:, row0:row0+nloc] of the Hermitian positive
+ * definite B; not modified. L (out, device n x n, ldl >= n, caller-owned): the full Cholesky factor
+ * B = L L^H in its lower triangle (identical on every rank: factored once on rank 0 and broadcast; the
+ * strict upper triangle holds B's), for chfsi_back_transform_panel.
+ * Work: B and A gathered on every rank (two n x n scratch uses of 16 n^2 bytes), ZPOTRF (n^3 / 3, rank 0),
+ * 2 ZTRSM + 1 ZGEMM with nloc right-hand sides per rank. Errors: CHFSI_ERR_ARG (dims / panel,
+ * B not positive definite -- returned by every rank, pivot in chfsi_last_error), CHFSI_ERR_CUDA,
+ * CHFSI_ERR_NCCL, CHFSI_ERR_NOMEM. */
+chfsi_status chfsi_reduce_generalized_panel(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, void* Ap,
+                                            int64_t lda, const void* Bp, int64_t ldb, void* L, int64_t ldl);
+/* Row-panel back-transformation, collective: X (in/out, device nloc x k, ldx >= nloc) holds this
+ * rank's rows of eigenvectors y of H; on return its rows of c = L^{-H} y. L as returned by
+ * chfsi_reduce_generalized_panel (any rank's copy). The k columns are gathered on every rank and solved
+ * whole (n^2 k per rank, about one filter step). k <= n. Errors: CHFSI_ERR_ARG, CHFSI_ERR_CUDA,
+ * CHFSI_ERR_NCCL, CHFSI_ERR_NOMEM. */
+chfsi_status chfsi_back_transform_panel(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* L,
+                                        int64_t ldl, void* X, int64_t ldx, int64_t k);
 
 typedef struct {
   int32_t nev, nex;      /* wanted eigenpairs and extra buffer columns, k = nev + nex <= n; nex >= 1

@@ -27,7 +27,8 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_NOCONV", 4: "ERR_QR
 EXPORTS = ("chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_ctx_create_nccl", "chfsi_nccl_unique_id", "chfsi_ctx_reserve", "chfsi_ctx_destroy",
            "chfsi_last_error", "chfsi_kernel_launches", "chfsi_ctx_set_pipeline", "chfsi_ctx_set_complex_mult", "chfsi_ctx_set_exchange", "chfsi_local_group_create", "chfsi_local_group_destroy",
            "chfsi_filter", "chfsi_filter_real", "chfsi_lanczos_bounds", "chfsi_qr", "chfsi_rayleigh_ritz", "chfsi_solve_sequence",
-           "chfsi_reduce_generalized", "chfsi_back_transform", "chfsi_solve_batch", "chfsi_solve_sequence_real")
+           "chfsi_reduce_generalized", "chfsi_back_transform", "chfsi_reduce_generalized_panel", "chfsi_back_transform_panel",
+           "chfsi_solve_batch", "chfsi_solve_sequence_real")
 
 
 class ChfsiError(RuntimeError):
@@ -112,10 +113,13 @@ def lib():
                                            ctypes.POINTER(Report)]
         L.chfsi_reduce_generalized.argtypes = [vp, i64, vp, i64, vp, i64]
         L.chfsi_back_transform.argtypes = [vp, i64, vp, i64, vp, i64, i64]
+        L.chfsi_reduce_generalized_panel.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, vp, i64]
+        L.chfsi_back_transform_panel.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, i64]
         L.chfsi_solve_sequence_real.argtypes = L.chfsi_solve_sequence.argtypes
         L.chfsi_solve_sequence_real.restype = ctypes.c_int
         L.chfsi_solve_batch.argtypes = [i32, i32, i64, ctypes.POINTER(Opts), ctypes.POINTER(Sequence), i32]
-        for name in ("chfsi_solve_batch", "chfsi_reduce_generalized", "chfsi_back_transform", "chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_local_group_create", "chfsi_ctx_reserve", "chfsi_filter", "chfsi_lanczos_bounds", "chfsi_qr",
+        for name in ("chfsi_solve_batch", "chfsi_reduce_generalized", "chfsi_back_transform",
+                     "chfsi_reduce_generalized_panel", "chfsi_back_transform_panel", "chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_local_group_create", "chfsi_ctx_reserve", "chfsi_filter", "chfsi_lanczos_bounds", "chfsi_qr",
                      "chfsi_rayleigh_ritz", "chfsi_solve_sequence"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
@@ -321,6 +325,24 @@ class Context:
         lp, ldl = _mat(L, n, n, "L")
         xp, ldx = _mat(X, n, k, "X")
         self._check(lib().chfsi_back_transform(self.h, n, lp, ldl, xp, ldx, k))
+
+    def reduce_generalized_panel(self, Ap, Bp, L, n=None, row0=0):
+        """Row-panel form (collective): Ap (n x nloc) <- this rank's slab of H = L^{-1} A L^{-H};
+        Bp (n x nloc) is read only; L (n x n) <- the full Cholesky factor (lower triangle)."""
+        n = n or Ap.shape[0]
+        nloc = Ap.shape[1]
+        ap, lda = _mat(Ap, n, nloc, "Ap")
+        bp, ldb = _mat(Bp, n, nloc, "Bp")
+        lp, ldl = _mat(L, n, n, "L")
+        self._check(lib().chfsi_reduce_generalized_panel(self.h, n, row0, nloc, ap, lda, bp, ldb, lp, ldl))
+
+    def back_transform_panel(self, L, X, n=None, row0=0):
+        """Row-panel back-transformation (collective): X (this rank's nloc x k rows) <- its rows of L^{-H} X."""
+        nloc, k = X.shape
+        n = n or L.shape[0]
+        lp, ldl = _mat(L, n, n, "L")
+        xp, ldx = _mat(X, nloc, k, "X")
+        self._check(lib().chfsi_back_transform_panel(self.h, n, row0, nloc, lp, ldl, xp, ldx, k))
 
     # -- Alg 1 over a sequence ----------------------------------------------------------------------
     def solve_sequence(self, get_h, nprob, X, nev, nex, tol, deg_cap=40, deg0=8, max_loops=50, lanczos_steps=25,

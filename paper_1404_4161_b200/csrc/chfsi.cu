@@ -667,7 +667,7 @@ void chfsi_ctx_destroy(chfsi_ctx ctx) {
   comm_destroy(ctx);
   DevBuf* bufs[] = {&ctx->h3, &ctx->L0, &ctx->L1, &ctx->R0, &ctx->R1, &ctx->flag, &ctx->sk, &ctx->hpad, &ctx->w1, &ctx->w2, &ctx->w3, &ctx->w4,
                     &ctx->small1, &ctx->small2, &ctx->small3, &ctx->solver_ws, &ctx->devinfo, &ctx->lz,
-                    &ctx->ya,    &ctx->xl,     &ctx->tb,     &ctx->idx};
+                    &ctx->ya,    &ctx->xl,     &ctx->tb,     &ctx->idx,    &ctx->gw,     &ctx->gx};
   for (DevBuf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   for (cudaEvent_t ev : ctx->k1_events) cudaEventDestroy(ev);

@@ -11,7 +11,7 @@
          vs concurrently by chfsi_solve_batch with W worker contexts on one GPU; aggregate throughput.
 
 Inputs are built on the GPU with torch where the product is large (input construction only; the solves
-go through the C-ABI). Usage: python tools/bench_next.py [next1] [next3] [next4] (default: all)."""
+go through the C-ABI). Usage: python tools/bench_next.py [next1] [next1p] [next3] [next4] (default: all)."""
 import json
 import os
 import sys
@@ -72,6 +72,38 @@ def next1(cf):
                       "reduce_share": t_red / (t_red + t_solve + t_back), "loops": rep["loops"],
                       "max_rel_eig_err_vs_exact": err, "max_resid_over_tol": float(np.max(out["resid"][0]) / cf["tol"]),
                       "input_gen_s": gen_s}), flush=True)
+
+
+def next1_panel(cf):
+    """NEXT-1 through the row-panel entry points at p = 1 (chfsi_reduce_generalized_panel: ZPOTRF, then
+    L^{-H} E, A X, L^{-1}(A X) and the cross-slab hermitisation; chfsi_back_transform_panel)."""
+    n, nev, nex = cf["n"], cf["nev"], cf["nex"]
+    w = G.wy(n, cf["nd"], cf["seed"])
+    M = torch.as_tensor(G.lower_factor(n, cf["seed"] + 7, 0.5)).cuda()
+    H1 = torch.as_tensor(w.full()).cuda()
+    A = M @ H1 @ M.conj().t()
+    B = M @ M.conj().t()
+    Ad, Bd = chfsi.colmajor(n, n), chfsi.colmajor(n, n)
+    Ad.copy_((A + A.conj().t()) / 2)
+    Bd.copy_((B + B.conj().t()) / 2)
+    del A, B, H1, M
+    torch.cuda.empty_cache()
+    Ld = chfsi.colmajor(n, n)
+    ctx = chfsi.Context(0)
+    ctx.reserve(n, n, nev + nex)
+    _, t_red = ev_time(lambda: ctx.reduce_generalized_panel(Ad, Bd, Ld))
+    Xd = chfsi.to_colmajor(G.start_basis(n, nev + nex, cf["seed"]))
+    out, t_solve = ev_time(lambda: ctx.solve_sequence(lambda ell: Ad, 1, Xd, nev, nex, cf["tol"], deg_cap=cf["cap"],
+                                                      seed=cf["seed"]))
+    C = Xd[:, :nev].contiguous().t().contiguous().t()
+    _, t_back = ev_time(lambda: ctx.back_transform_panel(Ld, C))
+    ctx.close()
+    lam = out["lam"][0]
+    print(json.dumps({"row": "NEXT-1 generalised, row-panel entry points (p = 1)", "n": n, "nev": nev, "nex": nex,
+                      "status": out["status"], "t_reduce_s": t_red, "t_solve_s": t_solve, "t_back_transform_s": t_back,
+                      "loops": out["reports"][0]["loops"],
+                      "max_rel_eig_err_vs_exact": float(np.max(np.abs(lam - w.lam[:nev]) / np.abs(w.lam[:nev]))),
+                      "max_resid_over_tol": float(np.max(out["resid"][0]) / cf["tol"])}), flush=True)
 
 
 def real_sym_known(n, nd, seed):
@@ -151,9 +183,11 @@ def next4(cf, S=8, nprob=3, workers=(1, 2, 4)):
 
 
 def main():
-    which = set(sys.argv[1:]) or {"next1", "next3", "next4"}
+    which = set(sys.argv[1:]) or {"next1", "next1p", "next3", "next4"}
     if "next1" in which:
         next1(CONFIGS["c2"])
+    if "next1p" in which:
+        next1_panel(CONFIGS["c2"])
     if "next3" in which:
         next3(CONFIGS["c2"])
     if "next4" in which:
