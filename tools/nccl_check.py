@@ -63,6 +63,23 @@ def main():
         if rank == 0:
             print(json.dumps({"case": "solve", "exchange": mode, "world": world, "status": out["status"],
                               "max_rel_eig_err": err}), flush=True)
+        if mode == 0:  # NEXT-1 on row panels: reduce, back-transform (collectives over the same communicator)
+            A, B, _ = G.generalized_pair(w, 2)
+            cols = slice(rank * nloc, (rank + 1) * nloc)
+            Ap = chfsi.to_colmajor(np.asfortranarray(A[:, cols]))
+            Bp = chfsi.to_colmajor(np.asfortranarray(B[:, cols]))
+            Ld = chfsi.colmajor(n, n)
+            ctx.reduce_generalized_panel(Ap, Bp, Ld, n=n, row0=rank * nloc)
+            parts = [torch.empty_like(Ap) for _ in range(world)]
+            dist.all_gather(parts, Ap.contiguous())
+            if rank == 0:
+                Hg = np.concatenate([q.cpu().numpy() for q in parts], axis=1)
+                Ho, _ = O.reduce_generalized(A, B)
+                herr = float(np.abs(Hg - Ho).max())
+                herm = bool(np.array_equal(Hg, Hg.conj().T))
+                ok &= herr <= 1e-11 and herm
+                print(json.dumps({"case": "reduce_generalized_panel", "world": world, "max_abs_err": herr,
+                                  "exactly_hermitian": herm}), flush=True)
         ctx.close()
     dist.barrier()
     dist.destroy_process_group()
