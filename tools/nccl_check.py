@@ -70,10 +70,11 @@ def main():
             Bp = chfsi.to_colmajor(np.asfortranarray(B[:, cols]))
             Ld = chfsi.colmajor(n, n)
             ctx.reduce_generalized_panel(Ap, Bp, Ld, n=n, row0=rank * nloc)
-            parts = [torch.empty_like(Ap) for _ in range(world)]
-            dist.all_gather(parts, Ap.contiguous())
+            At = Ap.t().contiguous()
+            parts = [torch.empty_like(At) for _ in range(world)]
+            dist.all_gather(parts, At)
             if rank == 0:
-                Hg = np.concatenate([q.cpu().numpy() for q in parts], axis=1)
+                Hg = np.concatenate([q.t().cpu().numpy() for q in parts], axis=1)
                 Ho, _ = O.reduce_generalized(A, B)
                 herr = float(np.abs(Hg - Ho).max())
                 herm = bool(np.array_equal(Hg, Hg.conj().T))
