@@ -213,13 +213,16 @@ def test_filter_degree_extremes(gpu_lib, ctx, deg_kind):
     assert colrel(Y, Yc).max() <= 1e-13
 
 
-@pytest.mark.parametrize("env,vid,mults", [("CHFSI_FILTER_VARIANT_Z3", "200", 3), ("CHFSI_FILTER_VARIANT", "7", 4)])
+@pytest.mark.parametrize("env,vid,mults", [("CHFSI_FILTER_VARIANT_Z3", "200", 3), ("CHFSI_FILTER_VARIANT", "7", 4),
+                                           ("CHFSI_FILTER_VARIANT_Z3", "210", 3), ("CHFSI_FILTER_VARIANT_Z3", "206", 3)])
 def test_filter_stream_k_hybrid_schedule(gpu_lib, ctx, env, vid, mults):
     """Persistent schedule with a small stream-K remainder: n = 2000, k = 480 under a 128 x 48 tile is
     16 x 10 = 160 tiles on 148 CTAs (remainder 12 < 148 / 2). The default schedule folds one
     data-parallel wave into the stream-K tail (12 + 148 tail tiles, at most two contributors each);
     CHFSI_SK_HYBRID=0 keeps the plain split (12 tail tiles over all 148 CTAs). Both within the filter
-    tolerance of the compact-WY closed form (App. A) and of each other (they only re-associate the k sum)."""
+    tolerance of the compact-WY closed form (App. A) and of each other (they only re-associate the k sum).
+    z210 (CTA pairs: 80 pair tiles on 74 cluster slots) and z206 (2 CTAs per SM: 320 tiles on 296 slots)
+    take the same hybrid over their own schedule units."""
     n, k = 2000, 480
     w = G.wy(n, int(0.9 * n), 31)
     H = w.full()
