@@ -23,24 +23,29 @@ namespace {
 
 // X (n x nloc) <- columns row0 .. row0 + nloc - 1 of the identity
 __global__ void unit_cols_kernel(int64_t n, int64_t nloc, int64_t row0, double2* X, int64_t ldx) {
-  const int64_t j = blockIdx.y;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    X[j * ldx + i] = make_double2(i == row0 + j ? 1.0 : 0.0, 0.0);
+  for (int64_t j = blockIdx.y; j < nloc; j += gridDim.y)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+      X[j * ldx + i] = make_double2(i == row0 + j ? 1.0 : 0.0, 0.0);
 }
 
 // Hp[:, j] <- column row0 + j of (W + W^H) / 2, W the gathered n x n matrix: the (i, c) entry computed
 // here and the (c, i) entry computed by the rank that owns column i are exact conjugates (the same
 // two operands, added in either order), so the assembled H is Hermitian bit for bit (R13)
-__global__ void hermitize_panel_kernel(int64_t n, int64_t row0, const double2* __restrict__ W, int64_t ldw, double2* Hp,
-                                       int64_t ldh) {
-  const int64_t j = blockIdx.y, c = row0 + j;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double2 a = W[c * ldw + i], b = W[i * ldw + c];
-    Hp[j * ldh + i] = i == c ? make_double2(a.x, 0.0) : make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+__global__ void hermitize_panel_kernel(int64_t n, int64_t nloc, int64_t row0, const double2* __restrict__ W,
+                                       int64_t ldw, double2* Hp, int64_t ldh) {
+  for (int64_t j = blockIdx.y; j < nloc; j += gridDim.y) {
+    const int64_t c = row0 + j;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      const double2 a = W[c * ldw + i], b = W[i * ldw + c];
+      Hp[j * ldh + i] = i == c ? make_double2(a.x, 0.0) : make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+    }
   }
 }
 
-unsigned col_blocks(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 64); }
+// grid over (rows, columns): <= 64 row blocks of 256 threads, <= 65535 column blocks (grid-stride beyond)
+dim3 col_grid(int64_t n, int64_t cols) {
+  return dim3((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(cols, 65535));
+}
 
 // W (n x n, ld n) <- the p column slabs S_q (n x nloc) of all ranks: this rank's slab is copied into its
 // column range, then one in-place allgather
@@ -179,8 +184,7 @@ chfsi_status chfsi_reduce_generalized_panel(chfsi_ctx ctx, int64_t n, int64_t ro
   TRY(comm_bcast(ctx, reinterpret_cast<double*>(W), (size_t)2 * n * n, 0));
   CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(L, 16 * ldl, W, 16 * n, 16 * n, n, cudaMemcpyDeviceToDevice, ctx->stream));
   // this rank's columns of H = L^{-1} A L^{-H}: X = L^{-H} E_cols, then L^{-1} (A X)
-  unit_cols_kernel<<<dim3(col_blocks(n), (unsigned)nloc), 256, 0, ctx->stream>>>(n, nloc, row0,
-                                                                                 reinterpret_cast<double2*>(X), n);
+  unit_cols_kernel<<<col_grid(n, nloc), 256, 0, ctx->stream>>>(n, nloc, row0, reinterpret_cast<double2*>(X), n);
   CHFSI_CUDA_TRY(ctx, cudaGetLastError());
   ctx->launches++;
   TRY(gather_slabs(ctx, n, nloc, Ap, lda, W));  // the whole A
@@ -195,8 +199,8 @@ chfsi_status chfsi_reduce_generalized_panel(chfsi_ctx ctx, int64_t n, int64_t ro
   }
   // exact Hermitian storage across the ranks' slabs (R13): gather the unsymmetrised H, average with H^H
   TRY(gather_slabs(ctx, n, nloc, Ap, lda, W));
-  hermitize_panel_kernel<<<dim3(col_blocks(n), (unsigned)nloc), 256, 0, ctx->stream>>>(n, row0, W, n,
-                                                                                      static_cast<double2*>(Ap), lda);
+  hermitize_panel_kernel<<<col_grid(n, nloc), 256, 0, ctx->stream>>>(n, nloc, row0, W, n, static_cast<double2*>(Ap),
+                                                                     lda);
   CHFSI_CUDA_TRY(ctx, cudaGetLastError());
   ctx->launches++;
   CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));

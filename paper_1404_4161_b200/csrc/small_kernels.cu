@@ -36,18 +36,18 @@ __global__ void hemv_kernel(int64_t n, int64_t nloc, const double2* __restrict__
 // K entry q of chunk c = q / chunk lands at c * ldk + q % chunk (ldk >= chunk; the gaps are zero)
 __global__ void h3_plane_kernel(int64_t n, int64_t nloc, const double2* __restrict__ Hp, int64_t ldh,
                                 double* __restrict__ H3, int64_t ld3, int64_t chunk, int64_t ldk) {
-  const int64_t r = blockIdx.y;
   const int64_t nchunks = (n + chunk - 1) / chunk;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nchunks * ldk;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = i / ldk, o = i - c * ldk, q = c * chunk + o;
-    double v = 0.0;
-    if (o < chunk && q < n) {
-      const double2 h = __ldcs(Hp + r * ldh + q);
-      v = h.x - h.y;
+  for (int64_t r = blockIdx.y; r < nloc; r += gridDim.y)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nchunks * ldk;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t c = i / ldk, o = i - c * ldk, q = c * chunk + o;
+      double v = 0.0;
+      if (o < chunk && q < n) {
+        const double2 h = __ldcs(Hp + r * ldh + q);
+        v = h.x - h.y;
+      }
+      H3[r * ld3 + i] = v;
     }
-    H3[r * ld3 + i] = v;
-  }
 }
 
 __global__ void pack_y3_kernel(int64_t rows, const double2* __restrict__ X, int64_t ldx, double* __restrict__ dst,
@@ -104,18 +104,19 @@ __global__ void resid2_kernel(int64_t rows, const double2* __restrict__ HY, int6
 }
 
 __global__ void hermitize_kernel(int64_t k, double2* G, int64_t ldg) {
-  const int64_t j = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > j || j >= k) return;
-  const double2 a = G[j * ldg + i], b = G[i * ldg + j];
-  if (i == j) {
-    G[j * ldg + i] = make_double2(a.x, 0.0);
-    return;
+  for (int64_t j = blockIdx.y; j < k; j += gridDim.y) {
+    if (i > j) continue;
+    const double2 a = G[j * ldg + i], b = G[i * ldg + j];
+    if (i == j) {
+      G[j * ldg + i] = make_double2(a.x, 0.0);
+      continue;
+    }
+    // upper (i,j) = (a + conj(b))/2, lower (j,i) = conj(upper)
+    const double2 u = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+    G[j * ldg + i] = u;
+    G[i * ldg + j] = make_double2(u.x, -u.y);
   }
-  // upper (i,j) = (a + conj(b))/2, lower (j,i) = conj(upper)
-  const double2 u = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
-  G[j * ldg + i] = u;
-  G[i * ldg + j] = make_double2(u.x, -u.y);
 }
 
 __global__ void col_gather_kernel(int64_t rows, const double2* __restrict__ src, int64_t lds, const int* __restrict__ idx,
@@ -236,7 +237,7 @@ cudaError_t launch_resid2(int64_t rows, int64_t cols, const double2* HY, int64_t
 
 cudaError_t launch_hermitize(int64_t k, double2* G, int64_t ldg, cudaStream_t st) {
   if (k <= 0) return cudaSuccess;
-  dim3 grid((unsigned)((k + 127) / 128), (unsigned)k);
+  dim3 grid((unsigned)((k + 127) / 128), (unsigned)std::min<int64_t>(k, 65535));
   hermitize_kernel<<<grid, 128, 0, st>>>(k, G, ldg);
   return cudaGetLastError();
 }
@@ -323,12 +324,13 @@ __global__ void resid2_real_kernel(int64_t rows, const double* __restrict__ HY, 
 }
 
 __global__ void symmetrize_kernel(int64_t k, double* G, int64_t ldg) {
-  const int64_t j = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= j || j >= k) return;
-  const double u = 0.5 * (G[j * ldg + i] + G[i * ldg + j]);
-  G[j * ldg + i] = u;
-  G[i * ldg + j] = u;
+  for (int64_t j = blockIdx.y; j < k; j += gridDim.y) {
+    if (i >= j) continue;
+    const double u = 0.5 * (G[j * ldg + i] + G[i * ldg + j]);
+    G[j * ldg + i] = u;
+    G[i * ldg + j] = u;
+  }
 }
 
 __global__ void col_gather_real_kernel(int64_t rows, const double* __restrict__ src, int64_t lds,
@@ -395,7 +397,7 @@ cudaError_t launch_resid2(int64_t rows, int64_t cols, const double* HY, int64_t 
 }
 cudaError_t launch_hermitize(int64_t k, double* G, int64_t ldg, cudaStream_t st) {
   if (k <= 0) return cudaSuccess;
-  dim3 grid((unsigned)((k + 127) / 128), (unsigned)k);
+  dim3 grid((unsigned)((k + 127) / 128), (unsigned)std::min<int64_t>(k, 65535));
   symmetrize_kernel<<<grid, 128, 0, st>>>(k, G, ldg);
   return cudaGetLastError();
 }
@@ -437,7 +439,7 @@ cudaError_t launch_h3_plane(int64_t n, int64_t nloc, const double2* Hp, int64_t 
   if (n <= 0 || nloc <= 0) return cudaSuccess;
   const int64_t len = (n + chunk - 1) / chunk * ldk;
   const unsigned bx = (unsigned)std::min<int64_t>((len + 255) / 256, 16);
-  h3_plane_kernel<<<dim3(bx, (unsigned)nloc), 256, 0, st>>>(n, nloc, Hp, ldh, H3, ld3, chunk, ldk);
+  h3_plane_kernel<<<dim3(bx, (unsigned)std::min<int64_t>(nloc, 65535)), 256, 0, st>>>(n, nloc, Hp, ldh, H3, ld3, chunk, ldk);
   return cudaGetLastError();
 }
 
