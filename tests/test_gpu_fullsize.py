@@ -91,3 +91,28 @@ def test_filter_c3_full_width(gpu_lib):
     Yo, _ = O.chebyshev_filter(H, Y0[:, cols], [deg[j] for j in cols], l1, c, e)
     rel = np.linalg.norm(Y[:, cols] - Yo, axis=0) / np.linalg.norm(Yo, axis=0)
     assert rel.max() <= 1e-11
+
+
+def test_solve_c3_first_problem(gpu_lib):
+    """c3 size (n = 30000, nev 1200 + nex 240, cap 40): the first eigenproblem of the sequence against
+    H^(1)'s exact spectrum (1e-10 relative, J), orthonormal eigenvectors, naive-oracle residuals on a
+    sample."""
+    cf = CONFIGS["c3"]
+    n, nev, nex = cf["n"], cf["nev"], cf["nex"]
+    w = G.wy(n, cf["nd"], cf["seed"])
+    X0 = G.start_basis(n, nev + nex, cf["seed"])
+    ctx = gpu_lib.Context(0)
+    H = w.full()
+    Hd = gpu_lib.to_colmajor(H)
+    Xd = gpu_lib.to_colmajor(X0)
+    out = ctx.solve_sequence(lambda ell: Hd, 1, Xd, nev, nex, cf["tol"], deg_cap=cf["cap"], seed=cf["seed"])
+    X = Xd.cpu().numpy()[:, :nev]
+    del Hd, Xd
+    ctx.close()
+    assert out["status"] == 0
+    lam = out["lam"][0]
+    assert np.max(np.abs(lam - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
+    sample = [0, nev // 2, nev - 1]
+    assert np.abs(X[:, sample].conj().T @ X - np.eye(nev)[sample]).max() <= 1e-12
+    res = O.residuals(H, X[:, sample], lam[sample], HNORM)
+    assert res.max() <= cf["tol"]
