@@ -116,3 +116,84 @@ def test_solve_c3_first_problem(gpu_lib):
     assert np.abs(X[:, sample].conj().T @ X - np.eye(nev)[sample]).max() <= 1e-12
     res = O.residuals(H, X[:, sample], lam[sample], HNORM)
     assert res.max() <= cf["tol"]
+
+
+def _real_sym_known(n, nd, seed):
+    """Input construction only (torch on the GPU): H = P_8 ... P_1 diag(lambda) P_1 ... P_8 with seeded
+    real Householder reflectors P = I - 2 v v^T, so H's spectrum is exactly gen.spectrum(n, nd)."""
+    import torch
+
+    lam = G.spectrum(n, nd)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    H = torch.diag(torch.as_tensor(lam, dtype=torch.float64, device="cuda"))
+    for _ in range(8):
+        v = torch.randn(n, 1, dtype=torch.float64, device="cuda", generator=g)
+        v = v / torch.linalg.norm(v)
+        Hv = H @ v
+        H = H - 2.0 * v @ Hv.t() - 2.0 * Hv @ v.t() + 4.0 * (v.t() @ Hv) * (v @ v.t())
+    return (H + H.t()) / 2, lam, g
+
+
+def test_solve_real_c2_first_problem(gpu_lib):
+    """NEXT-3 at the c2 size (n = 13000, nev 520 + 104, cap 36): the real-symmetric solver's first
+    eigenproblem against the exact spectrum, orthonormality and naive-oracle residuals on a sample."""
+    import torch
+
+    cf = CONFIGS["c2"]
+    n, nev, nex = cf["n"], cf["nev"], cf["nex"]
+    H, lam, g = _real_sym_known(n, cf["nd"], cf["seed"])
+    Hd = gpu_lib.colmajor(n, n, dtype=torch.float64)
+    Hd.copy_(H)
+    Xd = gpu_lib.colmajor(n, nev + nex, dtype=torch.float64)
+    Xd.copy_(torch.randn(n, nev + nex, dtype=torch.float64, device="cuda", generator=g))
+    del H
+    ctx = gpu_lib.Context(0)
+    out = ctx.solve_sequence(lambda ell: Hd, 1, Xd, nev, nex, cf["tol"], deg_cap=cf["cap"], seed=cf["seed"], real=True)
+    ctx.close()
+    assert out["status"] == 0
+    mu = out["lam"][0]
+    assert np.max(np.abs(mu - lam[:nev]) / np.abs(lam[:nev])) <= 1e-10
+    sample = [0, 1, nev // 2, nev - 1]
+    X = Xd.cpu().numpy()[:, :nev]
+    assert np.abs(X[:, sample].T @ X - np.eye(nev)[sample]).max() <= 1e-12
+    res = O.residuals(Hd.cpu().numpy(), X[:, sample], mu[sample], HNORM)
+    assert res.max() <= cf["tol"]
+
+
+def test_generalized_c2_first_problem(gpu_lib):
+    """NEXT-1 at the c2 size: A = M H^(1) M^H, B = M M^H (generator's lower factor M; products formed
+    with torch on the GPU, input construction only) -> chfsi_reduce_generalized -> the solver ->
+    chfsi_back_transform. Generalised eigenvalues = the exact spectrum of H^(1); generalised residuals
+    and B-orthonormality on a sample of eigenvectors."""
+    import torch
+
+    cf = CONFIGS["c2"]
+    n, nev, nex = cf["n"], cf["nev"], cf["nex"]
+    w = G.wy(n, cf["nd"], cf["seed"])
+    M = torch.as_tensor(G.lower_factor(n, cf["seed"] + 7, 0.5)).cuda()
+    H1 = torch.as_tensor(w.full()).cuda()
+    A = M @ H1 @ M.conj().t()
+    B = M @ M.conj().t()
+    del H1, M
+    Ad, Bd = gpu_lib.colmajor(n, n), gpu_lib.colmajor(n, n)
+    Ad.copy_((A + A.conj().t()) / 2)
+    Bd.copy_((B + B.conj().t()) / 2)
+    del A, B
+    torch.cuda.empty_cache()
+    A_h, B_h = Ad.cpu().numpy(), Bd.cpu().numpy()  # for the residual check
+    ctx = gpu_lib.Context(0)
+    ctx.reduce_generalized(Ad, Bd)
+    Xd = gpu_lib.to_colmajor(G.start_basis(n, nev + nex, cf["seed"]))
+    out = ctx.solve_sequence(lambda ell: Ad, 1, Xd, nev, nex, cf["tol"], deg_cap=cf["cap"], seed=cf["seed"])
+    sample = [0, nev // 2, nev - 1]
+    Cd = Xd[:, sample].contiguous().t().contiguous().t()
+    ctx.back_transform(Bd, Cd)
+    ctx.close()
+    assert out["status"] == 0
+    lam = out["lam"][0]
+    assert np.max(np.abs(lam - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
+    C = Cd.cpu().numpy()
+    BC = B_h @ C
+    r = np.linalg.norm(A_h @ C - BC * lam[sample], axis=0) / (HNORM * np.linalg.norm(BC, axis=0))
+    assert r.max() <= 1e-9
+    assert np.abs(C.conj().T @ BC - np.eye(len(sample))).max() <= 1e-10
