@@ -1,9 +1,9 @@
 """Summarise a CHFSI_K1_LOG trace (stderr of a bench/solve run): K1 time vs the DMMA-peak ideal by width and variant.
-Usage: python tools/k1_log_summary.py <stderr file>  (n fixed to 13000, the c2 size)"""
+Usage: python tools/k1_log_summary.py <stderr file> [n]  (n defaults to 13000, the c2 size)"""
 import collections, sys
 rows=[l.split() for l in open(sys.argv[1]) if l.startswith('k1 ')]
 # k1 rank R n N nloc N ka K variant V ms T
-n=13000
+n=int(sys.argv[2]) if len(sys.argv)>2 else 13000
 tot=0; ideal=0; byw=collections.defaultdict(lambda:[0,0,0]); byv=collections.defaultdict(lambda:[0,0,0])
 for r in rows:
     d=dict(zip(r[1::2], r[2::2]))
