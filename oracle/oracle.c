@@ -858,35 +858,123 @@ int32_t ora_chfsi_solve(int64_t n, const double* H, int64_t ldh, const ora_opts*
 }
 
 /* ------------------------------------------------------------------------------------------------ */
+/* Sylvester's law of inertia: H - sigma I = P L D L^H P^T has as many negative eigenvalues as the
+ * block-diagonal D. D is produced by the Bunch-Kaufman symmetric pivoting strategy (1x1 and 2x2
+ * pivots, alpha = (1 + sqrt 17)/8, the strategy of LAPACK's xHETF2), right-looking, on the lower
+ * triangle of a copy. Only D is needed, so L is not kept and interchanges touch the trailing
+ * matrix only. |.| is the complex modulus. */
+#define LA(i, j) A[2 * ((j) * n + (i))]     /* Re A[i,j], i >= j (lower triangle) */
+#define LAI(i, j) A[2 * ((j) * n + (i)) + 1] /* Im A[i,j] */
+
+/* symmetric interchange of rows/columns p < r of the trailing matrix A[c0:, c0:] (lower storage,
+ * c0 <= p): the entries of the columns c0..p-1 in rows p and r are exchanged as well */
+static void bk_swap(int64_t n, double* A, int64_t c0, int64_t p, int64_t r) {
+  if (r == p) return;
+  double t;
+  for (int64_t c = c0; c < p; ++c) {
+    t = LA(p, c), LA(p, c) = LA(r, c), LA(r, c) = t;
+    t = LAI(p, c), LAI(p, c) = LAI(r, c), LAI(r, c) = t;
+  }
+  t = LA(p, p), LA(p, p) = LA(r, r), LA(r, r) = t; /* diagonal entries (real) */
+  for (int64_t i = r + 1; i < n; ++i) {           /* below both: A[i,p] <-> A[i,r] */
+    t = LA(i, p), LA(i, p) = LA(i, r), LA(i, r) = t;
+    t = LAI(i, p), LAI(i, p) = LAI(i, r), LAI(i, r) = t;
+  }
+  for (int64_t i = p + 1; i < r; ++i) { /* between: A[i,p] <-> conj(A[r,i]) */
+    double xr = LA(i, p), xi = LAI(i, p);
+    LA(i, p) = LA(r, i), LAI(i, p) = -LAI(r, i);
+    LA(r, i) = xr, LAI(r, i) = -xi;
+  }
+  LAI(r, p) = -LAI(r, p); /* A[r,p] <- conj(A[r,p]) */
+}
+
 int64_t ora_count_below(int64_t n, const double* H, int64_t ldh, double sigma) {
   double* A = (double*)malloc(sizeof(double) * 2 * (size_t)n * (size_t)n);
   for (int64_t j = 0; j < n; ++j)
-    for (int64_t i = 0; i < n; ++i) {
-      A[2 * (j * n + i)] = H[2 * (j * ldh + i)] - (i == j ? sigma : 0.0);
-      A[2 * (j * n + i) + 1] = (i == j) ? 0.0 : H[2 * (j * ldh + i) + 1];
+    for (int64_t i = j; i < n; ++i) {
+      LA(i, j) = H[2 * (j * ldh + i)] - (i == j ? sigma : 0.0);
+      LAI(i, j) = (i == j) ? 0.0 : H[2 * (j * ldh + i) + 1];
     }
+  const double alpha = (1.0 + sqrt(17.0)) / 8.0;
   int64_t neg = 0;
-  /* right-looking LDL^H without pivoting: pivot d = A[p,p] (real); trailing update
-   * A[i,j] -= A[i,p] conj(A[j,p]) / d for i,j > p (lower triangle used, Hermitian) */
-  for (int64_t p = 0; p < n; ++p) {
-    double d = A[2 * (p * n + p)];
-    if (d < 0.0) ++neg;
-    if (d == 0.0) d = -1e-300;
-#pragma omp parallel for schedule(static)
-    for (int64_t j = p + 1; j < n; ++j) {
-      double ljr = A[2 * (p * n + j)], lji = A[2 * (p * n + j) + 1]; /* A[j,p] */
-      for (int64_t i = j; i < n; ++i) {
-        double lir = A[2 * (p * n + i)], lii = A[2 * (p * n + i) + 1]; /* A[i,p] */
-        /* A[i,p] conj(A[j,p]) / d */
-        double pr = (lir * ljr + lii * lji) / d, pi = (lii * ljr - lir * lji) / d;
-        A[2 * (j * n + i)] -= pr;
-        A[2 * (j * n + i) + 1] -= pi;
+  int64_t p = 0;
+  while (p < n) {
+    /* lambda = largest off-diagonal modulus in column p, at row r */
+    double lam = 0.0;
+    int64_t r = p;
+    for (int64_t i = p + 1; i < n; ++i) {
+      double a = hypot(LA(i, p), LAI(i, p));
+      if (a > lam) lam = a, r = i;
+    }
+    const double app = fabs(LA(p, p));
+    int size = 1;
+    if (lam == 0.0) { /* column p already reduced: 1x1 pivot, no update */
+      if (LA(p, p) < 0.0) ++neg;
+      ++p;
+      continue;
+    }
+    if (app < alpha * lam) {
+      /* sigma_r = largest off-diagonal modulus in row/column r of the trailing matrix */
+      double sr = 0.0;
+      for (int64_t j = p; j < r; ++j) {
+        double a = hypot(LA(r, j), LAI(r, j));
+        if (a > sr) sr = a;
       }
+      for (int64_t i = r + 1; i < n; ++i) {
+        double a = hypot(LA(i, r), LAI(i, r));
+        if (a > sr) sr = a;
+      }
+      if (app * sr >= alpha * lam * lam) {
+        /* 1x1 pivot at p, no interchange */
+      } else if (fabs(LA(r, r)) >= alpha * sr) {
+        bk_swap(n, A, p, p, r); /* 1x1 pivot A[r,r] */
+      } else {
+        bk_swap(n, A, p, p + 1, r); /* 2x2 pivot on (p, r) */
+        size = 2;
+      }
+    }
+    if (size == 1) {
+      const double d = LA(p, p);
+      if (d < 0.0) ++neg;
+      /* A[i,j] -= A[i,p] conj(A[j,p]) / d, i >= j > p */
+#pragma omp parallel for schedule(dynamic, 16)
+      for (int64_t j = p + 1; j < n; ++j) {
+        const double xjr = LA(j, p), xji = LAI(j, p);
+        for (int64_t i = j; i < n; ++i) {
+          const double xir = LA(i, p), xii = LAI(i, p);
+          LA(i, j) -= (xir * xjr + xii * xji) / d;
+          LAI(i, j) -= (xii * xjr - xir * xji) / d;
+        }
+      }
+      ++p;
+    } else {
+      /* D = [[a, conj(b)], [b, c]], a, c real, b = A[p+1,p]; inertia of D from det and trace */
+      const double a = LA(p, p), c = LA(p + 1, p + 1), br = LA(p + 1, p), bi = LAI(p + 1, p);
+      const double det = a * c - (br * br + bi * bi);
+      if (det < 0.0) neg += 1;
+      else if (det > 0.0) neg += (a + c < 0.0) ? 2 : 0;
+      else neg += (a + c < 0.0) ? 1 : 0;
+      /* A[i,j] -= u_i conj(x_j) + v_i conj(y_j), i >= j >= p+2, with x = A[:,p], y = A[:,p+1] and
+       * [u_i v_i] = [x_i y_i] D^{-1} = [c x_i - b y_i, -conj(b) x_i + a y_i] / det */
+#pragma omp parallel for schedule(dynamic, 16)
+      for (int64_t j = p + 2; j < n; ++j) {
+        const double xjr = LA(j, p), xji = LAI(j, p), yjr = LA(j, p + 1), yji = LAI(j, p + 1);
+        for (int64_t i = j; i < n; ++i) {
+          const double xr = LA(i, p), xi = LAI(i, p), yr = LA(i, p + 1), yi = LAI(i, p + 1);
+          const double ur = (c * xr - (br * yr - bi * yi)) / det, ui = (c * xi - (br * yi + bi * yr)) / det;
+          const double vr = (-(br * xr + bi * xi) + a * yr) / det, vi = (-(br * xi - bi * xr) + a * yi) / det;
+          LA(i, j) -= (ur * xjr + ui * xji) + (vr * yjr + vi * yji);
+          LAI(i, j) -= (ui * xjr - ur * xji) + (vi * yjr - vr * yji);
+        }
+      }
+      p += 2;
     }
   }
   free(A);
   return neg;
 }
+#undef LA
+#undef LAI
 
 /* ------------------------------------------------------------------------------------------------ */
 /* Cholesky, column by column (left-looking): L[j,j] = sqrt(B[j,j] - sum_p |L[j,p]|^2),

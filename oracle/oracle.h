@@ -120,8 +120,11 @@ void ora_trsm_lower(int64_t n, int64_t k, const double* L, int64_t ldl, double* 
 int32_t ora_reduce_generalized(int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb,
                                double* H, int64_t ldh, double* L, int64_t ldl);
 
-/* Number of eigenvalues of H strictly below sigma: inertia of H - sigma I by an LDL^H factorisation
- * with Bunch-Kaufman-free diagonal pivoting on a copy (Sylvester's law of inertia). */
+/* Number of eigenvalues of H strictly below sigma (Sylvester's law of inertia): H - sigma I =
+ * P L D L^H P^T by the Bunch-Kaufman pivoting strategy (1x1 / 2x2 pivots, alpha = (1 + sqrt 17)/8)
+ * on a copy of the lower triangle; the count is the number of negative eigenvalues of the block
+ * diagonal D. Pinned against numpy.eigvalsh at n >= 512 (shifts within 1e-8 of an eigenvalue), the
+ * generator's exact spectrum, and matrices an unpivoted LDL^H miscounts (tests/test_oracle_linalg.py). */
 int64_t ora_count_below(int64_t n, const double* H, int64_t ldh, double sigma);
 
 #ifdef __cplusplus

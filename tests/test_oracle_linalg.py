@@ -105,6 +105,60 @@ def test_count_below_vs_numpy():
         assert O.count_below(A, s) == int(np.sum(ev < s))
 
 
+@pytest.mark.parametrize("n", [512, 640])
+def test_count_below_near_eigenvalues(n):
+    """Bunch-Kaufman inertia at n >= 512 (the completeness gate's sizes scale this up) with shifts
+    within 1e-8 of an eigenvalue, on either side (Sylvester's law of inertia vs numpy.eigvalsh)."""
+    rng = np.random.default_rng(n)
+    A = crand(rng, n, n) / np.sqrt(2 * n)
+    A = (A + A.conj().T) / 2
+    ev = np.linalg.eigvalsh(A)
+    for i in (0, 7, n // 3, n // 2, n - 5):
+        gap = min(ev[i] - ev[i - 1] if i else 1.0, ev[i + 1] - ev[i])
+        assert gap > 1e-6
+        for s in (ev[i] - 1e-8, ev[i] + 1e-8):
+            assert O.count_below(A, s) == int(np.sum(ev < s)), (i, s)
+
+
+def test_count_below_exact_spectrum_h1():
+    """H^(1) = Q diag(Lambda) Q^H from the generator has an exactly known spectrum: the count below a
+    point halfway between Lambda_i and Lambda_{i+1} is i + 1 (independent of any eigensolver)."""
+    n = 600
+    w = G.wy(n, 540, 31)
+    H = w.full()
+    for i in (0, 31, 200, 539, 540, 598):
+        s = 0.5 * (w.lam[i] + w.lam[i + 1])
+        assert O.count_below(H, s) == i + 1
+
+
+def test_count_below_needs_pivoting():
+    """Cases an unpivoted LDL^H gets wrong: (a) a zero diagonal (every 1x1 pivot of [[0, B], [B^H, 0]]
+    at sigma = 0 is 0: the 2x2 pivots are required; the spectrum is +-singular values of B, so exactly
+    n/2 are negative); (b) a leading pivot of 1e-14 next to O(1) off-diagonals (element growth 1e14)."""
+    rng = np.random.default_rng(12)
+    h = 256
+    B = crand(rng, h, h)
+    Z = np.zeros((2 * h, 2 * h), dtype=complex)
+    Z[:h, h:] = B
+    Z[h:, :h] = B.conj().T
+    assert O.count_below(Z, 0.0) == h
+    sv = np.linalg.svd(B, compute_uv=False)  # eigenvalues of Z: -sv (h of them) and +sv
+    assert O.count_below(Z, -0.5 * sv.min()) == h
+    assert O.count_below(Z, 0.5 * sv.min()) == h
+    assert O.count_below(Z, -np.sort(sv)[h // 2] + 1e-9) == h - h // 2
+    # (b) a GUE-like matrix whose leading entry is 1e-15 / 1e-17: the unpivoted count returns 255 and
+    # 256 here instead of 254 (checked when this pin was written); Bunch-Kaufman interchanges first
+    n = 512
+    for tiny in (1e-15, 1e-17):
+        rng = np.random.default_rng(4)
+        A = crand(rng, n, n) / np.sqrt(2 * n)
+        A = (A + A.conj().T) / 2
+        A[0, 0] = tiny
+        ev = np.linalg.eigvalsh(A)
+        assert np.min(np.abs(ev)) > 1e-6
+        assert O.count_below(A, 0.0) == int(np.sum(ev < 0)) == 254
+
+
 # ---- Lanczos (Alg 1 l3, P:548-558; R17) ---------------------------------------------------------------
 @pytest.mark.parametrize("g", gold("lanczos"), ids=lambda g: g["cite"][:12])
 def test_lanczos_golden(g):
