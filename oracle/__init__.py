@@ -75,6 +75,8 @@ def lib():
         L.ora_trsm_lower.argtypes = [i64, i64, ptr, i64, ptr, i64, i32]
         L.ora_reduce_generalized.argtypes = [i64, ptr, i64, ptr, i64, ptr, i64, ptr, i64]
         L.ora_reduce_generalized.restype = i32
+        L.ora_orthonormalize.argtypes = [i64, ptr, i64, ptr, i64, u64, ptr]
+        L.ora_orthonormalize.restype = i32
         L.ora_count_below.argtypes = [i64, ptr, i64, dbl]
         L.ora_count_below.restype = i64
         _lib = L
@@ -153,6 +155,19 @@ def householder_qr(A):
     R = np.empty((k, k), dtype=np.complex128, order="F")
     defic = lib().ora_householder_qr(n, k, _p(A), n, _p(Q), n, _p(R), k)
     return Q, R, defic
+
+
+def orthonormalize(Y, XL=None, seed=0):
+    """Alg 1 l6 with the rank-deficiency rule R23. Returns (Q, replaced); raises if R23 failed."""
+    Y = _cf(Y).copy(order="F")
+    n, ka = Y.shape
+    nl = 0 if XL is None else XL.shape[1]
+    X = _cf(XL) if nl else np.zeros((n, 1), dtype=np.complex128, order="F")
+    rep = ctypes.c_int32(0)
+    st = lib().ora_orthonormalize(n, _p(X), nl, _p(Y), ka, seed, ctypes.byref(rep))
+    if st:
+        raise RuntimeError("ora_orthonormalize: still rank deficient after 3 replacement rounds")
+    return Y, rep.value
 
 
 def jacobi_eig(A):

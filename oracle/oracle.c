@@ -687,6 +687,48 @@ static void cgs2(int64_t n, const double* X, int64_t nl, double* Y, int64_t ka) 
   free(XC);
 }
 
+/* Alg 1 l6 with the rank-deficiency rule R23:
+ *  nu_j = ||y_j|| (input);  repeat: Y <- CGS2(Y against X_L); Householder QR Y = Q R;
+ *  D = {j : |R_jj| <= 1e-12 nu_j}; if D is empty, Y <- Q and stop; otherwise (at most 3 rounds)
+ *  y_j <- x_j for j in D, x_j the R22 vector with seed `seed + round` and stream (6 << 16) | (nl + j),
+ *  nu_j <- ||x_j||, and repeat on the whole block. */
+int32_t ora_orthonormalize(int64_t n, const double* XL, int64_t nl, double* Y, int64_t ka, uint64_t seed,
+                           int32_t* replaced) {
+  if (replaced) *replaced = 0;
+  if (ka == 0) return 0;
+  const size_t colsz = sizeof(double) * 2 * (size_t)n;
+  double* Q = (double*)malloc(colsz * (size_t)ka);
+  double* R = (double*)malloc(sizeof(double) * 2 * (size_t)ka * (size_t)ka);
+  double* nu = (double*)malloc(sizeof(double) * (size_t)ka);
+  for (int64_t j = 0; j < ka; ++j) nu[j] = znrm2(n, Y + 2 * j * n);
+  int32_t status = 4;
+  for (int round = 0; round <= 3; ++round) {
+    cgs2(n, XL, nl, Y, ka);
+    ora_householder_qr(n, ka, Y, n, Q, n, R, ka);
+    int32_t nd = 0;
+    for (int64_t j = 0; j < ka; ++j) {
+      const double rjj = hypot(R[2 * (j * ka + j)], R[2 * (j * ka + j) + 1]);
+      if (!(rjj <= 1e-12 * nu[j])) continue;
+      ++nd;
+      if (round < 3) {
+        ora_random_vector(n, seed + (uint64_t)round, ((uint64_t)6 << 16) | (uint64_t)(nl + j), Y + 2 * j * n);
+        nu[j] = znrm2(n, Y + 2 * j * n);
+      }
+    }
+    if (nd == 0) {
+      memcpy(Y, Q, colsz * (size_t)ka);
+      status = 0;
+      break;
+    }
+    if (round == 3) break;
+    if (replaced) *replaced += nd;
+  }
+  free(Q);
+  free(R);
+  free(nu);
+  return status;
+}
+
 int32_t ora_chfsi_solve(int64_t n, const double* H, int64_t ldh, const ora_opts* o, double* X,
                         int64_t ldx, int32_t have_prev, double* lambda1, double* lambdak,
                         double* lam, double* resid, ora_report* rep) {
@@ -718,10 +760,12 @@ int32_t ora_chfsi_solve(int64_t n, const double* H, int64_t ldh, const ora_opts*
   rep->matvecs_total += o->lanczos_steps;
 
   double lam1, alpha;
+  int32_t status = 3;
   if (!have_prev) {
     /* R11: random start -> QR -> RR seeds (lambda_1, alpha) */
-    rep->qr_replaced += ora_householder_qr(n, k, Ya, n, Tmp, n, NULL, 0);
-    memcpy(Ya, Tmp, colsz * (size_t)k);
+    int32_t nrep = 0;
+    if (ora_orthonormalize(n, NULL, 0, Ya, k, o->seed, &nrep)) status = 4;
+    rep->qr_replaced += nrep;
     ora_rayleigh_ritz(n, H, ldh, Ya, n, k, mu);
     rep->matvecs_total += k;
     lam1 = mu[0];
@@ -733,8 +777,7 @@ int32_t ora_chfsi_solve(int64_t n, const double* H, int64_t ldh, const ora_opts*
   /* Alg 1 l2 (R12): degrees start at deg0 */
   for (int64_t j = 0; j < k; ++j) m[j] = o->deg0;
   int64_t nl = 0; /* locked count */
-  int32_t status = 3;
-  while (rep->loops < o->max_loops) {
+  while (status == 3 && rep->loops < o->max_loops) {
     const int64_t ka = k - nl;
     double c = 0.5 * (alpha + beta), e = 0.5 * (beta - alpha);
     /* R6: stable ascending sort of the active columns by degree */
@@ -758,8 +801,13 @@ int32_t ora_chfsi_solve(int64_t n, const double* H, int64_t ldh, const ora_opts*
     rep->matvecs_filter += mvf;
     rep->matvecs_total += mvf;
     /* Alg 1 l6: orthonormalise against the locked block (R15), then Householder QR (R14) */
-    cgs2(n, XL, nl, Tmp, ka);
-    rep->qr_replaced += ora_householder_qr(n, ka, Tmp, n, Ya, n, NULL, 0);
+    int32_t nrep = 0;
+    if (ora_orthonormalize(n, XL, nl, Tmp, ka, o->seed, &nrep)) {
+      status = 4;
+      break;
+    }
+    rep->qr_replaced += nrep;
+    memcpy(Ya, Tmp, colsz * (size_t)ka);
     /* Alg 1 l7-9: Rayleigh-Ritz on the active block (R16) */
     ora_rayleigh_ritz(n, H, ldh, Ya, n, ka, mu);
     rep->matvecs_total += ka;

@@ -87,6 +87,15 @@ int32_t ora_degree_literal(double res, double tol, double rho, int32_t cap);
 /* |rho| = |t| + sqrt(t^2-1) for |t| > 1 (eq:ratio), 1 inside [-1,1] (R5). */
 double ora_rho(double t);
 
+/* Alg 1 l6 with the QR rank-deficiency rule R23: the active
+ * block Y (n x ka, ld n, in/out) is orthonormalised against the locked block XL (n x nl, ld n; left
+ * unchanged) by CGS2 and then by Householder QR; a column j with |R_jj| <= 1e-12 ||y_j(input)|| is
+ * replaced by the R22 vector (seed + round, stream (6 << 16) | (nl + j)) and the block is redone
+ * (at most 3 rounds). *replaced (nullable) = the number of replacements. Returns 0, or 4 if columns
+ * were still deficient after 3 rounds. */
+int32_t ora_orthonormalize(int64_t n, const double* XL, int64_t nl, double* Y, int64_t ka, uint64_t seed,
+                           int32_t* replaced);
+
 typedef struct {
   int32_t nev, nex, deg0, deg_cap, max_loops, lanczos_steps;
   double tol;
@@ -104,7 +113,8 @@ typedef struct {
  * problem's hand-off; out: hand-off block [locked (ascending) | remaining active]. lambda1/lambdak:
  * in (used when have_prev), out (smallest / largest of the final k values). lam[nev], resid[nev]:
  * the converged eigenvalues (ascending) and their residuals; X[:, 0:nev] are their vectors.
- * Returns 0, 3 if max_loops was hit (partial results), 1 on bad arguments. */
+ * QR rank deficiency follows R23 (ora_orthonormalize, seed = opts->seed; rep->qr_replaced counts it).
+ * Returns 0, 3 if max_loops was hit (partial results), 1 on bad arguments, 4 if R23 failed. */
 int32_t ora_chfsi_solve(int64_t n, const double* H, int64_t ldh, const ora_opts* opts, double* X,
                         int64_t ldx, int32_t have_prev, double* lambda1, double* lambdak,
                         double* lam, double* resid, ora_report* rep);

@@ -64,6 +64,53 @@ def test_qr_detects_rank_deficiency():
     assert d == 1
 
 
+def _unique_qr(A):
+    """numpy QR with the positive-real-diagonal convention (the unique QR of a full-rank A)."""
+    Q, R = np.linalg.qr(A)
+    return Q * (np.diag(R) / np.abs(np.diag(R)))
+
+
+def _r22(n, seed, strm):
+    """The R22 vector written out from gen's uniform hash (independent of the oracle's own code)."""
+    u = np.array([G.uniform(seed, strm, t) for t in range(2 * n)])
+    return (2 * u[0::2] - 1) + 1j * (2 * u[1::2] - 1)
+
+
+@pytest.mark.parametrize("case", ["duplicate", "zero", "in_locked_span"])
+def test_orthonormalize_rank_deficiency_rule(case):
+    """R23: a numerically dependent active column is replaced by the R22 vector of stream
+    (6 << 16) | (nl + j) and the block is orthonormalised again. Pinned against numpy: the result is the
+    unique QR of [X_L | Y'] restricted to the active columns, Y' = Y with the column replaced."""
+    rng = np.random.default_rng(21)
+    n, ka, seed = 120, 9, 77
+    nl = 0 if case == "duplicate" else 5
+    XL = _unique_qr(crand(rng, n, nl)) if nl else None
+    Y = crand(rng, n, ka)
+    j = 4
+    if case == "duplicate":  # SPEC S:54: duplicated column
+        Y[:, j] = Y[:, j - 1]
+    elif case == "zero":
+        Y[:, j] = 0
+    else:  # lies in span(X_L): nothing is left after the projection against the locked block
+        Y[:, j] = XL @ crand(rng, nl)
+    Q, replaced = O.orthonormalize(Y, XL, seed=seed)
+    assert replaced == 1
+    full = Q if XL is None else np.hstack([XL, Q])
+    assert np.abs(full.conj().T @ full - np.eye(full.shape[1])).max() <= 1e-13
+    Yp = Y.copy()
+    Yp[:, j] = _r22(n, seed, (6 << 16) | (nl + j))
+    ref = _unique_qr(Yp if XL is None else np.hstack([XL, Yp]))[:, nl:]
+    np.testing.assert_allclose(Q, ref, rtol=0, atol=1e-12)
+
+
+def test_orthonormalize_full_rank_untouched():
+    rng = np.random.default_rng(22)
+    Y = crand(rng, 80, 12)
+    Q, replaced = O.orthonormalize(Y, None, seed=3)
+    assert replaced == 0
+    np.testing.assert_allclose(Q, _unique_qr(Y), rtol=0, atol=1e-12)
+
+
 # ---- Jacobi eigensolver (S:100) -----------------------------------------------------------------------
 @pytest.mark.parametrize("g", gold("eig"), ids=lambda g: g["cite"][:11])
 def test_jacobi_golden(g):
