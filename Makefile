@@ -22,10 +22,17 @@ gen/libgen.so: gen/gen.c gen/gen.h
 oracle/liboracle.so: oracle/oracle.c oracle/oracle.h
 	$(HOSTCC) $(CFLAGS_HOST) -shared -o $@ oracle/oracle.c -lm
 
-$(LIBCHFSI): $(CU_SRCS) $(CU_HDRS)
-	$(NVCC) $(NVCCFLAGS) -Iinclude -I$(NCCL_INC) -shared -o $@ $(CU_SRCS) -lcublas -lcusolver -ldl
+# one object per translation unit (built in parallel: make -j), then one shared library
+CU_OBJS = $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
+
+build/%.o: $(CSRC)/%.cu $(CU_HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVCCFLAGS) -Iinclude -I$(NCCL_INC) -c -o $@ $<
+
+$(LIBCHFSI): $(CU_OBJS)
+	$(NVCC) $(NVCCFLAGS) -shared -o $@ $(CU_OBJS) -lcublas -lcusolver -ldl
 
 clean:
-	rm -f gen/libgen.so oracle/liboracle.so $(LIBCHFSI)
+	rm -f gen/libgen.so oracle/liboracle.so $(LIBCHFSI) $(CU_OBJS)
 
 .PHONY: all clean

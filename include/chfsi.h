@@ -153,10 +153,19 @@ chfsi_status chfsi_lanczos_bounds(chfsi_ctx ctx, int64_t n, int64_t row0, int64_
  * Y <- Y R^{-1}, twice). If a Cholesky pivot fails or ||Q^H Q - I||_max > 1e-12 the block is
  * re-orthonormalised by Householder QR instead (*used_fallback = 1). Q has R with real positive
  * diagonal (Y_in = Q R).
- *   Y  device, nloc x k, ldy >= nloc, in/out.  used_fallback host, nullable.
- * Errors: CHFSI_ERR_ARG, CHFSI_ERR_QR (fallback failed), CUDA/NCCL. */
+ * Rank deficiency (reading R23; the paper's "could easily become linearly dependent",
+ * P:598-601): an active column j whose Householder |R_jj| (after the projection against the locked
+ * block) is <= 1e-12 times its input norm is replaced by the counter-based vector of R22 with seed
+ * `seed + round` and stream (6 << 16) | j (j counted from column 0 of Y), and the block is
+ * orthonormalised again (at most 3 rounds); [locked | Q] is then orthonormal.
+ *   Y  device, nloc x k, ldy >= nloc, in/out; k <= 65536.  used_fallback, replaced host, nullable.
+ * chfsi_qr = chfsi_qr_ex with seed 0 and no replacement count.
+ * Errors: CHFSI_ERR_ARG, CHFSI_ERR_QR (still deficient after 3 rounds / Householder failed), CUDA/NCCL. */
 chfsi_status chfsi_qr(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, void* Y, int64_t ldy,
                       int64_t k, int64_t nlocked, int32_t* used_fallback);
+chfsi_status chfsi_qr_ex(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, void* Y, int64_t ldy,
+                         int64_t k, int64_t nlocked, uint64_t seed, int32_t* used_fallback,
+                         int32_t* replaced);
 
 /* Rayleigh-Ritz -- Alg 1 lines 7-9: G = Q^H H Q (hermitised), G W = W M,
  * Q <- Q W. Q must have orthonormal columns.
@@ -232,6 +241,12 @@ typedef struct {
   double theta_min, theta_max, beta_up, normH;
   double t_filter_kernel; /* seconds inside K1 launches of the filter (CUDA events per launch) */
   int64_t filter_launches; /* K1 launches of the filter */
+  int32_t qr_replaced;     /* columns replaced by the QR rank-deficiency rule (R23) */
+  int32_t reseeded;        /* 1: the previous problem's (lambda_1, lambda_k) did not fit this problem's
+                              Lanczos bound (beta <= alpha): re-seeded from QR + Rayleigh-Ritz (R11) */
+  int32_t eig_refined;     /* loops whose k x k eigensolve ran as the Jacobi-type refinement */
+  int32_t eig_dense;       /* loops whose k x k eigensolve ran as a dense ZHEEVD */
+  double t_eig;            /* seconds in the k x k eigensolves (CUDA events) */
 } chfsi_report;
 
 /* Callback giving problem ell's column slab (device pointer and its leading dimension). */

@@ -61,6 +61,7 @@ def lib():
         L.ora_rayleigh_ritz.argtypes = [i64, ptr, i64, ptr, i64, i64, ptr]
         L.ora_rayleigh_ritz.restype = i32
         L.ora_residuals.argtypes = [i64, ptr, i64, ptr, i64, i64, ptr, dbl, ptr]
+        L.ora_rayleigh_quotients.argtypes = [i64, ptr, i64, ptr, i64, i64, ptr, ptr]
         L.ora_degree.argtypes = [dbl, dbl, dbl, i32]
         L.ora_degree.restype = i32
         L.ora_degree_literal.argtypes = [dbl, dbl, dbl, i32]
@@ -212,6 +213,17 @@ def residuals(H, X, lam, normH):
     r = np.empty(X.shape[1], dtype=np.float64)
     lib().ora_residuals(X.shape[0], _p(H), H.shape[0], _p(X), X.shape[0], X.shape[1], _p(lam), normH, _p(r))
     return r
+
+
+def rayleigh_quotients(H, X):
+    """(rho, resid_abs): Rayleigh quotients of the columns of X and ||H x - rho x|| / ||x||."""
+    H = _cf(H)
+    X = _cf(X)
+    k = X.shape[1]
+    rho = np.empty(k)
+    ra = np.empty(k)
+    lib().ora_rayleigh_quotients(X.shape[0], _p(H), H.shape[0], _p(X), X.shape[0], k, _p(rho), _p(ra))
+    return rho, ra
 
 
 def degree(res, tol, t, cap):

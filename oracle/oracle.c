@@ -647,6 +647,31 @@ void ora_residuals(int64_t n, const double* H, int64_t ldh, const double* X, int
   free(w);
 }
 
+/* rho_j = Re(x_j^H H x_j) / (x_j^H x_j) (the Rayleigh quotient) and
+ * resid_abs[j] = ||H x_j - rho_j x_j||_2 / ||x_j||_2, one naive mat-vec per column (R13). */
+void ora_rayleigh_quotients(int64_t n, const double* H, int64_t ldh, const double* X, int64_t ldx, int64_t k,
+                            double* rho, double* resid_abs) {
+  double* w = (double*)malloc(sizeof(double) * 2 * (size_t)n);
+  for (int64_t j = 0; j < k; ++j) {
+    const double* x = X + 2 * j * ldx;
+    zhemv_naive(n, H, ldh, x, w);
+    double xhx = 0.0, xx = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      xhx += x[2 * i] * w[2 * i] + x[2 * i + 1] * w[2 * i + 1];
+      xx += x[2 * i] * x[2 * i] + x[2 * i + 1] * x[2 * i + 1];
+    }
+    const double r = xhx / xx;
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      const double dr = w[2 * i] - r * x[2 * i], di = w[2 * i + 1] - r * x[2 * i + 1];
+      s += dr * dr + di * di;
+    }
+    rho[j] = r;
+    resid_abs[j] = sqrt(s) / sqrt(xx);
+  }
+  free(w);
+}
+
 double ora_rho(double t) {
   double a = fabs(t);
   if (a <= 1.0) return 1.0;
@@ -759,8 +784,11 @@ int32_t ora_chfsi_solve(int64_t n, const double* H, int64_t ldh, const ora_opts*
   rep->normH = normH;
   rep->matvecs_total += o->lanczos_steps;
 
-  double lam1, alpha;
+  double lam1 = *lambda1, alpha = *lambdak;
   int32_t status = 3;
+  /* the previous problem's (lambda_1, lambda_k) must fit under this problem's bound; otherwise the
+   * start block seeds them as for a first problem (R11) */
+  if (have_prev && !(beta > alpha && lam1 < alpha)) have_prev = 0;
   if (!have_prev) {
     /* R11: random start -> QR -> RR seeds (lambda_1, alpha) */
     int32_t nrep = 0;
@@ -770,9 +798,6 @@ int32_t ora_chfsi_solve(int64_t n, const double* H, int64_t ldh, const ora_opts*
     rep->matvecs_total += k;
     lam1 = mu[0];
     alpha = mu[k - 1];
-  } else {
-    lam1 = *lambda1;
-    alpha = *lambdak;
   }
   /* Alg 1 l2 (R12): degrees start at deg0 */
   for (int64_t j = 0; j < k; ++j) m[j] = o->deg0;

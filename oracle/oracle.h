@@ -80,6 +80,10 @@ int32_t ora_rayleigh_ritz(int64_t n, const double* H, int64_t ldh, double* Q, in
 /* resid[j] = ||H x_j - lam_j x_j||_2 / (||x_j||_2 * normH) (R8; eq:resl definition). */
 void ora_residuals(int64_t n, const double* H, int64_t ldh, const double* X, int64_t ldx, int64_t k,
                    const double* lam, double normH, double* resid);
+/* Rayleigh quotients rho_j = Re(x_j^H H x_j)/(x_j^H x_j) and absolute residuals ||H x_j - rho_j x_j|| /
+ * ||x_j|| of the columns of X (n x k), naive (the Kato-Temple / residual checks of SURVEY 8(c) c4). */
+void ora_rayleigh_quotients(int64_t n, const double* H, int64_t ldh, const double* X, int64_t ldx, int64_t k,
+                            double* rho, double* resid_abs);
 /* Degree rule R21: smallest m with C_m(|t|) >= max(res/tol, 1), clamped to [1, cap]; |t| <= 1 -> cap. */
 int32_t ora_degree(double res, double tol, double t, int32_t cap);
 /* Literal degree bound: ceil(ln(res/tol)/ln rho), clamped to [1, cap]. */

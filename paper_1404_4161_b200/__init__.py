@@ -26,7 +26,7 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_NOCONV", 4: "ERR_QR
 
 EXPORTS = ("chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_ctx_create_nccl", "chfsi_nccl_unique_id", "chfsi_ctx_reserve", "chfsi_ctx_destroy",
            "chfsi_last_error", "chfsi_kernel_launches", "chfsi_ctx_set_pipeline", "chfsi_ctx_set_complex_mult", "chfsi_ctx_set_exchange", "chfsi_local_group_create", "chfsi_local_group_destroy",
-           "chfsi_filter", "chfsi_filter_real", "chfsi_lanczos_bounds", "chfsi_qr", "chfsi_rayleigh_ritz", "chfsi_solve_sequence",
+           "chfsi_filter", "chfsi_filter_real", "chfsi_lanczos_bounds", "chfsi_qr", "chfsi_qr_ex", "chfsi_rayleigh_ritz", "chfsi_solve_sequence",
            "chfsi_reduce_generalized", "chfsi_back_transform", "chfsi_reduce_generalized_panel", "chfsi_back_transform_panel",
            "chfsi_solve_batch", "chfsi_solve_sequence_real")
 
@@ -51,7 +51,9 @@ class Report(ctypes.Structure):
                 ("t_qr", ctypes.c_double), ("t_rr", ctypes.c_double), ("t_resid", ctypes.c_double),
                 ("t_opt", ctypes.c_double), ("t_total", ctypes.c_double), ("theta_min", ctypes.c_double),
                 ("theta_max", ctypes.c_double), ("beta_up", ctypes.c_double), ("normH", ctypes.c_double),
-                ("t_filter_kernel", ctypes.c_double), ("filter_launches", ctypes.c_int64)]
+                ("t_filter_kernel", ctypes.c_double), ("filter_launches", ctypes.c_int64),
+                ("qr_replaced", ctypes.c_int32), ("reseeded", ctypes.c_int32), ("eig_refined", ctypes.c_int32),
+                ("eig_dense", ctypes.c_int32), ("t_eig", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -108,6 +110,8 @@ def lib():
         L.chfsi_filter_real.restype = ctypes.c_int
         L.chfsi_lanczos_bounds.argtypes = [vp, i64, i64, i64, vp, i64, i32, u64, pd, pd, pd]
         L.chfsi_qr.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, pi32]
+        L.chfsi_qr_ex.argtypes = [vp, i64, i64, i64, vp, i64, i64, i64, u64, pi32, pi32]
+        L.chfsi_qr_ex.restype = ctypes.c_int
         L.chfsi_rayleigh_ritz.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, i64, dbl, pd, pd]
         L.chfsi_solve_sequence.argtypes = [vp, i64, i64, i64, i32, GET_H, vp, ctypes.POINTER(Opts), vp, i64, pd, pd,
                                            ctypes.POINTER(Report)]
@@ -296,6 +300,16 @@ class Context:
         fb = ctypes.c_int32()
         self._check(lib().chfsi_qr(self.h, n, row0, nloc, yp, ldy, k, nlocked, ctypes.byref(fb)))
         return fb.value
+
+    def qr_ex(self, Y, nlocked=0, seed=0, n=None, row0=0):
+        """chfsi_qr_ex: QR with the rank-deficiency rule R23; returns (used_fallback, replaced)."""
+        nloc, k = Y.shape
+        n = n or nloc
+        yp, ldy = _mat(Y, nloc, k, "Y")
+        fb, rep = ctypes.c_int32(), ctypes.c_int32()
+        self._check(lib().chfsi_qr_ex(self.h, n, row0, nloc, yp, ldy, k, nlocked, seed, ctypes.byref(fb),
+                                      ctypes.byref(rep)))
+        return fb.value, rep.value
 
     # -- Alg 1 l7-9 --------------------------------------------------------------------------------
     def rayleigh_ritz(self, Hp, Q, normH=None, n=None, row0=0):

@@ -283,6 +283,14 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
     ctx->launches++;
     bsrc = static_cast<const double*>(ctx->L0.ptr);
     bld = ldl;
+  } else if ((eb * ldq) % 16 != 0) {  // real data with an odd ld: TMA strides must be multiples of 16 bytes
+    const int64_t ldl = round_up(nloc, 2);
+    st = ensure(ctx, ctx->L0, eb * (size_t)ldl * k);
+    if (st) return st;
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(ctx->L0.ptr, eb * ldl, Q, eb * ldq, eb * nloc, k, cudaMemcpyDeviceToDevice,
+                                          ctx->stream));
+    bsrc = static_cast<const double*>(ctx->L0.ptr);
+    bld = ldl;
   }
   st = b_operand(ctx, &op, bsrc, p == 1 ? n : nloc, bld, k, 0, p, t.bnc, elem, cw, z3, t.kh);
   if (st) return st;
@@ -556,6 +564,16 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     int h = 0;
     CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (p > 1) {  // a non-finite value lives in one rank's rows: every rank takes the same branch
+      double hv = h ? 1.0 : 0.0;
+      double* dv = reinterpret_cast<double*>(flag) + 1;
+      CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(dv, &hv, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      st = comm_allreduce_sum(ctx, dv, 1);
+      if (st) return st;
+      CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&hv, dv, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      h = hv > 0.0;
+    }
     if (h) {
       set_err(ctx, "chfsi_filter: non-finite value in the filtered block");
       return CHFSI_ERR_NONFINITE;
@@ -667,7 +685,8 @@ void chfsi_ctx_destroy(chfsi_ctx ctx) {
   comm_destroy(ctx);
   DevBuf* bufs[] = {&ctx->h3, &ctx->L0, &ctx->L1, &ctx->R0, &ctx->R1, &ctx->flag, &ctx->sk, &ctx->hpad, &ctx->w1, &ctx->w2, &ctx->w3, &ctx->w4,
                     &ctx->small1, &ctx->small2, &ctx->small3, &ctx->solver_ws, &ctx->devinfo, &ctx->lz,
-                    &ctx->ya,    &ctx->xl,     &ctx->tb,     &ctx->idx,    &ctx->gw,     &ctx->gx};
+                    &ctx->ya,    &ctx->xl,     &ctx->tb,     &ctx->idx,    &ctx->gw,     &ctx->gx,
+                    &ctx->qsave, &ctx->qrn};
   for (DevBuf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   for (cudaEvent_t ev : ctx->k1_events) cudaEventDestroy(ev);

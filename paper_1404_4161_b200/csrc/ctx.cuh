@@ -106,6 +106,7 @@ struct chfsi_ctx_s {
   chfsi::DevBuf devinfo;
   chfsi::DevBuf lz;              // Lanczos basis
   chfsi::DevBuf ya, xl, tb, idx;  // solver: active block, locked block, filter block, column indices
+  chfsi::DevBuf qsave, qrn;      // QR: the projected block (Householder / R23 restart), column norms
   chfsi::DevBuf gw, gx;          // generalised front / back end on row panels: n x n and n x nloc scratch
   chfsi::DevBuf host_pinned_dummy;
   std::vector<char> hbuf;        // host staging

@@ -1,48 +1,11 @@
 // filter_step.cu -- instantiations and launcher of K1 (see filter_step.cuh).
-#include <atomic>
 #include <cstdlib>
 
-#include "filter_step.cuh"
+#include "filter_step_launch.cuh"
 
 namespace chfsi {
 
 namespace {
-
-template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int OCC = 1, int KH = 2>
-cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3,
-                       const CUtensorMap& tmB3, const StepParams& p, cudaStream_t stream) {
-  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE, CL, KH>;
-  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, MODE, CL, OCC, KH>;
-  // the opt-in shared-memory size is a per-device function attribute: set it once per device (contexts
-  // on several host threads may launch the same instantiation concurrently)
-  static std::atomic<uint64_t> attr_devices{0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const uint64_t bit = 1ull << (dev & 63);
-  if (!(attr_devices.load(std::memory_order_acquire) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_devices.fetch_or(bit, std::memory_order_release);
-  }
-  if constexpr (CL == 1) {
-    kern<<<p.grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(tmA, tmB, tmA3, tmB3, p);
-    return cudaGetLastError();
-  } else {  // p.grid counts clusters
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(p.grid * CL));
-    cfg.blockDim = dim3(Cfg::kThreads);
-    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmA3, tmB3, p);
-  }
-}
 
 struct Variant {
   int id, bm, bnc, wnc, threads, acc;
@@ -52,16 +15,23 @@ struct Variant {
   int kh = 2;       // 128-byte swizzle rows per stage (1: half stages)
 };
 // 4M (real embedding) variants; ids are the launch_filter_step cases
+// The variants the step model never selects (for any width 1..2048 and panel height 64..32768: 4M 0, 2,
+// 4, 8, 15; 3M 201-204, 206, 209, 210, 220, 227; real 100, 101) are built only with -DCHFSI_K1_AB (their
+// A/B measurements stay in profiles/r01_*_variants.log, r01_cluster_ab.log, r01_occ2_ab.log,
+// r01_halfstage_ab.log).
 constexpr Variant kVariants[] = {
+#ifdef CHFSI_K1_AB
     {0, 128, 32, 16, 256, 32, 0.930},  // 8 warps, warp tile 32 x 16
-    {1, 64, 64, 16, 256, 32, 0.920},   // 8 warps, warp tile 32 x 16
     {2, 128, 64, 32, 256, 64, 0.940},  // 8 warps, warp tile 32 x 32
-    {3, 64, 32, 16, 128, 32, 0.700},   // 4 warps
     {4, 128, 64, 16, 512, 32, 0.950},  // 16 warps (4 per SMSP), warp tile 32 x 16
+    {8, 128, 64, 16, 256, 64, 0.900},  // 8 warps, warp tile 64 x 16 (measured slower; kept for sweeps)
+    {15, 256, 8, 4, 256, 16, 0.750},   // 8 warps (4 x 2), warp tile 64 x 4
+#endif
+    {1, 64, 64, 16, 256, 32, 0.920},   // 8 warps, warp tile 32 x 16
+    {3, 64, 32, 16, 128, 32, 0.700},   // 4 warps
     {5, 128, 16, 16, 256, 16, 0.900},  // 8 warps, warp tile 16 x 16 (narrow blocks; best at k_a = 16)
     {6, 128, 32, 8, 512, 16, 0.960},   // 16 warps, warp tile 32 x 8
     {7, 128, 48, 16, 384, 32, 1.000},  // 12 warps, warp tile 32 x 16 (34.9 TF/s at n=13000, k=624)
-    {8, 128, 64, 16, 256, 64, 0.900},  // 8 warps, warp tile 64 x 16 (measured slower; kept for sweeps)
     {9, 256, 32, 16, 256, 64, 0.970},  // 8 warps, warp tile 64 x 16, BM 256 (best at exact 32-column fits)
     // narrow (HBM-bound) steps, warp tile 32 or 64 x 4 complex columns (no padding at k_a = 4, 8, 12);
     // eff from n = 16384, 10 steps (profiles/r01_narrow_variants.log): k_a = 4: v10 6.60 ms (6.5 TB/s);
@@ -71,27 +41,32 @@ constexpr Variant kVariants[] = {
     {12, 128, 12, 4, 384, 8, 0.700},   // 12 warps (4 x 3), warp tile 32 x 4
     {13, 256, 8, 4, 512, 8, 0.850},    // 16 warps (8 x 2), warp tile 32 x 4
     {14, 256, 12, 4, 384, 16, 0.820},  // 12 warps (4 x 3), warp tile 64 x 4
-    {15, 256, 8, 4, 256, 16, 0.750},   // 8 warps (4 x 2), warp tile 64 x 4
 };
 // 3M variants: accumulators are 3 sets (P1, P2, P3) of (WM/8) x (WNC/8) 8x8 tiles. eff: measured
 // full-width rates relative to 200 (n = 13000, k = 624: 45.5 / 42.0 / 32.4 / 41.8 / 30.2 TF/s
 // ZGEMM-equivalent; profiles/r01_z3_variants.log)
 constexpr Variant kVariantsZ3[] = {
-    {200, 128, 48, 16, 384, 48, 1.0}, {201, 128, 32, 16, 256, 48, 0.93}, {202, 128, 16, 8, 256, 24, 0.72},
+    {200, 128, 48, 16, 384, 48, 1.0},
+    {207, 64, 64, 16, 512, 24, 0.963},      // 16 warps, warp tile 16 x 16, 4 stages (k_a = 64, 128, 256)
+    {208, 128, 32, 8, 512, 24, 0.94},       // 16 warps, warp tile 32 x 8, 3 stages (k_a = 32, 160)
+#ifdef CHFSI_K1_AB
+    {201, 128, 32, 16, 256, 48, 0.93}, {202, 128, 16, 8, 256, 24, 0.72},
     {203, 64, 64, 16, 256, 48, 0.925}, {204, 192, 32, 16, 384, 48, 0.67},
     {210, 128, 48, 16, 384, 48, 0.5, 2},  // z200 as multicast CTA pairs (A/B measurement; not chosen yet)
     {206, 64, 48, 16, 192, 48, 0.5, 1, 2},  // 6 warps, 2 stages, 2 CTAs per SM (A/B measurement)
-    {207, 64, 64, 16, 512, 24, 0.963},      // 16 warps, warp tile 16 x 16, 4 stages (k_a = 64, 128, 256)
-    {208, 128, 32, 8, 512, 24, 0.94},       // 16 warps, warp tile 32 x 8, 3 stages (k_a = 32, 160)
     {209, 128, 48, 16, 384, 48, 0.5},       // z200 with 2 stages (pipeline-depth probe, never chosen)
     {220, 128, 48, 16, 384, 48, 0.5, 1, 1, 1},   // z200 in 6 half stages (A/B measurement)
     {227, 64, 64, 16, 512, 24, 0.5, 1, 1, 1},    // z207 in 8 half stages (A/B measurement)
+#endif
 };
 // real-symmetric variants (columns are real columns; kNT = WNC / 8). eff relative to 103 (n = 13000,
 // k = 624: 33.6 / 32.1 / 31.7 / 29.2 / 32.9 / 32.6 TF/s for 103 / 100 / 101 / 102 / 104 / 105;
 // profiles/r01_real_variants.log)
 constexpr Variant kVariantsReal[] = {
-    {100, 128, 96, 32, 384, 32, 0.955}, {101, 128, 64, 32, 256, 32, 0.94}, {102, 128, 32, 16, 256, 16, 0.87},
+#ifdef CHFSI_K1_AB
+    {100, 128, 96, 32, 384, 32, 0.955}, {101, 128, 64, 32, 256, 32, 0.94},
+#endif
+    {102, 128, 32, 16, 256, 16, 0.87},
     {103, 192, 64, 32, 384, 32, 1.0},   {104, 128, 64, 16, 512, 16, 0.98}, {105, 128, 48, 16, 384, 16, 0.97},
 };
 
@@ -142,7 +117,10 @@ static TileChoice choose(const Variant (&vs)[N], const char* env, int64_t nrows,
       best = (int)v;
     }
   }
-  if (best < 0) best = 0;
+  if (best < 0) {  // a forced variant that is not built (-DCHFSI_K1_AB): the launch reports an invalid value
+    const Variant& V = vs[0];
+    return TileChoice{forced, V.cluster, V.occ, V.kh, V.bm, V.bnc, V.threads, V.acc, V.wnc, 1e300};
+  }
   const Variant& V = vs[best];
   return TileChoice{V.id, V.cluster, V.occ, V.kh, V.bm, V.bnc, V.threads, V.acc, V.wnc, best_cost};
 }
@@ -199,82 +177,9 @@ size_t filter_partials_doubles(const TileChoice& t, int num_sms) {
 cudaError_t launch_filter_step(const TileChoice& t, const CUtensorMap& tmA, const CUtensorMap& tmB,
                                const CUtensorMap& tmA3, const CUtensorMap& tmB3, const StepParams& p,
                                cudaStream_t stream) {
-#define LC(BM, BNC, WM, WNC, ST, MODE) launch_cfg<BM, BNC, WM, WNC, ST, MODE>(tmA, tmB, tmA3, tmB3, p, stream)
-  switch (t.id) {
-    case 0:
-      return LC(128, 32, 32, 16, 5, kZ4M);
-    case 1:
-      return LC(64, 64, 32, 16, 6, kZ4M);
-    case 2:
-      return LC(128, 64, 32, 32, 4, kZ4M);
-    case 3:
-      return LC(64, 32, 32, 16, 8, kZ4M);
-    case 4:
-      return LC(128, 64, 32, 16, 4, kZ4M);
-    case 5:
-      return LC(128, 16, 16, 16, 6, kZ4M);
-    case 6:
-      return LC(128, 32, 32, 8, 5, kZ4M);
-    case 7:
-      return LC(128, 48, 32, 16, 4, kZ4M);
-    case 8:
-      return LC(128, 64, 64, 16, 4, kZ4M);
-    case 9:
-      return LC(256, 32, 64, 16, 3, kZ4M);
-    case 10:
-      return LC(256, 4, 32, 4, 3, kZ4M);
-    case 11:
-      return LC(128, 8, 32, 4, 6, kZ4M);
-    case 12:
-      return LC(128, 12, 32, 4, 6, kZ4M);
-    case 13:
-      return LC(256, 8, 32, 4, 3, kZ4M);
-    case 14:
-      return LC(256, 12, 64, 4, 3, kZ4M);
-    case 15:
-      return LC(256, 8, 64, 4, 3, kZ4M);
-    // real symmetric (columns are real columns)
-    case 100:
-      return LC(128, 96, 32, 32, 3, kReal);
-    case 101:
-      return LC(128, 64, 32, 32, 4, kReal);
-    case 102:
-      return LC(128, 32, 32, 16, 5, kReal);
-    case 103:
-      return LC(192, 64, 32, 32, 3, kReal);
-    case 104:
-      return LC(128, 64, 32, 16, 4, kReal);
-    case 105:
-      return LC(128, 48, 32, 16, 5, kReal);
-    // complex 3M (columns are complex columns)
-    case 200:
-      return LC(128, 48, 32, 16, 3, kZ3M);
-    case 201:
-      return LC(128, 32, 32, 16, 3, kZ3M);
-    case 202:
-      return LC(128, 16, 32, 8, 3, kZ3M);
-    case 203:
-      return LC(64, 64, 32, 16, 4, kZ3M);
-    case 204:
-      return LC(192, 32, 32, 16, 2, kZ3M);
-    case 210:
-      return launch_cfg<128, 48, 32, 16, 3, kZ3M, 2>(tmA, tmB, tmA3, tmB3, p, stream);
-    case 220:
-      return launch_cfg<128, 48, 32, 16, 6, kZ3M, 1, 1, 1>(tmA, tmB, tmA3, tmB3, p, stream);
-    case 227:
-      return launch_cfg<64, 64, 16, 16, 8, kZ3M, 1, 1, 1>(tmA, tmB, tmA3, tmB3, p, stream);
-    case 209:
-      return LC(128, 48, 32, 16, 2, kZ3M);
-    case 207:
-      return LC(64, 64, 16, 16, 4, kZ3M);
-    case 208:
-      return LC(128, 32, 32, 8, 3, kZ3M);
-    case 206:
-      return launch_cfg<64, 48, 32, 16, 2, kZ3M, 1, 2>(tmA, tmB, tmA3, tmB3, p, stream);
-    default:
-      return cudaErrorInvalidValue;
-  }
-#undef LC
+  if (t.id >= 200) return launch_filter_z3(t.id, tmA, tmB, tmA3, tmB3, p, stream);
+  if (t.id >= 100) return launch_filter_real(t.id, tmA, tmB, tmA3, tmB3, p, stream);
+  return launch_filter_z4(t.id, tmA, tmB, tmA3, tmB3, p, stream);
 }
 
 }  // namespace chfsi

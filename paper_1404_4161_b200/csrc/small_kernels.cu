@@ -50,14 +50,15 @@ __global__ void h3_plane_kernel(int64_t n, int64_t nloc, const double2* __restri
     }
 }
 
-__global__ void pack_y3_kernel(int64_t rows, const double2* __restrict__ X, int64_t ldx, double* __restrict__ dst,
-                               int64_t cs, int64_t y3_off) {
-  const int64_t j = blockIdx.y;
-  double* col = dst + j * cs;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-    const double2 x = X[j * ldx + r];
-    reinterpret_cast<double2*>(col)[r] = x;
-    col[y3_off + r] = x.x + x.y;
+__global__ void pack_y3_kernel(int64_t rows, int64_t cols, const double2* __restrict__ X, int64_t ldx,
+                               double* __restrict__ dst, int64_t cs, int64_t y3_off) {
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y) {
+    double* col = dst + j * cs;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+      const double2 x = X[j * ldx + r];
+      reinterpret_cast<double2*>(col)[r] = x;
+      col[y3_off + r] = x.x + x.y;
+    }
   }
 }
 
@@ -119,24 +120,26 @@ __global__ void hermitize_kernel(int64_t k, double2* G, int64_t ldg) {
   }
 }
 
-__global__ void col_gather_kernel(int64_t rows, const double2* __restrict__ src, int64_t lds, const int* __restrict__ idx,
-                                  double2* __restrict__ dst, int64_t ldd) {
-  const int64_t j = blockIdx.y;
-  const double2* s = src + (int64_t)idx[j] * lds;
-  double2* d = dst + j * ldd;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
-    d[r] = s[r];
+__global__ void col_gather_kernel(int64_t rows, int64_t cols, const double2* __restrict__ src, int64_t lds,
+                                  const int* __restrict__ idx, double2* __restrict__ dst, int64_t ldd) {
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y) {
+    const double2* s = src + (int64_t)idx[j] * lds;
+    double2* d = dst + j * ldd;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+      d[r] = s[r];
+  }
 }
 
-__global__ void col_phase_kernel(int64_t rows, double2* Q, int64_t ldq, const double2* R, int64_t ldr) {
-  const int64_t j = blockIdx.y;
-  const double2 d = R[j * ldr + j];
-  const double a = hypot(d.x, d.y);
-  const double pr = a > 0 ? d.x / a : 1.0, pi = a > 0 ? d.y / a : 0.0;
-  double2* q = Q + j * ldq;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-    const double2 x = q[r];
-    q[r] = make_double2(x.x * pr - x.y * pi, x.x * pi + x.y * pr);
+__global__ void col_phase_kernel(int64_t rows, int64_t cols, double2* Q, int64_t ldq, const double2* R, int64_t ldr) {
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y) {
+    const double2 d = R[j * ldr + j];
+    const double a = hypot(d.x, d.y);
+    const double pr = a > 0 ? d.x / a : 1.0, pi = a > 0 ? d.y / a : 0.0;
+    double2* q = Q + j * ldq;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+      const double2 x = q[r];
+      q[r] = make_double2(x.x * pr - x.y * pi, x.x * pi + x.y * pr);
+    }
   }
 }
 
@@ -147,17 +150,18 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
-__global__ void random_block_kernel(int64_t rows, int64_t row0, uint64_t seed, uint64_t stream_base,
+__global__ void random_block_kernel(int64_t rows, int64_t cols, int64_t row0, uint64_t seed, uint64_t stream_base,
                                     uint64_t stream_stride, double2* X, int64_t ldx) {
-  const int64_t j = blockIdx.y;
-  const uint64_t strm = stream_base | (stream_stride * (uint64_t)j);
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t g = (uint64_t)(row0 + r);
-    const uint64_t h0 = splitmix64(seed ^ (strm << 40) ^ (2 * g));
-    const uint64_t h1 = splitmix64(seed ^ (strm << 40) ^ (2 * g + 1));
-    const double u0 = (double)(h0 >> 11) * (1.0 / 9007199254740992.0);
-    const double u1 = (double)(h1 >> 11) * (1.0 / 9007199254740992.0);
-    X[j * ldx + r] = make_double2(__dadd_rn(__dmul_rn(2.0, u0), -1.0), __dadd_rn(__dmul_rn(2.0, u1), -1.0));
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y) {
+    const uint64_t strm = stream_base | (stream_stride * (uint64_t)j);
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+      const uint64_t g = (uint64_t)(row0 + r);
+      const uint64_t h0 = splitmix64(seed ^ (strm << 40) ^ (2 * g));
+      const uint64_t h1 = splitmix64(seed ^ (strm << 40) ^ (2 * g + 1));
+      const double u0 = (double)(h0 >> 11) * (1.0 / 9007199254740992.0);
+      const double u1 = (double)(h1 >> 11) * (1.0 / 9007199254740992.0);
+      X[j * ldx + r] = make_double2(__dadd_rn(__dmul_rn(2.0, u0), -1.0), __dadd_rn(__dmul_rn(2.0, u1), -1.0));
+    }
   }
 }
 
@@ -197,16 +201,19 @@ __global__ void lanczos_next_kernel(int64_t rows, const D* __restrict__ w, D* __
 }
 
 __global__ void orth_err_kernel(int64_t k, const double2* G, int64_t ldg, unsigned long long* out) {
-  const int64_t j = blockIdx.y;
   double m = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
-    const double2 a = G[j * ldg + i];
-    const double e = hypot(a.x - (i == j ? 1.0 : 0.0), a.y);
-    m = fmax(m, e);
-  }
+  for (int64_t j = blockIdx.y; j < k; j += gridDim.y)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+      const double2 a = G[j * ldg + i];
+      const double e = hypot(a.x - (i == j ? 1.0 : 0.0), a.y);
+      m = fmax(m, e);
+    }
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, __double_as_longlong(m));  // m >= 0: bit order == value order
 }
+
+// gridDim.y limit: the column-indexed kernels loop j += gridDim.y
+inline unsigned ycap(int64_t cols) { return (unsigned)std::min<int64_t>(cols, 65535); }
 
 inline unsigned grid1(int64_t rows, int threads) {
   int64_t b = (rows + threads - 1) / threads;
@@ -245,24 +252,24 @@ cudaError_t launch_hermitize(int64_t k, double2* G, int64_t ldg, cudaStream_t st
 cudaError_t launch_col_gather(int64_t rows, int64_t cols, const double2* src, int64_t lds, const int* idx,
                               double2* dst, int64_t ldd, cudaStream_t st) {
   if (cols <= 0 || rows <= 0) return cudaSuccess;
-  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), (unsigned)cols);
-  col_gather_kernel<<<grid, 256, 0, st>>>(rows, src, lds, idx, dst, ldd);
+  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), ycap(cols));
+  col_gather_kernel<<<grid, 256, 0, st>>>(rows, cols, src, lds, idx, dst, ldd);
   return cudaGetLastError();
 }
 
 cudaError_t launch_col_phase(int64_t rows, int64_t cols, double2* Q, int64_t ldq, const double2* R, int64_t ldr,
                              cudaStream_t st) {
   if (cols <= 0 || rows <= 0) return cudaSuccess;
-  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), (unsigned)cols);
-  col_phase_kernel<<<grid, 256, 0, st>>>(rows, Q, ldq, R, ldr);
+  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), ycap(cols));
+  col_phase_kernel<<<grid, 256, 0, st>>>(rows, cols, Q, ldq, R, ldr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_random_block(int64_t rows, int64_t cols, int64_t row0, uint64_t seed, uint64_t stream_base,
                                 uint64_t stream_stride, double2* X, int64_t ldx, cudaStream_t st) {
   if (cols <= 0 || rows <= 0) return cudaSuccess;
-  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), (unsigned)cols);
-  random_block_kernel<<<grid, 256, 0, st>>>(rows, row0, seed, stream_base, stream_stride, X, ldx);
+  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), ycap(cols));
+  random_block_kernel<<<grid, 256, 0, st>>>(rows, cols, row0, seed, stream_base, stream_stride, X, ldx);
   return cudaGetLastError();
 }
 
@@ -274,7 +281,7 @@ cudaError_t launch_scale(int64_t rows, double2* x, double s, cudaStream_t st) {
 cudaError_t launch_orth_err(int64_t k, const double2* G, int64_t ldg, double* out, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), st);
   if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)((k + 255) / 256), (unsigned)k);
+  dim3 grid((unsigned)((k + 255) / 256), ycap(k));
   orth_err_kernel<<<grid, 256, 0, st>>>(k, G, ldg, reinterpret_cast<unsigned long long*>(out));
   return cudaGetLastError();
 }
@@ -333,32 +340,35 @@ __global__ void symmetrize_kernel(int64_t k, double* G, int64_t ldg) {
   }
 }
 
-__global__ void col_gather_real_kernel(int64_t rows, const double* __restrict__ src, int64_t lds,
+__global__ void col_gather_real_kernel(int64_t rows, int64_t cols, const double* __restrict__ src, int64_t lds,
                                        const int* __restrict__ idx, double* __restrict__ dst, int64_t ldd) {
-  const int64_t j = blockIdx.y;
-  const double* s = src + (int64_t)idx[j] * lds;
-  double* d = dst + j * ldd;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
-    d[r] = s[r];
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y) {
+    const double* s = src + (int64_t)idx[j] * lds;
+    double* d = dst + j * ldd;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+      d[r] = s[r];
+  }
 }
 
-__global__ void col_sign_kernel(int64_t rows, double* Q, int64_t ldq, const double* R, int64_t ldr) {
-  const int64_t j = blockIdx.y;
-  const double sgn = R[j * ldr + j] < 0 ? -1.0 : 1.0;
-  double* q = Q + j * ldq;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
-    q[r] *= sgn;
+__global__ void col_sign_kernel(int64_t rows, int64_t cols, double* Q, int64_t ldq, const double* R, int64_t ldr) {
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y) {
+    const double sgn = R[j * ldr + j] < 0 ? -1.0 : 1.0;
+    double* q = Q + j * ldq;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+      q[r] *= sgn;
+  }
 }
 
-__global__ void random_block_real_kernel(int64_t rows, int64_t row0, uint64_t seed, uint64_t stream_base,
-                                         uint64_t stream_stride, double* X, int64_t ldx) {
-  const int64_t j = blockIdx.y;
-  const uint64_t strm = stream_base | (stream_stride * (uint64_t)j);
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t g = (uint64_t)(row0 + r);
-    const uint64_t h0 = splitmix64(seed ^ (strm << 40) ^ (2 * g));
-    const double u0 = (double)(h0 >> 11) * (1.0 / 9007199254740992.0);
-    X[j * ldx + r] = __dadd_rn(__dmul_rn(2.0, u0), -1.0);
+__global__ void random_block_real_kernel(int64_t rows, int64_t cols, int64_t row0, uint64_t seed,
+                                         uint64_t stream_base, uint64_t stream_stride, double* X, int64_t ldx) {
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y) {
+    const uint64_t strm = stream_base | (stream_stride * (uint64_t)j);
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+      const uint64_t g = (uint64_t)(row0 + r);
+      const uint64_t h0 = splitmix64(seed ^ (strm << 40) ^ (2 * g));
+      const double u0 = (double)(h0 >> 11) * (1.0 / 9007199254740992.0);
+      X[j * ldx + r] = __dadd_rn(__dmul_rn(2.0, u0), -1.0);
+    }
   }
 }
 
@@ -368,10 +378,10 @@ __global__ void scale_real_kernel(int64_t rows, double* x, double s) {
 }
 
 __global__ void orth_err_real_kernel(int64_t k, const double* G, int64_t ldg, unsigned long long* out) {
-  const int64_t j = blockIdx.y;
   double m = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
-    m = fmax(m, fabs(G[j * ldg + i] - (i == j ? 1.0 : 0.0)));
+  for (int64_t j = blockIdx.y; j < k; j += gridDim.y)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+      m = fmax(m, fabs(G[j * ldg + i] - (i == j ? 1.0 : 0.0)));
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, __double_as_longlong(m));
 }
@@ -404,22 +414,22 @@ cudaError_t launch_hermitize(int64_t k, double* G, int64_t ldg, cudaStream_t st)
 cudaError_t launch_col_gather(int64_t rows, int64_t cols, const double* src, int64_t lds, const int* idx, double* dst,
                               int64_t ldd, cudaStream_t st) {
   if (cols <= 0 || rows <= 0) return cudaSuccess;
-  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), (unsigned)cols);
-  col_gather_real_kernel<<<grid, 256, 0, st>>>(rows, src, lds, idx, dst, ldd);
+  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), ycap(cols));
+  col_gather_real_kernel<<<grid, 256, 0, st>>>(rows, cols, src, lds, idx, dst, ldd);
   return cudaGetLastError();
 }
 cudaError_t launch_col_phase(int64_t rows, int64_t cols, double* Q, int64_t ldq, const double* R, int64_t ldr,
                              cudaStream_t st) {
   if (cols <= 0 || rows <= 0) return cudaSuccess;
-  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), (unsigned)cols);
-  col_sign_kernel<<<grid, 256, 0, st>>>(rows, Q, ldq, R, ldr);
+  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), ycap(cols));
+  col_sign_kernel<<<grid, 256, 0, st>>>(rows, cols, Q, ldq, R, ldr);
   return cudaGetLastError();
 }
 cudaError_t launch_random_block(int64_t rows, int64_t cols, int64_t row0, uint64_t seed, uint64_t stream_base,
                                 uint64_t stream_stride, double* X, int64_t ldx, cudaStream_t st) {
   if (cols <= 0 || rows <= 0) return cudaSuccess;
-  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), (unsigned)cols);
-  random_block_real_kernel<<<grid, 256, 0, st>>>(rows, row0, seed, stream_base, stream_stride, X, ldx);
+  dim3 grid(grid1(rows, 256) > 64 ? 64 : grid1(rows, 256), ycap(cols));
+  random_block_real_kernel<<<grid, 256, 0, st>>>(rows, cols, row0, seed, stream_base, stream_stride, X, ldx);
   return cudaGetLastError();
 }
 cudaError_t launch_scale(int64_t rows, double* x, double s, cudaStream_t st) {
@@ -429,7 +439,7 @@ cudaError_t launch_scale(int64_t rows, double* x, double s, cudaStream_t st) {
 cudaError_t launch_orth_err(int64_t k, const double* G, int64_t ldg, double* out, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), st);
   if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)((k + 255) / 256), (unsigned)k);
+  dim3 grid((unsigned)((k + 255) / 256), ycap(k));
   orth_err_real_kernel<<<grid, 256, 0, st>>>(k, G, ldg, reinterpret_cast<unsigned long long*>(out));
   return cudaGetLastError();
 }
@@ -447,7 +457,7 @@ cudaError_t launch_pack_y3(int64_t rows, int64_t cols, const double2* X, int64_t
                            int64_t y3_off, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   const unsigned bx = (unsigned)std::min<int64_t>((rows + 255) / 256, 64);
-  pack_y3_kernel<<<dim3(bx, (unsigned)cols), 256, 0, st>>>(rows, X, ldx, dst, cs, y3_off);
+  pack_y3_kernel<<<dim3(bx, ycap(cols)), 256, 0, st>>>(rows, cols, X, ldx, dst, cs, y3_off);
   return cudaGetLastError();
 }
 

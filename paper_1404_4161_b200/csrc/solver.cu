@@ -133,22 +133,27 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
 
   CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(Ya, eb * nloc, X, eb * ldx, eb * nloc, k, cudaMemcpyDeviceToDevice, ctx->stream));
   std::vector<double> mu(k), res(k), lamL, resL;
-  double lam1, alpha;
+  double lam1 = lam1_io, alpha = lamk_io;
+  // the previous problem's (lambda_1, lambda_k) seed this one unless they do not fit under
+  // this problem's upper bound (beta <= alpha: the filter interval would be empty); then, as for a
+  // first problem (R11), the start block is orthonormalised and its Ritz values seed (lambda_1, alpha)
+  if (have_prev && !(beta > alpha && lam1 < alpha)) {
+    have_prev = false;
+    rep.reseeded = 1;
+  }
   if (!have_prev) {  // R11: start block -> QR -> RR seeds (lambda_1, alpha)
-    int32_t fb = 0;
+    int32_t fb = 0, nrep = 0;
     auto t1 = tm.begin("chfsi: qr (start)");
-    TRY(qr_t<Scal>(ctx, n, nloc, nullptr, nloc, 0, Ya, nloc, k, &fb));
+    TRY(qr_t<Scal>(ctx, n, row0, nloc, nullptr, nloc, 0, Ya, nloc, k, seed, &fb, &nrep));
     tm.end(T_QR, t1);
     rep.qr_fallbacks += fb;
+    rep.qr_replaced += nrep;
     auto t2 = tm.begin("chfsi: rayleigh-ritz (start)");
     TRY(rr_t<Scal>(ctx, n, row0, nloc, Hp, ldh, Ya, nloc, k, normH, mu.data(), nullptr));
     tm.end(T_RR, t2);
     rep.matvecs_total += k;
     lam1 = mu[0];
     alpha = mu[k - 1];
-  } else {
-    lam1 = lam1_io;
-    alpha = lamk_io;
   }
   std::vector<int32_t> m(k, o.fixed_degree > 0 ? o.fixed_degree : o.deg0), ms(k);
   int64_t nl = 0;
@@ -175,12 +180,13 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
     rep.matvecs_filter += mv;
     rep.matvecs_total += mv;
     rep.filter_flops += (elem == 2 ? 8.0 : 2.0) * (double)n * (double)n * (double)mv;
-    // Alg 1 l6: orthonormalise [locked | filtered] (R14, R15)
-    int32_t fb = 0;
+    // Alg 1 l6: orthonormalise [locked | filtered] (R14, R15, R23)
+    int32_t fb = 0, nrep = 0;
     auto t4 = tm.begin("chfsi: qr");
-    TRY(qr_t<Scal>(ctx, n, nloc, XL, nloc, nl, T, nloc, ka, &fb));
+    TRY(qr_t<Scal>(ctx, n, row0, nloc, XL, nloc, nl, T, nloc, ka, seed, &fb, &nrep));
     tm.end(T_QR, t4);
     rep.qr_fallbacks += fb;
+    rep.qr_replaced += nrep;
     // Alg 1 l7-9 (+ residuals, R8): Rayleigh-Ritz on the active block (R16)
     auto t5 = tm.begin("chfsi: rayleigh-ritz");
     TRY(rr_t<Scal>(ctx, n, row0, nloc, Hp, ldh, T, nloc, ka, normH, mu.data(), res.data()));

@@ -283,9 +283,11 @@ chfsi_status lanczos_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
 }
 
 // ---------------------------------------------------------------------------------------------
-// Householder QR of Y (nloc x ka) with a positive real R diagonal; p > 1 gathers the block.
+// Householder QR of Y (nloc x ka) with a positive real R diagonal; p > 1 gathers the block (every rank
+// factors the same gathered block, so every rank gets the same R). rdiag (host, nullable) <- |R_jj|.
 template <typename T>
-static chfsi_status householder(chfsi_ctx ctx, int64_t n, int64_t nloc, void* Y, int64_t ldy, int64_t ka) {
+static chfsi_status householder(chfsi_ctx ctx, int64_t n, int64_t nloc, void* Y, int64_t ldy, int64_t ka,
+                                std::vector<double>* rdiag) {
   using S = Sc<T>;
   using D = typename S::D;
   const size_t eb = sizeof(T);
@@ -321,6 +323,10 @@ static chfsi_status householder(chfsi_ctx ctx, int64_t n, int64_t nloc, void* Y,
   CUSOLVER_TRY(ctx, S::geqrf(ctx->cusolver, (int)m, (int)ka, At, (int)lda, tau, static_cast<T*>(ctx->solver_ws.ptr), lw,
                              info));
   CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(Rd, eb * ka, A, eb * lda, eb * ka, ka, cudaMemcpyDeviceToDevice, ctx->stream));
+  std::vector<T> hdiag(rdiag ? ka : 0);
+  if (rdiag)  // the diagonal of R: stride ka + 1 elements
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(hdiag.data(), eb, Rd, eb * (ka + 1), eb, ka, cudaMemcpyDeviceToHost,
+                                          ctx->stream));
   CUSOLVER_TRY(ctx, S::orgqr(ctx->cusolver, (int)m, (int)ka, At, (int)lda, tau, static_cast<T*>(ctx->solver_ws.ptr), lw,
                              info));
   CHFSI_CUDA_TRY(ctx, launch_col_phase(m, ka, static_cast<D*>(A), lda, reinterpret_cast<D*>(Rd), ka, ctx->stream));
@@ -337,63 +343,134 @@ static chfsi_status householder(chfsi_ctx ctx, int64_t n, int64_t nloc, void* Y,
     set_err(ctx, "Householder fallback failed (info " + std::to_string(hinfo) + ")");
     return CHFSI_ERR_QR;
   }
+  if (rdiag) {
+    rdiag->resize(ka);
+    for (int64_t j = 0; j < ka; ++j) {
+      if constexpr (S::elem == 2)
+        (*rdiag)[j] = std::hypot(hdiag[j].x, hdiag[j].y);
+      else
+        (*rdiag)[j] = std::fabs(hdiag[j]);
+    }
+  }
   return CHFSI_OK;
 }
 
+// Alg 1 l6 with the rank-deficiency rule R23, mirroring ora_orthonormalize:
+//   nu_j = ||y_j|| (input); repeat { Y <- CGS2(Y vs X_L); QR(Y); D = {j : |R_jj| <= 1e-12 nu_j};
+//   if D is empty stop; y_j <- R22 vector (seed + round, stream (6 << 16) | (nl + j)) for j in D }.
+// The QR is CholeskyQR2 (R14) unless a projected column is already below 1e-12 nu_j (it then lies in
+// span(X_L) and CholeskyQR's R_jj could not resolve it); a failed Cholesky pivot or ||Q^H Q - I||_max
+// > 1e-12 falls back to Householder, whose |R_jj| decide D (CholeskyQR2 only ever succeeds on blocks
+// with condition numbers far below 1e12, which have no such column).
 template <typename T>
-chfsi_status qr_t(chfsi_ctx ctx, int64_t n, int64_t nloc, const void* XL, int64_t ldxl, int64_t nl, void* Y, int64_t ldy,
-                  int64_t ka, int32_t* used_fallback) {
+chfsi_status qr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* XL, int64_t ldxl, int64_t nl,
+                  void* Y, int64_t ldy, int64_t ka, uint64_t seed, int32_t* used_fallback, int32_t* replaced) {
   using S = Sc<T>;
   using D = typename S::D;
   const T one = S::one(), mone = S::mone();
   if (used_fallback) *used_fallback = 0;
+  if (replaced) *replaced = 0;
   if (ka == 0) return CHFSI_OK;
   TRY(ensure(ctx, ctx->small1, sizeof(T) * (size_t)std::max<int64_t>(ka, nl) * ka + 64));
   TRY(ensure(ctx, ctx->devinfo, 64));
+  TRY(ensure(ctx, ctx->qrn, sizeof(double) * (size_t)(ka + 8)));
   T* G = static_cast<T*>(ctx->small1.ptr);
   T* Yt = static_cast<T*>(Y);
+  D* Yd = static_cast<D*>(Y);
   const T* Xt = static_cast<const T*>(XL);
   int* info = static_cast<int*>(ctx->devinfo.ptr);
-  // CGS2 against the locked block (R15: the locked columns are not modified)
-  if (nl > 0) {
-    for (int pass = 0; pass < 2; ++pass) {
-      TRY(gram<T>(ctx, nloc, nl, ka, XL, ldxl, Y, ldy, G, nl));
-      CUBLAS_TRY(ctx, S::gemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)nl, &mone, Xt, (int)ldxl, G,
-                              (int)nl, &one, Yt, (int)ldy));
-    }
-  }
-  // CholeskyQR2: S = Y^H Y = R^H R, Y <- Y R^{-1}, twice
-  bool ok = true;
+  double* dnrm = static_cast<double*>(ctx->qrn.ptr);
+  const size_t eb = sizeof(T);
+  // R23: input column norms nu_j^2 (before the projection against the locked block)
+  std::vector<double> nu2(ka), mu2(ka);
+  CHFSI_CUDA_TRY(ctx, launch_colnorm2(nloc, ka, Yd, ldy, dnrm, ctx->stream));
+  ctx->launches++;
+  TRY(comm_allreduce_sum(ctx, dnrm, (size_t)ka));
+  CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(nu2.data(), dnrm, sizeof(double) * ka, cudaMemcpyDeviceToHost, ctx->stream));
   int lw = 0;
   CUSOLVER_TRY(ctx, S::potrf_bs(ctx->cusolver, (int)ka, G, (int)ka, &lw));
   TRY(ensure(ctx, ctx->solver_ws, sizeof(T) * (size_t)std::max(lw, 1)));
-  for (int pass = 0; pass < 2 && ok; ++pass) {
-    TRY(gram<T>(ctx, nloc, ka, ka, Y, ldy, Y, ldy, G, ka));
-    CUSOLVER_TRY(ctx, S::potrf(ctx->cusolver, (int)ka, G, (int)ka, static_cast<T*>(ctx->solver_ws.ptr), lw, info));
-    int hinfo = 0;
-    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    if (hinfo != 0) {
-      ok = false;
-      break;
+  for (int round = 0;; ++round) {
+    // CGS2 against the locked block (R15: the locked columns are not modified)
+    if (nl > 0) {
+      for (int pass = 0; pass < 2; ++pass) {
+        TRY(gram<T>(ctx, nloc, nl, ka, XL, ldxl, Y, ldy, G, nl));
+        CUBLAS_TRY(ctx, S::gemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)nl, &mone, Xt, (int)ldxl, G,
+                                (int)nl, &one, Yt, (int)ldy));
+      }
     }
-    CUBLAS_TRY(ctx, S::trsm_ru(ctx->cublas, (int)nloc, (int)ka, G, (int)ka, Yt, (int)ldy));
-  }
-  if (ok) {  // orthogonality check ||Q^H Q - I||_max <= 1e-12
-    TRY(gram<T>(ctx, nloc, ka, ka, Y, ldy, Y, ldy, G, ka));
-    double* e = reinterpret_cast<double*>(info + 4);
-    CHFSI_CUDA_TRY(ctx, launch_orth_err(ka, reinterpret_cast<const D*>(G), ka, e, ctx->stream));
-    ctx->launches++;
-    double he = 0;
-    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&he, e, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    ok = he <= 1e-12;
-  }
-  if (!ok) {
+    bool ok = true;
+    if (nl > 0) {  // a column numerically inside span(X_L) goes straight to the Householder detection
+      CHFSI_CUDA_TRY(ctx, launch_colnorm2(nloc, ka, Yd, ldy, dnrm, ctx->stream));
+      ctx->launches++;
+      TRY(comm_allreduce_sum(ctx, dnrm, (size_t)ka));
+      CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(mu2.data(), dnrm, sizeof(double) * ka, cudaMemcpyDeviceToHost, ctx->stream));
+      CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      for (int64_t j = 0; j < ka; ++j)
+        if (std::sqrt(mu2[j]) <= 1e-12 * std::sqrt(nu2[j])) ok = false;
+    }
+    // the projected block, kept for a Householder / replacement restart (CholeskyQR2 overwrites Y)
+    TRY(ensure(ctx, ctx->qsave, eb * (size_t)nloc * ka));
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(ctx->qsave.ptr, eb * nloc, Y, eb * ldy, eb * nloc, ka,
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+    // CholeskyQR2: S = Y^H Y = R^H R, Y <- Y R^{-1}, twice
+    for (int pass = 0; pass < 2 && ok; ++pass) {
+      TRY(gram<T>(ctx, nloc, ka, ka, Y, ldy, Y, ldy, G, ka));
+      CUSOLVER_TRY(ctx, S::potrf(ctx->cusolver, (int)ka, G, (int)ka, static_cast<T*>(ctx->solver_ws.ptr), lw, info));
+      int hinfo = 0;
+      CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      if (hinfo != 0) {
+        ok = false;
+        break;
+      }
+      CUBLAS_TRY(ctx, S::trsm_ru(ctx->cublas, (int)nloc, (int)ka, G, (int)ka, Yt, (int)ldy));
+    }
+    if (ok) {  // orthogonality check ||Q^H Q - I||_max <= 1e-12
+      TRY(gram<T>(ctx, nloc, ka, ka, Y, ldy, Y, ldy, G, ka));
+      double* e = reinterpret_cast<double*>(info + 4);
+      CHFSI_CUDA_TRY(ctx, launch_orth_err(ka, reinterpret_cast<const D*>(G), ka, e, ctx->stream));
+      ctx->launches++;
+      double he = 0;
+      CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&he, e, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      ok = he <= 1e-12;
+    }
+    if (ok) return CHFSI_OK;
+    // Householder QR of the projected block; its |R_jj| decide the dependent columns, and a replacement
+    // round restarts from the same projected block as the oracle
     if (used_fallback) *used_fallback = 1;
-    TRY(householder<T>(ctx, n, nloc, Y, ldy, ka));
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(Y, eb * ldy, ctx->qsave.ptr, eb * nloc, eb * nloc, ka,
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+    std::vector<double> rdiag;
+    TRY(householder<T>(ctx, n, nloc, Y, ldy, ka, &rdiag));
+    std::vector<int64_t> defic;
+    for (int64_t j = 0; j < ka; ++j)
+      if (rdiag[j] <= 1e-12 * std::sqrt(nu2[j])) defic.push_back(j);
+    if (defic.empty()) return CHFSI_OK;
+    if (round == 3) {
+      set_err(ctx, "QR: " + std::to_string(defic.size()) + " column(s) still rank deficient after 3 replacement rounds");
+      return CHFSI_ERR_QR;
+    }
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(Y, eb * ldy, ctx->qsave.ptr, eb * nloc, eb * nloc, ka,
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
+    for (size_t i = 0; i < defic.size(); ++i) {
+      D* col = Yd + (size_t)defic[i] * ldy;
+      CHFSI_CUDA_TRY(ctx, launch_random_block(nloc, 1, row0, seed + (uint64_t)round, (6ull << 16) | (uint64_t)(nl + defic[i]),
+                                              0, col, ldy, ctx->stream));
+      CHFSI_CUDA_TRY(ctx, launch_colnorm2(nloc, 1, col, ldy, dnrm + (i % 8), ctx->stream));
+      ctx->launches += 2;
+      if (i % 8 == 7 || i + 1 == defic.size()) {  // the replaced columns' nu_j^2, 8 at a time
+        const size_t cnt = i % 8 + 1;
+        double h8[8];
+        TRY(comm_allreduce_sum(ctx, dnrm, cnt));
+        CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(h8, dnrm, sizeof(double) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+        CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        for (size_t q = 0; q < cnt; ++q) nu2[defic[i + 1 - cnt + q]] = h8[q];
+      }
+    }
+    if (replaced) *replaced += (int32_t)defic.size();
   }
-  return CHFSI_OK;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -445,6 +522,7 @@ chfsi_status rr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const vo
     fprintf(stderr, "rr k %lld offdiag_rel %.3e offdiag_max %.3e\n", (long long)ka, std::sqrt(off / tot), offmax);
   }
   // small dense eigensolve: once, on rank 0, broadcast (identical bits on every rank)
+  CHFSI_CUDA_TRY(ctx, cudaMemsetAsync(info, 0, sizeof(double), ctx->stream));
   if (ctx->rank == 0) {
     int lw = 0;
     CUSOLVER_TRY(ctx, S::heevd_bs(ctx->cusolver, (int)ka, G, (int)ka, dmu, &lw));
@@ -453,6 +531,8 @@ chfsi_status rr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const vo
   }
   TRY(comm_bcast(ctx, reinterpret_cast<double*>(G), (size_t)S::elem * ka * ka, 0));
   TRY(comm_bcast(ctx, dmu, (size_t)ka, 0));
+  // rank 0's info travels with the result (8 bytes), so every rank takes the same error branch
+  TRY(comm_bcast(ctx, reinterpret_cast<double*>(info), 1, 0));
   CUBLAS_TRY(ctx, S::gemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, (int)nloc, (int)ka, (int)ka, &one, Qt, (int)ldq, G,
                           (int)ka, &zero, Yr, (int)nloc));
   if (resid) {
@@ -470,8 +550,7 @@ chfsi_status rr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const vo
   CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), dmu, sizeof(double) * (resid ? 3 * ka : ka), cudaMemcpyDeviceToHost,
                                       ctx->stream));
   int hinfo = 0;
-  if (ctx->rank == 0)
-    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   if (hinfo != 0) {
     set_err(ctx, "zheevd failed (info " + std::to_string(hinfo) + ")");
@@ -489,10 +568,10 @@ template chfsi_status lanczos_t<cuDoubleComplex>(chfsi_ctx, int64_t, int64_t, in
                                                  uint64_t, double*, double*, double*);
 template chfsi_status lanczos_t<double>(chfsi_ctx, int64_t, int64_t, int64_t, const void*, int64_t, int32_t, uint64_t,
                                         double*, double*, double*);
-template chfsi_status qr_t<cuDoubleComplex>(chfsi_ctx, int64_t, int64_t, const void*, int64_t, int64_t, void*, int64_t,
-                                            int64_t, int32_t*);
-template chfsi_status qr_t<double>(chfsi_ctx, int64_t, int64_t, const void*, int64_t, int64_t, void*, int64_t, int64_t,
-                                   int32_t*);
+template chfsi_status qr_t<cuDoubleComplex>(chfsi_ctx, int64_t, int64_t, int64_t, const void*, int64_t, int64_t, void*,
+                                            int64_t, int64_t, uint64_t, int32_t*, int32_t*);
+template chfsi_status qr_t<double>(chfsi_ctx, int64_t, int64_t, int64_t, const void*, int64_t, int64_t, void*, int64_t,
+                                   int64_t, uint64_t, int32_t*, int32_t*);
 template chfsi_status rr_t<cuDoubleComplex>(chfsi_ctx, int64_t, int64_t, int64_t, const void*, int64_t, void*, int64_t,
                                             int64_t, double, double*, double*);
 template chfsi_status rr_t<double>(chfsi_ctx, int64_t, int64_t, int64_t, const void*, int64_t, void*, int64_t, int64_t,
@@ -502,9 +581,9 @@ chfsi_status lanczos_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, 
                           int32_t steps, uint64_t seed, double* theta_min, double* theta_max, double* upper) {
   return lanczos_t<cuDoubleComplex>(ctx, n, row0, nloc, Hp, ldh, steps, seed, theta_min, theta_max, upper);
 }
-chfsi_status qr_impl(chfsi_ctx ctx, int64_t n, int64_t nloc, const void* XL, int64_t ldxl, int64_t nl, void* Y,
-                     int64_t ldy, int64_t ka, int32_t* used_fallback) {
-  return qr_t<cuDoubleComplex>(ctx, n, nloc, XL, ldxl, nl, Y, ldy, ka, used_fallback);
+chfsi_status qr_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* XL, int64_t ldxl, int64_t nl,
+                     void* Y, int64_t ldy, int64_t ka, uint64_t seed, int32_t* used_fallback, int32_t* replaced) {
+  return qr_t<cuDoubleComplex>(ctx, n, row0, nloc, XL, ldxl, nl, Y, ldy, ka, seed, used_fallback, replaced);
 }
 chfsi_status rr_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh, void* Q,
                      int64_t ldq, int64_t ka, double normH, double* mu, double* resid) {
@@ -533,16 +612,22 @@ chfsi_status chfsi_lanczos_bounds(chfsi_ctx ctx, int64_t n, int64_t row0, int64_
 
 chfsi_status chfsi_qr(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, void* Y, int64_t ldy, int64_t k,
                       int64_t nlocked, int32_t* used_fallback) {
+  return chfsi_qr_ex(ctx, n, row0, nloc, Y, ldy, k, nlocked, 0, used_fallback, nullptr);
+}
+
+chfsi_status chfsi_qr_ex(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, void* Y, int64_t ldy, int64_t k,
+                         int64_t nlocked, uint64_t seed, int32_t* used_fallback, int32_t* replaced) {
   if (!ctx) return CHFSI_ERR_ARG;
   ctx->err.clear();
-  if (n < 1 || nloc < 1 || row0 < 0 || row0 + nloc > n || ldy < nloc || k < 0 || k > n || nlocked < 0 ||
-      nlocked > k || (k > 0 && !Y) || (nloc * ctx->nranks != n || row0 != nloc * ctx->rank)) {
-    set_err(ctx, "chfsi_qr: bad arguments");
+  if (n < 1 || nloc < 1 || row0 < 0 || row0 + nloc > n || ldy < nloc || k < 0 || k > n || k > 65536 ||
+      nlocked < 0 || nlocked > k || (k > 0 && !Y) || (nloc * ctx->nranks != n || row0 != nloc * ctx->rank)) {
+    set_err(ctx, "chfsi_qr: bad arguments (k <= 65536 for the R23 replacement streams)");
     return CHFSI_ERR_ARG;
   }
   cudaSetDevice(ctx->device);
   double2* y = static_cast<double2*>(Y);
-  return qr_impl(ctx, n, nloc, y, ldy, nlocked, y + (size_t)ldy * nlocked, ldy, k - nlocked, used_fallback);
+  return qr_impl(ctx, n, row0, nloc, y, ldy, nlocked, y + (size_t)ldy * nlocked, ldy, k - nlocked, seed, used_fallback,
+                 replaced);
 }
 
 chfsi_status chfsi_rayleigh_ritz(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh,

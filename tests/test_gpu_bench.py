@@ -28,6 +28,7 @@ def test_bench_single_gpu_line():
     assert d["value"] > 0 and d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
     assert d["roofline"]["bound"] == "tensor" and 0 < d["roofline"]["frac"] < 1.2
     assert "sm_mhz" in d["clocks"]
+    assert d["sequence"]["problems"] == 1 and d["sequence"]["converged"]
 
 
 @pytest.mark.parametrize("P", [2, 4])

@@ -11,8 +11,9 @@ import oracle as O
 from gen.configs import C4_INTERVAL, CONFIGS, c4_ramp
 
 pytestmark = pytest.mark.gpu
-# 3M variants (the default complex arithmetic, ids 200..204) and the 4M real-embedding variants (0..9)
-VARIANTS = ["200", "201", "202", "203", "204", "206", "207", "208", "210", "220", "227", "0", "1", "2", "3", "4", "5", "6", "7", "8", "9", "10", "11", "12", "13", "14", "15"]
+# every built K1 variant the step model can select: 3M (the default complex arithmetic, ids >= 200) and
+# 4M real embedding (ids < 100); the A/B-only variants are compiled with -DCHFSI_K1_AB only
+VARIANTS = ["200", "207", "208", "1", "3", "5", "6", "7", "9", "10", "11", "12", "13", "14"]
 
 
 def crand(rng, *shape):
@@ -214,15 +215,14 @@ def test_filter_degree_extremes(gpu_lib, ctx, deg_kind):
 
 
 @pytest.mark.parametrize("env,vid,mults", [("CHFSI_FILTER_VARIANT_Z3", "200", 3), ("CHFSI_FILTER_VARIANT", "7", 4),
-                                           ("CHFSI_FILTER_VARIANT_Z3", "210", 3), ("CHFSI_FILTER_VARIANT_Z3", "206", 3)])
+                                           ("CHFSI_FILTER_VARIANT_Z3", "207", 3)])
 def test_filter_stream_k_hybrid_schedule(gpu_lib, ctx, env, vid, mults):
     """Persistent schedule with a small stream-K remainder: n = 2000, k = 480 under a 128 x 48 tile is
     16 x 10 = 160 tiles on 148 CTAs (remainder 12 < 148 / 2). The default schedule folds one
     data-parallel wave into the stream-K tail (12 + 148 tail tiles, at most two contributors each);
     CHFSI_SK_HYBRID=0 keeps the plain split (12 tail tiles over all 148 CTAs). Both within the filter
     tolerance of the compact-WY closed form (App. A) and of each other (they only re-associate the k sum).
-    z210 (CTA pairs: 80 pair tiles on 74 cluster slots) and z206 (2 CTAs per SM: 320 tiles on 296 slots)
-    take the same hybrid over their own schedule units."""
+    z207 (64 x 64 tiles: 32 x 8 = 256 tiles, remainder 108) keeps the plain split."""
     n, k = 2000, 480
     w = G.wy(n, int(0.9 * n), 31)
     H = w.full()

@@ -95,6 +95,54 @@ def test_qr_householder_fallback(gpu_lib, ctx):
     assert np.abs(Q[:, :3] - Qo).max() <= 1e-12
 
 
+@pytest.mark.parametrize("case", ["duplicate", "zero", "in_locked_span", "two_dependent"])
+def test_qr_rank_deficiency_rule_vs_oracle(gpu_lib, ctx, case):
+    """R23 on both sides: a dependent active column is replaced by the R22 vector
+    (seed, stream (6 << 16) | column) and the block is orthonormalised again. The GPU result equals the
+    oracle's ora_orthonormalize (same replacement count), [X_L | Q] is orthonormal and X_L is untouched
+    -- including the Householder fallback with locked columns."""
+    rng = np.random.default_rng(21)
+    n, ka, seed = 300, 24, 77
+    nl = 0 if case == "duplicate" else 9
+    XL = np.linalg.qr(crand(rng, n, nl))[0] if nl else None
+    Y = crand(rng, n, ka)
+    if case == "duplicate":  # S:54
+        Y[:, 6] = Y[:, 5]
+    elif case == "zero":
+        Y[:, 6] = 0
+    elif case == "in_locked_span":
+        Y[:, 6] = XL @ crand(rng, nl)
+    else:
+        Y[:, 6] = XL @ crand(rng, nl)
+        Y[:, 17] = 2j * Y[:, 3]
+    full = Y if XL is None else np.hstack([XL, Y])
+    Yd = gpu_lib.to_colmajor(full)
+    fb, replaced = ctx.qr_ex(Yd, nlocked=nl, seed=seed)
+    Q = Yd.cpu().numpy()
+    Qo, ro = O.orthonormalize(Y, XL, seed=seed)
+    assert fb == 1 and replaced == ro == (2 if case == "two_dependent" else 1)
+    if nl:
+        assert np.array_equal(Q[:, :nl], XL)
+    assert np.abs(Q.conj().T @ Q - np.eye(nl + ka)).max() <= 1e-13
+    assert np.abs(Q[:, nl:] - Qo).max() <= 1e-11
+
+
+def test_solve_real_odd_n(gpu_lib, ctx):
+    """Real-symmetric solve on one rank with odd n (the H Q operand's TMA stride must be a
+    multiple of 16 bytes, so an odd leading dimension is re-strided): eigenvalues = the exact spectrum."""
+    n, nev, nex = 301, 12, 6
+    lam = np.sort(np.concatenate([np.linspace(-2.0, -1.0, 40), np.linspace(0.0, 10.0, n - 40)]))
+    rng = np.random.default_rng(4)
+    Qm, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    H = (Qm * lam) @ Qm.T
+    H = (H + H.T) / 2
+    Hd = gpu_lib.to_colmajor(H, real=True)
+    Xd = gpu_lib.to_colmajor(rng.standard_normal((n, nev + nex)), real=True)
+    out = ctx.solve_sequence(lambda ell: Hd, 1, Xd, nev, nex, 1e-10, deg_cap=30, seed=3, real=True)
+    assert out["status"] == 0
+    np.testing.assert_allclose(out["lam"][0], lam[:nev], rtol=1e-10)
+
+
 # ---- Rayleigh-Ritz (Alg 1 l7-9) ------------------------------------------------------------------------
 def test_rr_exact_subspace(gpu_lib, ctx):
     n = 400

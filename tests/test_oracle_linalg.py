@@ -319,3 +319,23 @@ def test_degree_acosh_rule_is_minimal():
     assert O.degree(1.0, 1e-10, 0.5, 36) == 36  # |t| <= 1 -> cap (R5)
     assert O.degree(1.0, 1e-10, 1.0001, 36) == 36  # clamped
     assert O.degree(1e-12, 1e-10, 3.0, 36) == 1  # already converged -> 1
+
+
+def test_rayleigh_quotients_exact_and_closed_form():
+    """ora_rayleigh_quotients: exact eigenpairs of H^(1) (generator) give rho = Lambda_i and zero
+    residual; for diagonal H, rho = sum d_r |x_r|^2 / ||x||^2 and the residual is ||(d - rho) x|| / ||x||
+    (closed forms evaluated entrywise)."""
+    n = 300
+    w = G.wy(n, 270, 41)
+    idx = [0, 1, 150, 299]
+    rho, ra = O.rayleigh_quotients(w.full(), w.eigvecs(idx))
+    np.testing.assert_allclose(rho, w.lam[idx], rtol=0, atol=1e-12)
+    assert ra.max() <= 1e-12
+    rng = np.random.default_rng(42)
+    d = rng.uniform(-2, 5, n)
+    X = crand(rng, n, 3)
+    rho, ra = O.rayleigh_quotients(np.diag(d).astype(complex), X)
+    a2 = np.abs(X) ** 2
+    rr = (d[:, None] * a2).sum(0) / a2.sum(0)
+    np.testing.assert_allclose(rho, rr, rtol=1e-13)
+    np.testing.assert_allclose(ra, np.linalg.norm((d[:, None] - rr) * X, axis=0) / np.linalg.norm(X, axis=0), rtol=1e-12)
