@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--exchange", default="allgather", choices=["allgather", "push"],
                     help="N > 1: per-step operand exchange (pipelined in-place allgather, or the filter "
                          "epilogue's peer push)")
+    ap.add_argument("--eig", default="refine", choices=["refine", "dense"],
+                    help="Rayleigh-Ritz k x k eigensolve: Jacobi-type refinement with dense fallback, or dense only")
     ap.add_argument("--zmul", type=int, default=3, choices=[3, 4],
                     help="complex filter arithmetic: 3 = Gauss 3M (default), 4 = 4M real embedding")
     ap.add_argument("--emulate-ranks", type=int, default=1,
@@ -363,6 +365,7 @@ def rank_main(args, cf, rank, world, local_rank, group):
 
     ctx = group.context(chfsi, local_rank, rank, world) if group else chfsi.Context(local_rank)
     ctx.set_complex_mult(args.zmul)
+    ctx.set_eigensolver(0 if args.eig == "refine" else 1)
     ctx.reserve(n, nloc, k)
     if world > 1 and args.exchange == "push":
         ctx.set_exchange(1)  # collective: maps every rank's operand buffers
@@ -517,6 +520,7 @@ def rank_main(args, cf, rank, world, local_rank, group):
                        "parallelism": (f"1-D row panels over {world} emulated ranks on one GPU" if args.emulate_ranks > 1
                                        else f"1-D row panels over {world} GPU(s)" if world > 1 else "single GPU"),
                        "exchange": args.exchange if world > 1 else None, "complex_mult": f"{args.zmul}M",
+                       "eigensolver": args.eig,
                        "l2": "inputs larger than L2 (H panel per problem >> 126 MB)"},
             "time_per_eigenproblem_s": ms / K / 1e3,
             "filter_kernel_tflops": filt_tf, "frac_of_peak": filt_tf * tensor_per_zmac / 8.0 / FP64_PEAK_TFLOPS,
@@ -526,7 +530,8 @@ def rank_main(args, cf, rank, world, local_rank, group):
             "filter_share_of_step": t_filter / (ms * 1e-3),
             "loops_per_problem": [r["loops"] for r in reps],
             "phase_s_per_problem": {ph: sum(r[f"t_{ph}"] for r in reps) / len(reps)
-                                    for ph in ("lanczos", "filter", "qr", "rr", "opt", "total")},
+                                    for ph in ("lanczos", "filter", "qr", "rr", "eig", "opt", "total")},
+            "eigensolves_per_problem": {"refined": [r["eig_refined"] for r in reps], "dense": [r["eig_dense"] for r in reps]},
             "matvecs_filter_per_problem": [r["matvecs_filter"] for r in reps],
             "converged": conv, "max_resid_over_tol": res_max / cf["tol"],
             "sequence": sequence,

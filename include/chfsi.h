@@ -83,6 +83,17 @@ int64_t chfsi_kernel_launches(chfsi_ctx ctx);
  * creation. Errors: CHFSI_ERR_ARG for a null ctx or mults not in {3, 4}. */
 chfsi_status chfsi_ctx_set_complex_mult(chfsi_ctx ctx, int32_t mults);
 
+/* The k x k Hermitian eigensolve of Rayleigh-Ritz (Alg 1 lines 7-9; the paper uses EleMRRR,
+ * P:969-971). mode 0 (default): the projected matrix G = Q^H H Q of a problem's later loops is nearly
+ * diagonal, and a Jacobi-type simultaneous refinement from X = I (every first-order rotation
+ * E_ij = (S_ij - lam_j M_ij)/(lam_j - lam_i) at once, S = X^H G X, M = X^H X, iterated to quadratic
+ * convergence; k^3 cuBLAS products) replaces the dense solve; it declines -- and the dense cuSOLVER
+ * ZHEEVD / DSYEVD runs -- when a coupling exceeds 0.3 of its gap or the iteration stops contracting.
+ * mode 1: always the dense solve. Results agree to rounding (eigenvalues to ~1e-15 ||G||); reports count
+ * the two paths (eig_refined / eig_dense). CHFSI_EIG=dense selects mode 1 at context creation.
+ * Errors: CHFSI_ERR_ARG for a null ctx or a mode not in {0, 1}. */
+chfsi_status chfsi_ctx_set_eigensolver(chfsi_ctx ctx, int32_t mode);
+
 /* nranks > 1 only, collective (every rank calls it): how the filter's next-step operand is exchanged
  * (BASELINE.json north_star: Y is rebuilt each degree step across the row panels).
  *  mode 0 (default): in-place allgather per column group on a communication stream, overlapped with the

@@ -25,7 +25,7 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_NOCONV", 4: "ERR_QR
           7: "ERR_NOMEM"}
 
 EXPORTS = ("chfsi_ctx_create", "chfsi_ctx_create_local", "chfsi_ctx_create_nccl", "chfsi_nccl_unique_id", "chfsi_ctx_reserve", "chfsi_ctx_destroy",
-           "chfsi_last_error", "chfsi_kernel_launches", "chfsi_ctx_set_pipeline", "chfsi_ctx_set_complex_mult", "chfsi_ctx_set_exchange", "chfsi_local_group_create", "chfsi_local_group_destroy",
+           "chfsi_last_error", "chfsi_kernel_launches", "chfsi_ctx_set_pipeline", "chfsi_ctx_set_complex_mult", "chfsi_ctx_set_eigensolver", "chfsi_ctx_set_exchange", "chfsi_local_group_create", "chfsi_local_group_destroy",
            "chfsi_filter", "chfsi_filter_real", "chfsi_lanczos_bounds", "chfsi_qr", "chfsi_qr_ex", "chfsi_rayleigh_ritz", "chfsi_solve_sequence",
            "chfsi_reduce_generalized", "chfsi_back_transform", "chfsi_reduce_generalized_panel", "chfsi_back_transform_panel",
            "chfsi_solve_batch", "chfsi_solve_sequence_real")
@@ -104,6 +104,8 @@ def lib():
         L.chfsi_ctx_set_complex_mult.argtypes = [vp, i32]
         L.chfsi_ctx_set_complex_mult.restype = ctypes.c_int
         L.chfsi_ctx_set_exchange.argtypes = [vp, i32]
+        L.chfsi_ctx_set_eigensolver.argtypes = [vp, i32]
+        L.chfsi_ctx_set_eigensolver.restype = ctypes.c_int
         L.chfsi_ctx_set_exchange.restype = ctypes.c_int
         L.chfsi_filter.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, i64, pi32, dbl, dbl, dbl, pi64]
         L.chfsi_filter_real.argtypes = [vp, i64, i64, i64, vp, i64, vp, i64, i64, pi32, dbl, dbl, dbl, pi64]
@@ -247,6 +249,11 @@ class Context:
         """Complex filter / H Q arithmetic: 3 = Gauss 3M (default), 4 = 4M real embedding
         (chfsi_ctx_set_complex_mult)."""
         self._check(lib().chfsi_ctx_set_complex_mult(self.h, mults))
+
+    def set_eigensolver(self, mode: int = 0):
+        """Rayleigh-Ritz k x k eigensolve: 0 = Jacobi-type refinement with the dense fallback (default),
+        1 = dense ZHEEVD only (chfsi_ctx_set_eigensolver)."""
+        self._check(lib().chfsi_ctx_set_eigensolver(self.h, mode))
 
     def set_exchange(self, mode: int):
         """nranks > 1, collective: 0 = pipelined allgather, 1 = peer push from the filter epilogue

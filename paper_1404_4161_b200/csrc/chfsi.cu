@@ -613,6 +613,7 @@ static chfsi_status ctx_create_impl(chfsi_ctx* out, int32_t device, void* cuda_s
   ctx->nccl_comm = nccl_comm;
   ctx->local_group = group;
   if (const char* zm = getenv("CHFSI_ZMUL")) ctx->zmul = atoi(zm) == 4 ? 4 : 3;
+  if (const char* em = getenv("CHFSI_EIG")) ctx->eig_mode = strcmp(em, "dense") == 0 ? 1 : 0;
   if (nccl_id) {
     memcpy(ctx->nccl_id, nccl_id, sizeof(ctx->nccl_id));
     ctx->nccl_id_valid = true;
@@ -686,13 +687,15 @@ void chfsi_ctx_destroy(chfsi_ctx ctx) {
   DevBuf* bufs[] = {&ctx->h3, &ctx->L0, &ctx->L1, &ctx->R0, &ctx->R1, &ctx->flag, &ctx->sk, &ctx->hpad, &ctx->w1, &ctx->w2, &ctx->w3, &ctx->w4,
                     &ctx->small1, &ctx->small2, &ctx->small3, &ctx->solver_ws, &ctx->devinfo, &ctx->lz,
                     &ctx->ya,    &ctx->xl,     &ctx->tb,     &ctx->idx,    &ctx->gw,     &ctx->gx,
-                    &ctx->qsave, &ctx->qrn};
+                    &ctx->qsave, &ctx->qrn,   &ctx->eigw};
   for (DevBuf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   for (cudaEvent_t ev : ctx->k1_events) cudaEventDestroy(ev);
   for (cudaEvent_t ev : ctx->grp_k) cudaEventDestroy(ev);
   for (cudaEvent_t ev : ctx->grp_ag) cudaEventDestroy(ev);
   if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+  for (cudaEvent_t ev : ctx->eig_ev)
+    if (ev) cudaEventDestroy(ev);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->cublas) cublasDestroy(ctx->cublas);
   if (ctx->cusolver) cusolverDnDestroy(ctx->cusolver);
@@ -707,6 +710,12 @@ int64_t chfsi_kernel_launches(chfsi_ctx ctx) { return ctx ? ctx->launches : 0; }
 chfsi_status chfsi_ctx_set_complex_mult(chfsi_ctx ctx, int32_t mults) {
   if (!ctx || (mults != 3 && mults != 4)) return CHFSI_ERR_ARG;
   ctx->zmul = mults;
+  return CHFSI_OK;
+}
+
+chfsi_status chfsi_ctx_set_eigensolver(chfsi_ctx ctx, int32_t mode) {
+  if (!ctx || (mode != 0 && mode != 1)) return CHFSI_ERR_ARG;
+  ctx->eig_mode = mode;
   return CHFSI_OK;
 }
 

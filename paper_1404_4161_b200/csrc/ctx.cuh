@@ -107,6 +107,12 @@ struct chfsi_ctx_s {
   chfsi::DevBuf lz;              // Lanczos basis
   chfsi::DevBuf ya, xl, tb, idx;  // solver: active block, locked block, filter block, column indices
   chfsi::DevBuf qsave, qrn;      // QR: the projected block (Householder / R23 restart), column norms
+  chfsi::DevBuf eigw;            // k x k eigensolve: refinement workspace (eig_refine.cu)
+  // Rayleigh-Ritz eigensolver: 0 = Jacobi-type refinement with the dense fallback, 1 = dense (ZHEEVD) only
+  int32_t eig_mode = 0;
+  int64_t eig_refined = 0, eig_dense = 0;  // eigensolves by each path (rank 0)
+  double eig_seconds = 0;                  // their CUDA-event time (rank 0)
+  cudaEvent_t eig_ev[2] = {nullptr, nullptr};
   chfsi::DevBuf gw, gx;          // generalised front / back end on row panels: n x n and n x nloc scratch
   chfsi::DevBuf host_pinned_dummy;
   std::vector<char> hbuf;        // host staging

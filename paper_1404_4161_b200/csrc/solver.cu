@@ -84,6 +84,8 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
                               double& lamk_io, double* lam_out, double* res_out, chfsi_report& rep, uint64_t seed) {
   const int64_t nev = o.nev, k = (int64_t)o.nev + o.nex;
   rep = chfsi_report{};
+  const int64_t eig_r0 = ctx->eig_refined, eig_d0 = ctx->eig_dense;
+  const double eig_t0 = ctx->eig_seconds;
   PhaseTimer tm(ctx->stream);
   auto t_all = tm.begin("chfsi: eigenproblem");
   const size_t blk = sizeof(double) * 2 * (size_t)nloc * k;
@@ -288,6 +290,9 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
   rep.t_rr = tm.acc[T_RR];
   rep.t_opt = tm.acc[T_OPT];
   rep.t_total = tm.acc[T_TOTAL];
+  rep.eig_refined = (int32_t)(ctx->eig_refined - eig_r0);
+  rep.eig_dense = (int32_t)(ctx->eig_dense - eig_d0);
+  rep.t_eig = ctx->eig_seconds - eig_t0;
   if (status == CHFSI_ERR_NOCONV) set_err(ctx, "ChFSI: max_loops reached before nev eigenpairs converged");
   return status;
 }

@@ -10,140 +10,12 @@
 #include <cmath>
 #include <vector>
 
+#include "blas_traits.cuh"
 #include "ctx.cuh"
 #include "small_kernels.cuh"
 #include "supporting.cuh"
 
 namespace chfsi {
-
-#define CUBLAS_TRY(ctx, call)                                                   \
-  do {                                                                          \
-    cublasStatus_t _s = (call);                                                 \
-    if (_s != CUBLAS_STATUS_SUCCESS) {                                          \
-      set_err(ctx, std::string(#call) + ": cuBLAS status " + std::to_string((int)_s)); \
-      return CHFSI_ERR_CUDA;                                                    \
-    }                                                                           \
-  } while (0)
-#define CUSOLVER_TRY(ctx, call)                                                 \
-  do {                                                                          \
-    cusolverStatus_t _s = (call);                                               \
-    if (_s != CUSOLVER_STATUS_SUCCESS) {                                        \
-      set_err(ctx, std::string(#call) + ": cuSOLVER status " + std::to_string((int)_s)); \
-      return CHFSI_ERR_CUDA;                                                    \
-    }                                                                           \
-  } while (0)
-#define TRY(x)                   \
-  do {                           \
-    chfsi_status _st = (x);      \
-    if (_st != CHFSI_OK) return _st; \
-  } while (0)
-
-// Scalar traits: complex Hermitian (cuDoubleComplex, the north-star path) or real symmetric (double,
-// SURVEY 8(f) NEXT-3). D is the element type of the library's small kernels.
-template <typename T>
-struct Sc;
-template <>
-struct Sc<cuDoubleComplex> {
-  using T = cuDoubleComplex;
-  using D = double2;
-  static constexpr int elem = 2;
-  static constexpr cublasOperation_t opH = CUBLAS_OP_C;
-  static T one() { return {1.0, 0.0}; }
-  static T zero() { return {0.0, 0.0}; }
-  static T mone() { return {-1.0, 0.0}; }
-  // the n k^2-class products of QR / Rayleigh-Ritz: cuBLAS ZGEMM, or its Gauss 3M form (ZGEMM3M) when the
-  // context runs the filter in 3M (the same arithmetic, 25 % fewer real multiplications)
-  static cublasStatus_t gemm(chfsi_ctx ctx, cublasOperation_t a, cublasOperation_t b, int m, int n, int k,
-                             const T* al, const T* A, int lda, const T* B, int ldb, const T* be, T* C, int ldc) {
-    if (ctx->zmul == 3) return cublasZgemm3m(ctx->cublas, a, b, m, n, k, al, A, lda, B, ldb, be, C, ldc);
-    return cublasZgemm(ctx->cublas, a, b, m, n, k, al, A, lda, B, ldb, be, C, ldc);
-  }
-  static cublasStatus_t gemv(cublasHandle_t h, cublasOperation_t a, int m, int n, const T* al, const T* A, int lda,
-                             const T* x, const T* be, T* y) {
-    return cublasZgemv(h, a, m, n, al, A, lda, x, 1, be, y, 1);
-  }
-  static cublasStatus_t trsm_ru(cublasHandle_t h, int m, int n, const T* R, int ldr, T* Y, int ldy) {
-    const T o = one();
-    return cublasZtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, m, n, &o, R, ldr,
-                       Y, ldy);
-  }
-  static cusolverStatus_t potrf_bs(cusolverDnHandle_t h, int n, T* A, int lda, int* lw) {
-    return cusolverDnZpotrf_bufferSize(h, CUBLAS_FILL_MODE_UPPER, n, A, lda, lw);
-  }
-  static cusolverStatus_t potrf(cusolverDnHandle_t h, int n, T* A, int lda, T* w, int lw, int* info) {
-    return cusolverDnZpotrf(h, CUBLAS_FILL_MODE_UPPER, n, A, lda, w, lw, info);
-  }
-  static cusolverStatus_t heevd_bs(cusolverDnHandle_t h, int n, T* A, int lda, double* W, int* lw) {
-    return cusolverDnZheevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n, A, lda, W, lw);
-  }
-  static cusolverStatus_t heevd(cusolverDnHandle_t h, int n, T* A, int lda, double* W, T* w, int lw, int* info) {
-    return cusolverDnZheevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n, A, lda, W, w, lw, info);
-  }
-  static cusolverStatus_t geqrf_bs(cusolverDnHandle_t h, int m, int n, T* A, int lda, int* lw) {
-    return cusolverDnZgeqrf_bufferSize(h, m, n, A, lda, lw);
-  }
-  static cusolverStatus_t geqrf(cusolverDnHandle_t h, int m, int n, T* A, int lda, T* tau, T* w, int lw, int* info) {
-    return cusolverDnZgeqrf(h, m, n, A, lda, tau, w, lw, info);
-  }
-  static cusolverStatus_t orgqr_bs(cusolverDnHandle_t h, int m, int n, T* A, int lda, const T* tau, int* lw) {
-    return cusolverDnZungqr_bufferSize(h, m, n, n, A, lda, tau, lw);
-  }
-  static cusolverStatus_t orgqr(cusolverDnHandle_t h, int m, int n, T* A, int lda, const T* tau, T* w, int lw,
-                                int* info) {
-    return cusolverDnZungqr(h, m, n, n, A, lda, tau, w, lw, info);
-  }
-  static double re(const T& x) { return x.x; }
-};
-template <>
-struct Sc<double> {
-  using T = double;
-  using D = double;
-  static constexpr int elem = 1;
-  static constexpr cublasOperation_t opH = CUBLAS_OP_T;
-  static T one() { return 1.0; }
-  static T zero() { return 0.0; }
-  static T mone() { return -1.0; }
-  static cublasStatus_t gemm(chfsi_ctx ctx, cublasOperation_t a, cublasOperation_t b, int m, int n, int k,
-                             const T* al, const T* A, int lda, const T* B, int ldb, const T* be, T* C, int ldc) {
-    return cublasDgemm(ctx->cublas, a, b, m, n, k, al, A, lda, B, ldb, be, C, ldc);
-  }
-  static cublasStatus_t gemv(cublasHandle_t h, cublasOperation_t a, int m, int n, const T* al, const T* A, int lda,
-                             const T* x, const T* be, T* y) {
-    return cublasDgemv(h, a, m, n, al, A, lda, x, 1, be, y, 1);
-  }
-  static cublasStatus_t trsm_ru(cublasHandle_t h, int m, int n, const T* R, int ldr, T* Y, int ldy) {
-    const T o = one();
-    return cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, m, n, &o, R, ldr,
-                       Y, ldy);
-  }
-  static cusolverStatus_t potrf_bs(cusolverDnHandle_t h, int n, T* A, int lda, int* lw) {
-    return cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_UPPER, n, A, lda, lw);
-  }
-  static cusolverStatus_t potrf(cusolverDnHandle_t h, int n, T* A, int lda, T* w, int lw, int* info) {
-    return cusolverDnDpotrf(h, CUBLAS_FILL_MODE_UPPER, n, A, lda, w, lw, info);
-  }
-  static cusolverStatus_t heevd_bs(cusolverDnHandle_t h, int n, T* A, int lda, double* W, int* lw) {
-    return cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n, A, lda, W, lw);
-  }
-  static cusolverStatus_t heevd(cusolverDnHandle_t h, int n, T* A, int lda, double* W, T* w, int lw, int* info) {
-    return cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n, A, lda, W, w, lw, info);
-  }
-  static cusolverStatus_t geqrf_bs(cusolverDnHandle_t h, int m, int n, T* A, int lda, int* lw) {
-    return cusolverDnDgeqrf_bufferSize(h, m, n, A, lda, lw);
-  }
-  static cusolverStatus_t geqrf(cusolverDnHandle_t h, int m, int n, T* A, int lda, T* tau, T* w, int lw, int* info) {
-    return cusolverDnDgeqrf(h, m, n, A, lda, tau, w, lw, info);
-  }
-  static cusolverStatus_t orgqr_bs(cusolverDnHandle_t h, int m, int n, T* A, int lda, const T* tau, int* lw) {
-    return cusolverDnDorgqr_bufferSize(h, m, n, n, A, lda, tau, lw);
-  }
-  static cusolverStatus_t orgqr(cusolverDnHandle_t h, int m, int n, T* A, int lda, const T* tau, T* w, int lw,
-                                int* info) {
-    return cusolverDnDorgqr(h, m, n, n, A, lda, tau, w, lw, info);
-  }
-  static double re(const T& x) { return x; }
-};
-
 
 // C (m x n, ldc) = A^H B with A (K x m), B (K x n) local rows, summed over ranks
 template <typename T>
@@ -413,10 +285,17 @@ chfsi_status qr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const vo
     TRY(ensure(ctx, ctx->qsave, eb * (size_t)nloc * ka));
     CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(ctx->qsave.ptr, eb * nloc, Y, eb * ldy, eb * nloc, ka,
                                           cudaMemcpyDeviceToDevice, ctx->stream));
-    // CholeskyQR2: S = Y^H Y = R^H R, Y <- Y R^{-1}, twice
+    // CholeskyQR2: S = Y^H Y = R^H R, Y <- Y R^{-1}, twice. diag(R) = diag(R_2) diag(R_1) estimates the
+    // Householder |R_jj| to about eps ||y_j|| (a dependent column gets R_1jj ~ sqrt(eps) ||y_j|| from the
+    // rounding of the Gram matrix and R_2jj ~ sqrt(eps) from the noise it leaves), so a column with
+    // diag(R)_jj <= 1e-10 nu_j -- 100x above R23's 1e-12 -- is sent to the Householder decision
+    std::vector<T> rd[2];
     for (int pass = 0; pass < 2 && ok; ++pass) {
       TRY(gram<T>(ctx, nloc, ka, ka, Y, ldy, Y, ldy, G, ka));
       CUSOLVER_TRY(ctx, S::potrf(ctx->cusolver, (int)ka, G, (int)ka, static_cast<T*>(ctx->solver_ws.ptr), lw, info));
+      rd[pass].resize(ka);
+      CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(rd[pass].data(), eb, G, eb * (ka + 1), eb, ka, cudaMemcpyDeviceToHost,
+                                            ctx->stream));
       int hinfo = 0;
       CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
       CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
@@ -426,6 +305,8 @@ chfsi_status qr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const vo
       }
       CUBLAS_TRY(ctx, S::trsm_ru(ctx->cublas, (int)nloc, (int)ka, G, (int)ka, Yt, (int)ldy));
     }
+    for (int64_t j = 0; j < ka && ok; ++j)
+      if (std::fabs(S::re(rd[0][j])) * std::fabs(S::re(rd[1][j])) <= 1e-10 * std::sqrt(nu2[j])) ok = false;
     if (ok) {  // orthogonality check ||Q^H Q - I||_max <= 1e-12
       TRY(gram<T>(ctx, nloc, ka, ka, Y, ldy, Y, ldy, G, ka));
       double* e = reinterpret_cast<double*>(info + 4);
@@ -506,6 +387,18 @@ chfsi_status rr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const vo
   // diagnostics (CHFSI_RR_LOG): how far the projected matrix is from diagonal (relative Frobenius mass of
   // the off-diagonal part), the quantity a Jacobi-type eigensolver would have to remove
   static const bool rr_log = getenv("CHFSI_RR_LOG") != nullptr;
+  static const char* rr_dump = getenv("CHFSI_RR_DUMP");  // directory: every projected matrix as raw column-major
+  if (rr_dump && ctx->rank == 0) {
+    static int dump_no = 0;
+    std::vector<T> hg((size_t)ka * ka);
+    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(hg.data(), G, sizeof(T) * hg.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    const std::string path = std::string(rr_dump) + "/g_" + std::to_string(dump_no++) + "_k" + std::to_string(ka) + ".bin";
+    if (FILE* f = fopen(path.c_str(), "wb")) {
+      fwrite(hg.data(), sizeof(T), hg.size(), f);
+      fclose(f);
+    }
+  }
   if (rr_log && ctx->rank == 0) {
     std::vector<T> hg((size_t)ka * ka);
     CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(hg.data(), G, sizeof(T) * hg.size(), cudaMemcpyDeviceToHost, ctx->stream));
@@ -524,10 +417,24 @@ chfsi_status rr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const vo
   // small dense eigensolve: once, on rank 0, broadcast (identical bits on every rank)
   CHFSI_CUDA_TRY(ctx, cudaMemsetAsync(info, 0, sizeof(double), ctx->stream));
   if (ctx->rank == 0) {
-    int lw = 0;
-    CUSOLVER_TRY(ctx, S::heevd_bs(ctx->cusolver, (int)ka, G, (int)ka, dmu, &lw));
-    TRY(ensure(ctx, ctx->solver_ws, eb * (size_t)std::max(lw, 1)));
-    CUSOLVER_TRY(ctx, S::heevd(ctx->cusolver, (int)ka, G, (int)ka, dmu, static_cast<T*>(ctx->solver_ws.ptr), lw, info));
+    for (auto& ev : ctx->eig_ev)
+      if (!ev) CHFSI_CUDA_TRY(ctx, cudaEventCreate(&ev));
+    CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->eig_ev[0], ctx->stream));
+    // the nearly diagonal G of a problem's later loops: Jacobi-type refinement (eig_refine.cu); otherwise
+    // (or when it declines) the dense ZHEEVD
+    bool refined = false;
+    int steps = 0;
+    if (ctx->eig_mode == 0) TRY(eig_refine<T>(ctx, ka, G, dmu, &refined, &steps));
+    if (refined) {
+      ctx->eig_refined++;
+    } else {
+      int lw = 0;
+      CUSOLVER_TRY(ctx, S::heevd_bs(ctx->cusolver, (int)ka, G, (int)ka, dmu, &lw));
+      TRY(ensure(ctx, ctx->solver_ws, eb * (size_t)std::max(lw, 1)));
+      CUSOLVER_TRY(ctx, S::heevd(ctx->cusolver, (int)ka, G, (int)ka, dmu, static_cast<T*>(ctx->solver_ws.ptr), lw, info));
+      ctx->eig_dense++;
+    }
+    CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->eig_ev[1], ctx->stream));
   }
   TRY(comm_bcast(ctx, reinterpret_cast<double*>(G), (size_t)S::elem * ka * ka, 0));
   TRY(comm_bcast(ctx, dmu, (size_t)ka, 0));
@@ -552,6 +459,11 @@ chfsi_status rr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const vo
   int hinfo = 0;
   CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->rank == 0) {
+    float ms = 0;
+    CHFSI_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->eig_ev[0], ctx->eig_ev[1]));
+    ctx->eig_seconds += 1e-3 * ms;
+  }
   if (hinfo != 0) {
     set_err(ctx, "zheevd failed (info " + std::to_string(hinfo) + ")");
     return CHFSI_ERR_CUDA;

@@ -29,4 +29,10 @@ template <typename T>
 chfsi_status rr_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, const void* Hp, int64_t ldh, void* Q,
                   int64_t ldq, int64_t ka, double normH, double* mu, double* resid);
 
+// k x k Hermitian eigensolve of Rayleigh-Ritz by the Jacobi-type refinement (eig_refine.cu). On success
+// (*done = true) G holds the eigenvectors (columns ascending by eigenvalue) and dmu (device) the
+// eigenvalues; otherwise G is untouched and the caller runs the dense eigensolve. *steps: steps taken.
+template <typename T>
+chfsi_status eig_refine(chfsi_ctx ctx, int64_t ka, T* G, double* dmu, bool* done, int* steps);
+
 }  // namespace chfsi

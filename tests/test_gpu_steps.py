@@ -175,6 +175,66 @@ def test_rr_vs_oracle(gpu_lib, ctx):
     np.testing.assert_allclose(res, ro_res, rtol=1e-8, atol=1e-15)
 
 
+@pytest.mark.parametrize("eps", [1e-9, 1e-4, 3e-3])
+def test_rr_refinement_eigensolver(gpu_lib, ctx, eps):
+    """The Jacobi-type refinement of the k x k eigensolve (chfsi_ctx_set_eigensolver mode 0) on a nearly
+    diagonal projected matrix: Q = exact eigenvectors of H^(1) mixed by exp(eps A), A anti-Hermitian, so G =
+    Q^H H Q has couplings ~eps. Ritz values agree with the dense ZHEEVD path (mode 1) and the oracle's
+    Jacobi (ora_rayleigh_ritz) to 1e-13, with the exact spectrum, and the Ritz vectors agree up to phase."""
+    import scipy.linalg
+
+    n, k = 700, 96
+    w = G.wy(n, 640, 51)
+    H = w.full()
+    rng = np.random.default_rng(52)
+    idx = sorted(rng.choice(n - 100, k, replace=False))
+    A = crand(rng, k, k)
+    A = (A - A.conj().T) / 2
+    Q = w.eigvecs(idx) @ scipy.linalg.expm(eps * A)
+    Hd = gpu_lib.to_colmajor(H)
+    out = {}
+    for mode in (0, 1):
+        ctx.set_eigensolver(mode)
+        Qd = gpu_lib.to_colmajor(Q)
+        ritz, res = ctx.rayleigh_ritz(Hd, Qd, normH=HNORM)
+        out[mode] = (ritz, Qd.cpu().numpy(), res)
+    ctx.set_eigensolver(0)
+    ro, Yo = O.rayleigh_ritz(H, Q)
+    for mode in (0, 1):
+        np.testing.assert_allclose(out[mode][0], ro, rtol=0, atol=1e-13)
+        np.testing.assert_allclose(out[mode][0], w.lam[idx], rtol=0, atol=1e-12)
+        ov = np.abs(np.sum(out[mode][1].conj() * Yo, axis=0))
+        assert np.abs(ov - 1).max() <= 1e-10
+        assert out[mode][2].max() <= 1e-12
+    np.testing.assert_allclose(out[0][0], out[1][0], rtol=0, atol=1e-13)
+
+
+def test_solve_uses_refinement_and_matches_dense(gpu_lib, ctx):
+    """A 3-problem sequence: the later loops' eigensolves run as the refinement (reports count them), and
+    the converged eigenvalues equal those of the dense-only solver (mode 1) to 1e-12 relative."""
+    cf = CONFIGS["c0"]
+    n, nev, nex = cf["n"], cf["nev"], cf["nex"]
+    w = G.wy(n, cf["nd"], cf["seed"])
+    H = w.full()
+    Hs = [gpu_lib.to_colmajor(H)]
+    for ell in (1, 2):
+        G.perturb(H, cf["seed"], ell, 1e-3 * HNORM)
+        Hs.append(gpu_lib.to_colmajor(H))
+    outs = {}
+    for mode in (0, 1):
+        ctx.set_eigensolver(mode)
+        Xd = gpu_lib.to_colmajor(G.start_basis(n, nev + nex, cf["seed"]))
+        outs[mode] = ctx.solve_sequence(lambda ell: Hs[ell], 3, Xd, nev, nex, cf["tol"], deg_cap=cf["cap"],
+                                        seed=cf["seed"])
+        assert outs[mode]["status"] == 0
+    ctx.set_eigensolver(0)
+    assert sum(r["eig_refined"] for r in outs[0]["reports"]) > 0
+    assert sum(r["eig_refined"] for r in outs[1]["reports"]) == 0
+    np.testing.assert_allclose(outs[0]["lam"], outs[1]["lam"], rtol=1e-12)
+    ev = np.linalg.eigvalsh(Hs[-1].cpu().numpy())[:nev]
+    np.testing.assert_allclose(outs[0]["lam"][-1], ev, rtol=1e-10)
+
+
 # ---- the sequence solver (Alg 1; Def 1) ---------------------------------------------------------------
 def test_solve_c0_exact_and_vs_oracle(gpu_lib, ctx):
     cf = CONFIGS["c0"]
