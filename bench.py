@@ -198,9 +198,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sequence", action="store_true",
                     help="skip the untimed whole-sequence pass (per-problem times incl. the random-start problem 1)")
-    ap.add_argument("--exchange", default="allgather", choices=["allgather", "push"],
-                    help="N > 1: per-step operand exchange (pipelined in-place allgather, or the filter "
-                         "epilogue's peer push)")
+    ap.add_argument("--exchange", default="push", choices=["allgather", "push"],
+                    help="N > 1: per-step operand exchange -- the filter epilogue's peer push (default: the "
+                         "exchange fused into K1, 8-16 %% faster than the pipelined allgather on emulated ranks, "
+                         "profiles/r02_exchange_probe.jsonl) or the pipelined in-place allgather")
     ap.add_argument("--eig", default="refine", choices=["refine", "dense"],
                     help="Rayleigh-Ritz k x k eigensolve: Jacobi-type refinement with dense fallback, or dense only")
     ap.add_argument("--zmul", type=int, default=3, choices=[3, 4],

@@ -439,6 +439,28 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
   if (st) return st;
   int nev_used = 0;
   std::vector<std::pair<int, int>> launch_log;  // (active columns, variant) per K1 launch
+  // timeline (CHFSI_TIMELINE): K1 intervals come from k1_events; exchanges get their own event pairs
+  static const char* tl_prefix = getenv("CHFSI_TIMELINE");
+  static const int tl_max = getenv("CHFSI_TIMELINE_CALLS") ? atoi(getenv("CHFSI_TIMELINE_CALLS")) : 1;
+  static const int tl_skip = getenv("CHFSI_TIMELINE_SKIP") ? atoi(getenv("CHFSI_TIMELINE_SKIP")) : 0;
+  if (tl_prefix) ctx->tl_seen++;
+  const bool tl = tl_prefix && ctx->tl_seen > tl_skip && ctx->tl_calls < tl_max;
+  struct TlRec {
+    int kind, g, i, ev;  // kind 0: K1 (ev indexes k1_events), 1: exchange (ev indexes tl_events)
+  };
+  std::vector<TlRec> tl_log;
+  int tl_used = 0;
+  if (tl) {
+    st = ensure_events(ctx, ctx->tl_events, (size_t)2 * (mk + 2) * G + 1, cudaEventDefault);
+    if (st) return st;
+    CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->tl_events[tl_used++], ctx->stream));  // time origin
+  }
+  auto tl_pair = [&](int g, int i) -> const cudaEvent_t* {
+    if (!tl) return nullptr;
+    tl_log.push_back({1, g, i, tl_used});
+    tl_used += 2;
+    return &ctx->tl_events[tl_used - 2];
+  };
   std::vector<char> plane_ok(G, 1);  // group's B operand carries a current 3M plane
   int64_t s = 0;  // active start s_i = #{j : deg[j] <= i}
   for (int i = 0; i < mk; ++i) {
@@ -530,6 +552,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used], ctx->stream));
       CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, z3k ? tmA3 : tmA, op.tm3, sp, ctx->stream));
       launch_log.emplace_back((int)ka, t.id);
+      if (tl) tl_log.push_back({0, g, i, nev_used});
       CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used + 1], ctx->stream));
       nev_used += 2;
       ctx->launches++;
@@ -539,7 +562,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       } else if (p > 1 && ka_next > 0) {  // complete step i+1's operand of this group behind the next group's K1
         CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->grp_k[g], ctx->stream));
         CHFSI_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm_stream, ctx->grp_k[g], 0));
-        st = comm_allgather_inplace(ctx, region(oth, g), (size_t)cw * ldp * ka_next, ctx->comm_stream);
+        st = comm_allgather_inplace(ctx, region(oth, g), (size_t)cw * ldp * ka_next, ctx->comm_stream, tl_pair(g, i));
         if (st) return st;
         CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->grp_ag[g], ctx->comm_stream));
       }
@@ -550,6 +573,22 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     CHFSI_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   }
   CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (tl) {  // one JSON line per interval, times in ms from the call's origin event
+    ctx->tl_calls++;
+    const std::string path = std::string(tl_prefix) + "_rank" + std::to_string(ctx->rank) + ".jsonl";
+    if (FILE* f = fopen(path.c_str(), "a")) {
+      for (const TlRec& r : tl_log) {
+        const cudaEvent_t* e = r.kind == 0 ? &ctx->k1_events[r.ev] : &ctx->tl_events[r.ev];
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, ctx->tl_events[0], e[0]);
+        cudaEventElapsedTime(&b, ctx->tl_events[0], e[1]);
+        fprintf(f, "{\"call\": %d, \"rank\": %d, \"kind\": \"%s\", \"group\": %d, \"step\": %d, \"t0\": %.4f, \"t1\": %.4f, "
+                   "\"sm_reserve\": %d, \"groups\": %d}\n",
+                ctx->tl_calls, ctx->rank, r.kind == 0 ? "k1" : "exchange", r.g, r.i, a, b, ctx->pipe_sm_reserve, G);
+      }
+      fclose(f);
+    }
+  }
   static const bool k1_log = getenv("CHFSI_K1_LOG") != nullptr;  // per-launch trace (diagnostics)
   for (int q = 0; q < nev_used; q += 2) {
     float ms = 0;
@@ -693,6 +732,7 @@ void chfsi_ctx_destroy(chfsi_ctx ctx) {
   for (cudaEvent_t ev : ctx->k1_events) cudaEventDestroy(ev);
   for (cudaEvent_t ev : ctx->grp_k) cudaEventDestroy(ev);
   for (cudaEvent_t ev : ctx->grp_ag) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : ctx->tl_events) cudaEventDestroy(ev);
   if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   for (cudaEvent_t ev : ctx->eig_ev)
     if (ev) cudaEventDestroy(ev);

@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -119,6 +120,19 @@ __global__ void sum_ranks_kernel(const double* const* src, int P, size_t count, 
   }
 }
 
+// SM-kernel allgather for the local group: chunk q of every peer's buffer into ours (grid-stride copy)
+struct GatherSrc {
+  const double* src[8];
+};
+__global__ void lg_gather_kernel(GatherSrc s, int P, int rank, size_t count, double* dst) {
+  const size_t total = count * (size_t)P;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const int q = (int)(t / count);
+    if (q == rank) continue;
+    dst[t] = s.src[q][t];
+  }
+}
+
 // publish `buf`, wait until every rank has published and its producer work is ordered before ours
 void lg_enter(chfsi_ctx ctx, const void* buf, cudaStream_t st) {
   chfsi_local_group g = ctx->comm->local;
@@ -141,22 +155,36 @@ void lg_exit(chfsi_ctx ctx, cudaStream_t st) {
 
 }  // namespace
 
-chfsi_status comm_allgather_inplace(chfsi_ctx ctx, double* buf, size_t count, cudaStream_t st) {
+chfsi_status comm_allgather_inplace(chfsi_ctx ctx, double* buf, size_t count, cudaStream_t st,
+                                    const cudaEvent_t* ev_move) {
   if (ctx->nranks == 1 || count == 0) return CHFSI_OK;
   if (!st) st = ctx->stream;
   if (ctx->comm->local) {
     chfsi_local_group g = ctx->comm->local;
     lg_enter(ctx, buf, st);
-    for (int q = 0; q < g->P; ++q) {
-      if (q == ctx->rank) continue;
-      const double* src = static_cast<const double*>(g->bufs[q]) + count * q;
-      CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(buf + count * q, src, count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (ev_move) CHFSI_CUDA_TRY(ctx, cudaEventRecord(ev_move[0], st));
+    if (g->coll_kernel && g->P <= 8) {
+      GatherSrc s{};
+      for (int q = 0; q < g->P; ++q) s.src[q] = static_cast<const double*>(g->bufs[q]);
+      lg_gather_kernel<<<g->coll_ctas, 512, 0, st>>>(s, g->P, ctx->rank, count, buf);
+      CHFSI_CUDA_TRY(ctx, cudaGetLastError());
+      ctx->launches++;
+    } else {
+      for (int q = 0; q < g->P; ++q) {
+        if (q == ctx->rank) continue;
+        const double* src = static_cast<const double*>(g->bufs[q]) + count * q;
+        CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(buf + count * q, src, count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      }
     }
+    if (ev_move) CHFSI_CUDA_TRY(ctx, cudaEventRecord(ev_move[1], st));
     lg_exit(ctx, st);
     return CHFSI_OK;
   }
-  return nccl_check(ctx, ctx->comm->allgather(buf + count * ctx->rank, buf, count, ncclDouble, ctx->comm->comm, st),
-                    "ncclAllGather");
+  if (ev_move) CHFSI_CUDA_TRY(ctx, cudaEventRecord(ev_move[0], st));
+  chfsi_status r = nccl_check(
+      ctx, ctx->comm->allgather(buf + count * ctx->rank, buf, count, ncclDouble, ctx->comm->comm, st), "ncclAllGather");
+  if (!r && ev_move) CHFSI_CUDA_TRY(ctx, cudaEventRecord(ev_move[1], st));
+  return r;
 }
 
 chfsi_status comm_allreduce_sum(chfsi_ctx ctx, double* buf, size_t count) {
@@ -349,6 +377,8 @@ chfsi_status chfsi_local_group_create(chfsi_local_group* out, int32_t nranks) {
   if (!out || nranks < 1) return CHFSI_ERR_ARG;
   chfsi_local_group g = new chfsi_local_group_s();
   g->P = nranks;
+  if (const char* m = getenv("CHFSI_LG_COLL")) g->coll_kernel = strcmp(m, "kernel") == 0;
+  if (const char* c = getenv("CHFSI_LG_CTAS")) g->coll_ctas = std::max(1, atoi(c));
   g->bufs.assign(nranks, nullptr);
   g->ready.assign(nranks, nullptr);
   g->done.assign(nranks, nullptr);

@@ -23,6 +23,11 @@ struct chfsi_local_group_s {
   long generation = 0;
   std::vector<const void*> bufs;
   std::vector<cudaEvent_t> ready, done;
+  // collectives of the group: copy engines (cudaMemcpyAsync, default) or an SM copy kernel of coll_ctas
+  // thread blocks -- the way NCCL moves data, so it competes with the filter kernel for SMs
+  // (CHFSI_LG_COLL=kernel, CHFSI_LG_CTAS; the sm_reserve measurement of DESIGN.md 9)
+  bool coll_kernel = false;
+  int coll_ctas = 16;
   std::vector<void*> R0s, R1s;  // peer push: every rank's packed operand buffers (same device)
   std::vector<size_t> Rbytes;
   void barrier() {
@@ -81,6 +86,11 @@ struct chfsi_ctx_s {
   std::vector<void*> ipc_opened;          // peer mappings to close (cudaIpcCloseMemHandle)
   int32_t pipe_group_cols = 128;
   int32_t pipe_sm_reserve = 0;
+  // timeline of the p > 1 filter pipeline (CHFSI_TIMELINE=<prefix>): CUDA-event intervals of every K1
+  // launch and every column group's exchange of the first CHFSI_TIMELINE_CALLS (default 1) filter calls,
+  // written to <prefix>_rank<r>.jsonl
+  std::vector<cudaEvent_t> tl_events;
+  int tl_calls = 0, tl_seen = 0;  // calls written / filter calls seen (CHFSI_TIMELINE_SKIP skips the first)
   cudaStream_t comm_stream = nullptr;
   std::vector<cudaEvent_t> grp_k, grp_ag;  // per group: K1 done (stream), allgather done (comm_stream)
   cudaEvent_t join_ev = nullptr;
@@ -141,7 +151,10 @@ chfsi_status comm_init(chfsi_ctx ctx);
 void comm_destroy(chfsi_ctx ctx);
 // in-place allgather: buf holds nranks chunks of `count` doubles; chunk `rank` is the send part.
 // Enqueued on `st` (nullptr: the ctx stream).
-chfsi_status comm_allgather_inplace(chfsi_ctx ctx, double* buf, size_t count, cudaStream_t st = nullptr);
+// ev_move (nullable, timeline): two events recorded on `st` around the data movement itself (after the
+// wait for the peers' data to exist)
+chfsi_status comm_allgather_inplace(chfsi_ctx ctx, double* buf, size_t count, cudaStream_t st = nullptr,
+                                    const cudaEvent_t* ev_move = nullptr);
 chfsi_status comm_allreduce_sum(chfsi_ctx ctx, double* buf, size_t count);
 chfsi_status comm_bcast(chfsi_ctx ctx, double* buf, size_t count, int root);
 // every rank's work enqueued on `st` before the call is complete before any rank's later work on `st`

@@ -38,7 +38,7 @@ def test_bench_emulated_ranks(P):
     assert d["converged"] and d["max_resid_over_tol"] <= 1.0
 
 
-def test_bench_emulated_ranks_push():
-    d = bench("--emulate-ranks", "2", "--no-e2e", "--exchange", "push")
-    assert d["config"]["exchange"] == "push"
+def test_bench_emulated_ranks_allgather():
+    d = bench("--emulate-ranks", "2", "--no-e2e", "--exchange", "allgather")
+    assert d["config"]["exchange"] == "allgather"
     assert d["converged"] and d["max_resid_over_tol"] <= 1.0
