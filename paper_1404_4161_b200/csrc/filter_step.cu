@@ -1,5 +1,7 @@
 // filter_step.cu -- instantiations and launcher of K1 (see filter_step.cuh).
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "filter_step_launch.cuh"
 
@@ -72,9 +74,9 @@ constexpr Variant kVariantsReal[] = {
 
 // Model time of one step of `ncols` active columns over `nrows` rows for variant V, in units of a
 // full-efficiency 4M column-row (8 n flops at 34.9 TF/s):
-//  compute: the balanced N split gives the N tiles `per` or `per - 1` warp-column units; the persistent
-//           schedule hands out whole tiles (stream-K splits by k-iterations, not by work), so every
-//           tile is charged as the widest one (tn x per units) -- uneven splits cost their imbalance;
+//  compute: the balanced N split gives the N tiles `per` or `per - 1` warp-column units; the work-
+//           weighted persistent schedule charges the average tile (units / tn + woff per iteration,
+//           against per + woff for a full one);
 //           active warps in a tile cover latency as g(warps): >= 12 -> 1, 8..11 -> 0.85, 4..7 -> 0.6,
 //           relative to the variant's own warp count (its measured eff already includes that);
 //           `speed` = the family's best full-width rate relative to 4M (3M: 45.5 / 34.9)
@@ -82,6 +84,8 @@ constexpr Variant kVariantsReal[] = {
 //           tile), `hbm_cols` = the column count at which the family's compute time equals its H
 //           stream at ~5.9 TB/s (4M: 16 B / entry -> 11.8; 3M: 24 B / entry -> 17.7)
 // Calibrated on profiles/r01_mid_width_variants.log and r01_narrow_variants.log.
+constexpr double kSkWoff = 0.75;  // per-iteration cost of a tile's stage traffic, in column units (measured A/B)
+
 static double warp_cover(int warps) { return warps >= 12 ? 1.0 : warps >= 8 ? 0.85 : warps >= 4 ? 0.6 : 0.4; }
 
 static double step_cost(const Variant& V, int64_t nrows, int64_t ncols, double speed, double hbm_cols) {
@@ -92,7 +96,10 @@ static double step_cost(const Variant& V, int64_t nrows, int64_t ncols, double s
   const int warps = V.threads / 32;
   const int warps_m = warps / (V.bnc / V.wnc);
   const double cover = warp_cover((int)per * warps_m) / warp_cover(warps);
-  const double cols = (double)(tn * per * V.wnc);
+  // work-weighted stream-K (schedule_filter_step): the step costs the average tile, (units / tn + woff)
+  // per iteration, against a full tile's (per + woff); without weighting every tile costs the widest
+  const double fill = ((double)units / (double)tn + kSkWoff) / ((double)per + kSkWoff);
+  const double cols = (double)(tn * per * V.wnc) * (units % tn ? fill : 1.0);
   const double rows = (double)tm * V.bm;
   const double compute = rows * cols / (V.eff * cover * speed);
   const double memory = rows * hbm_cols * (1.0 + 0.25 * (double)(tn - 1));
@@ -168,6 +175,55 @@ void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
   p.dp_units = (int32_t)dp;
   p.tail_tile0 = (int32_t)(p.dp_units * grid);
   p.tail_iters = (tiles - p.tail_tile0) * p.num_kt;
+  // Work-weighted stream-K. The balanced N split gives tile column n either `base + 1` or `base` active
+  // column units; an iteration's cost is modelled as (units + woff) -- a warp with no units skips its
+  // MMAs, while the stage's TMA and barrier work is paid regardless (woff, in units). With the data-
+  // parallel tiles assigned c, c + grid, ... a CTA can own only full-unit tiles (e.g. every even CTA
+  // when tn = 2), so equal iteration counts leave the kernel as slow as if every tile were full. The
+  // tail ranges compensate: each CTA gets (total work / grid - its data-parallel work) of the tail.
+  // CHFSI_SK_WEIGHT=0 restores the equal split; CHFSI_SK_WOFF sets woff (A/B hooks, read per call).
+  const int64_t KT = p.num_kt, tail_tiles = tiles - p.tail_tile0;
+  const int64_t ntn = tn / cl;  // schedule tile columns
+  const int64_t U = p.units_n, base = U / tn, extra = U % tn;
+  const char* we = getenv("CHFSI_SK_WEIGHT");
+  const char* wo = getenv("CHFSI_SK_WOFF");
+  const bool weighted = !(we && we[0] == '0') && cl == 1 && extra != 0;
+  const double woff = wo ? atof(wo) : kSkWoff;
+  auto cost = [&](int64_t tile) {  // per-iteration cost of schedule tile `tile`
+    const int64_t n = tile % ntn;
+    return (double)(base + (n < extra ? 1 : 0)) + woff;
+  };
+  p.sk_bounds[0] = 0;
+  if (!weighted || tail_tiles == 0) {
+    for (int64_t c = 1; c <= grid; ++c) p.sk_bounds[c] = (int32_t)((c * p.tail_iters) / grid);
+    return;
+  }
+  std::vector<double> dpw(grid, 0.0);
+  double total = 0.0;
+  for (int64_t c = 0; c < grid; ++c) {
+    for (int64_t r = 0; r < dp; ++r) dpw[c] += cost(c + r * grid) * (double)KT;
+    total += dpw[c];
+  }
+  double tail_work = 0.0;
+  for (int64_t u = 0; u < tail_tiles; ++u) tail_work += cost(p.tail_tile0 + u) * (double)KT;
+  total += tail_work;
+  const double target = total / (double)grid;
+  double want_sum = 0.0;
+  std::vector<double> want(grid);
+  for (int64_t c = 0; c < grid; ++c) want_sum += (want[c] = std::max(0.0, target - dpw[c]));
+  // walk the tail iterations, closing CTA c's range once its (normalised) share of the work is reached
+  int64_t g = 0;           // tail iteration cursor
+  double acc = 0.0, goal = 0.0;
+  for (int64_t c = 0; c < grid; ++c) {
+    goal += want[c] * tail_work / want_sum;
+    while (g < p.tail_iters) {
+      const double w = cost(p.tail_tile0 + g / KT);
+      if (acc + 0.5 * w > goal) break;  // the iteration goes to whichever side it overlaps more
+      acc += w;
+      ++g;
+    }
+    p.sk_bounds[c + 1] = (int32_t)(c + 1 == grid ? p.tail_iters : g);
+  }
 }
 
 size_t filter_partials_doubles(const TileChoice& t, int num_sms) {

@@ -31,18 +31,22 @@ struct StepParams {
   int32_t col_end;      // k (one past the last active column)
   int32_t fin_end;      // columns [col0, fin_end) finish at this step and go to `out`
   int32_t b_col0;       // B-operand column coordinate of complex column col0
-  int32_t flags;        // 1: read y_cur (c != 0), 2: read y_prev (b != 0)
+  int32_t flags;        // 1: read y_cur (c != 0), 2: read y_prev (b != 0), 16: early (non-blocking) stage refill
   // persistent schedule (host-computed, see schedule_filter_step): tiles are numbered n-fastest;
   // CTA c owns the data-parallel tiles c, c + grid, ..., c + (dp_units - 1) grid, then the
-  // stream-K iterations [c*tail_iters/grid, (c+1)*tail_iters/grid) of the tail tiles
-  // tail_tile0.. (each tile = num_kt iterations); a split tile is finished by the last of its
-  // contributors to arrive (ticket), which sums the partial accumulators in k order.
+  // stream-K iterations [sk_bounds[c], sk_bounds[c+1]) of the tail tiles tail_tile0.. (each tile =
+  // num_kt iterations); a split tile is finished by the last of its contributors to arrive (ticket),
+  // which sums the partial accumulators in k order. The bounds balance WORK, not iterations: an
+  // iteration of a tile with fewer active column units is cheaper, and a CTA whose data-parallel
+  // tiles carry less work takes a larger share of the tail (work-weighted stream-K).
   int32_t tiles_n;      // N tiles
   int32_t units_n;      // WNC-wide column units of the active block, split evenly over the N tiles
   int32_t grid;         // CTAs
   int32_t dp_units;     // full tiles per CTA
   int32_t tail_tile0;   // first stream-K tile
   int64_t tail_iters;   // (tiles - tail_tile0) * num_kt
+  static constexpr int kMaxGrid = 296;  // schedule ids (CTAs, or clusters) a launch may use
+  int32_t sk_bounds[kMaxGrid + 1];      // tail iteration ranges per CTA, non-decreasing, [0] = 0, [grid] = tail_iters
   double* partials;     // 2 slots per CTA
   int* tickets;         // one per tail tile, zero between launches
   double a, b, c;       // Y_{i+1} = a (acc - c y_cur) - b y_prev
@@ -124,11 +128,19 @@ __device__ __forceinline__ uint32_t swz64(int row, int chunk) {
   return static_cast<uint32_t>(row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4));
 }
 
-// first iteration of CTA c in the stream-K tail (balanced integer split)
-__device__ __forceinline__ int64_t sk_start(int64_t c, int64_t iters, int64_t grid) { return (c * iters) / grid; }
-// CTA whose tail range contains iteration g
-__device__ __forceinline__ int64_t sk_owner(int64_t g, int64_t iters, int64_t grid) {
-  return ((g + 1) * grid - 1) / iters;
+// first iteration of CTA c in the stream-K tail
+__device__ __forceinline__ int64_t sk_start(const StepParams& p, int64_t c) { return p.sk_bounds[c]; }
+// CTA whose (non-empty) tail range contains iteration g: the last c with sk_bounds[c] <= g
+__device__ __forceinline__ int64_t sk_owner(const StepParams& p, int64_t g) {
+  int lo = 0, hi = p.grid - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (p.sk_bounds[mid] <= g)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
 }
 
 // balanced N split: N tile i covers column units [i*(U/T) + min(i, U%T), ...) of width U/T (+1 for
@@ -191,8 +203,8 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     }
   };
   const int KT = p.num_kt;
-  const int64_t t_beg = sk_start(cta, p.tail_iters, p.grid);
-  const int64_t t_end = sk_start(cta + 1, p.tail_iters, p.grid);
+  const int64_t t_beg = sk_start(p, cta);
+  const int64_t t_end = sk_start(p, cta + 1);
   const int64_t dp_iters = (int64_t)p.dp_units * KT;
   const int64_t my_iters = dp_iters + (t_end - t_beg);
 
@@ -466,6 +478,15 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     const bool warp_active = wn < nu;
     for (int kt = kbeg; kt < kend; ++kt, ++j) {
       const int s = stage;
+      // early refill: if every warp has already released the stage of iteration j - 1, thread 0 refills
+      // it now (one iteration more of TMA lead time) instead of after computing iteration j; a
+      // non-blocking test, so thread 0 never waits for the slower warps here
+      bool refilled = false;
+      if ((p.flags & 16) && threadIdx.x == 0 && j >= 1 && *(volatile int64_t*)&pc_j < my_iters &&
+          mbar_test(&empty[pc_stage], (s == 0) ? (phase ^ 1u) : phase)) {
+        produce();
+        refilled = true;
+      }
       mbar_wait(&full[s], phase);
       const uint8_t* sa = smem + s * Cfg::kStageBytes;
       const uint8_t* sb = sa + Cfg::kABytes;
@@ -569,7 +590,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
         }
       }
       // refill the stage of iteration j - 1 (stage pc_stage, phase of j - 1) with iteration pc_j
-      if (threadIdx.x == 0 && j >= 1 && *(volatile int64_t*)&pc_j < my_iters) {
+      if (threadIdx.x == 0 && j >= 1 && !refilled && *(volatile int64_t*)&pc_j < my_iters) {
         const uint32_t prev_phase = (s == 0) ? (phase ^ 1u) : phase;
         mbar_wait(&empty[pc_stage], prev_phase);
         produce();
@@ -600,18 +621,18 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
             __stcg(mine + (((ps * Cfg::kMT + i) * Cfg::kNT + jj) * 2 + e) * Cfg::kThreads + threadIdx.x, acc_ref(ps, i, jj, e));
     __threadfence();
     __syncthreads();
-    const int64_t c_lo = sk_owner(U0, p.tail_iters, p.grid), c_hi = sk_owner(U1 - 1, p.tail_iters, p.grid);
+    const int64_t c_lo = sk_owner(p, U0), c_hi = sk_owner(p, U1 - 1);
     int nseg = 0;
     for (int64_t c = c_lo; c <= c_hi; ++c)
-      if (sk_start(c + 1, p.tail_iters, p.grid) > sk_start(c, p.tail_iters, p.grid)) ++nseg;
+      if (sk_start(p, c + 1) > sk_start(p, c)) ++nseg;
     if (threadIdx.x == 0) s_ticket = atomicAdd(&p.tickets[u * CL + crank], 1);
     __syncthreads();
     if (s_ticket != nseg - 1) continue;  // not the last contributor
     __threadfence();
     zero_acc();
     for (int64_t c = c_lo; c <= c_hi; ++c) {  // fixed k order: deterministic sum
-      const int64_t cs = sk_start(c, p.tail_iters, p.grid);
-      if (sk_start(c + 1, p.tail_iters, p.grid) <= cs) continue;
+      const int64_t cs = sk_start(p, c);
+      if (sk_start(p, c + 1) <= cs) continue;
       const int slot = (cs / KT == u) ? 0 : 1;
       const double* src = p.partials + (((c * CL + crank) * 2 + slot) * kAcc) * (int64_t)Cfg::kThreads;
 #pragma unroll

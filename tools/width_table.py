@@ -1,6 +1,7 @@
 """Measure every 3M tile variant of K1 over the active widths a ChFSI solve visits (n = 13000, widths
-28..640 step 4, 2 filter steps each) and print, per width, the variant times (JSON lines). The result
-calibrates the variant choice of pick_tile for large panels (profiles/r01_width_table.jsonl)."""
+28..640, step 4 or argv[2], 2 filter steps each) and print, per width, the time of every built variant
+and of the step model's own choice ("auto"). The result calibrates pick_tile for large panels
+(profiles/r01_width_table.jsonl, r02_width_table.jsonl)."""
 import json
 import os
 import sys
@@ -13,13 +14,14 @@ import paper_1404_4161_b200 as chfsi  # noqa: E402
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 13000
-    variants = [200, 201, 203, 207, 208]
+    variants = [200, 207, 208]
+    step = int(sys.argv[2]) if len(sys.argv) > 2 else 4
     torch.manual_seed(0)
     H = chfsi.colmajor(n, n)
     H.copy_(torch.randn(n, n, dtype=torch.complex128, device="cuda") / (2 * n) ** 0.5)
     ctx = chfsi.Context(0)
     Y0 = torch.randn(n, 640, dtype=torch.complex128, device="cuda")
-    for k in range(28, 641, 4):
+    for k in range(28, 641, step):
         Yk = chfsi.colmajor(n, k)
         row = {"n": n, "k": k}
         for v in variants:
@@ -36,6 +38,17 @@ def main():
                 best = min(best, e0.elapsed_time(e1))
             row[str(v)] = best
         os.environ.pop("CHFSI_FILTER_VARIANT_Z3", None)
+        best = 1e30  # the step model's own choice
+        for _ in range(3):
+            Yk.copy_(Y0[:, :k])
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            ctx.filter(H, Yk, [2] * k, -2.2, 0.6, 1.6)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        row["auto"] = best
         print(json.dumps(row), flush=True)
     ctx.close()
 
