@@ -97,11 +97,6 @@ chfsi_status make_tmap_3d(chfsi_ctx ctx, CUtensorMap* m, const void* base, int64
 
 static inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-// K1's early (non-blocking) stage refill; CHFSI_EARLY_REFILL=0/1 (read per call: A/B hook)
-static bool early_refill() {
-  const char* e = getenv("CHFSI_EARLY_REFILL");
-  return e && e[0] == '1';
-}
 
 chfsi_status sk_workspace(chfsi_ctx ctx, const TileChoice& t, StepParams& p) {
   const size_t tick_bytes = sizeof(int) * kMaxTailTickets;  // >= tail tiles x cluster ranks (schedule_filter_step)
@@ -318,7 +313,6 @@ chfsi_status hmul_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
   sp.c = 0.0;
   sp.out = static_cast<double2*>(out);
   sp.ld_out = ldo;
-  if (early_refill()) sp.flags |= 16;
   schedule_filter_step(t, ctx->num_sms, sp);
   st = sk_workspace(ctx, t, sp);
   if (st) return st;
@@ -551,7 +545,6 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
         sp.y3_off_r = 2 * ldp;
       }
       sp.nonfinite = check_finite ? flag : nullptr;
-      if (early_refill()) sp.flags |= 16;
       schedule_filter_step(t, sms, sp);
       st = sk_workspace(ctx, t, sp);
       if (st) return st;

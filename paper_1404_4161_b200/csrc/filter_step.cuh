@@ -31,7 +31,7 @@ struct StepParams {
   int32_t col_end;      // k (one past the last active column)
   int32_t fin_end;      // columns [col0, fin_end) finish at this step and go to `out`
   int32_t b_col0;       // B-operand column coordinate of complex column col0
-  int32_t flags;        // 1: read y_cur (c != 0), 2: read y_prev (b != 0), 16: early (non-blocking) stage refill
+  int32_t flags;        // 1: read y_cur (c != 0), 2: read y_prev (b != 0)
   // persistent schedule (host-computed, see schedule_filter_step): tiles are numbered n-fastest;
   // CTA c owns the data-parallel tiles c, c + grid, ..., c + (dp_units - 1) grid, then the
   // stream-K iterations [sk_bounds[c], sk_bounds[c+1]) of the tail tiles tail_tile0.. (each tile =
@@ -478,15 +478,6 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     const bool warp_active = wn < nu;
     for (int kt = kbeg; kt < kend; ++kt, ++j) {
       const int s = stage;
-      // early refill: if every warp has already released the stage of iteration j - 1, thread 0 refills
-      // it now (one iteration more of TMA lead time) instead of after computing iteration j; a
-      // non-blocking test, so thread 0 never waits for the slower warps here
-      bool refilled = false;
-      if ((p.flags & 16) && threadIdx.x == 0 && j >= 1 && *(volatile int64_t*)&pc_j < my_iters &&
-          mbar_test(&empty[pc_stage], (s == 0) ? (phase ^ 1u) : phase)) {
-        produce();
-        refilled = true;
-      }
       mbar_wait(&full[s], phase);
       const uint8_t* sa = smem + s * Cfg::kStageBytes;
       const uint8_t* sb = sa + Cfg::kABytes;
@@ -590,7 +581,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
         }
       }
       // refill the stage of iteration j - 1 (stage pc_stage, phase of j - 1) with iteration pc_j
-      if (threadIdx.x == 0 && j >= 1 && !refilled && *(volatile int64_t*)&pc_j < my_iters) {
+      if (threadIdx.x == 0 && j >= 1 && *(volatile int64_t*)&pc_j < my_iters) {
         const uint32_t prev_phase = (s == 0) ? (phase ^ 1u) : phase;
         mbar_wait(&empty[pc_stage], prev_phase);
         produce();
