@@ -163,6 +163,15 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
   while (rep.loops < o.max_loops) {
     const int64_t ka = k - nl;
     const double c = 0.5 * (alpha + beta), e = 0.5 * (beta - alpha);
+    // the damped interval [alpha, beta] must be non-empty (Alg 2): Ritz values stay below the
+    // Lanczos bound beta in exact arithmetic, so this only trips on a broken input (lambda_1 = alpha, e.g. a
+    // k-fold degenerate spectrum, is fine: sigma_1 = -1)
+    if (!(e > 0.0) || !std::isfinite(c) || !(lam1 <= alpha)) {
+      set_err(ctx, "ChFSI: filter interval collapsed (lambda_1 = " + std::to_string(lam1) + ", alpha = " +
+                       std::to_string(alpha) + ", beta = " + std::to_string(beta) + ")");
+      status = CHFSI_ERR_NOCONV;
+      break;
+    }
     // R6: stable ascending sort of the active columns by degree
     std::vector<int> perm(ka);
     std::iota(perm.begin(), perm.end(), 0);
@@ -293,7 +302,8 @@ static chfsi_status solve_one(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nl
   rep.eig_refined = (int32_t)(ctx->eig_refined - eig_r0);
   rep.eig_dense = (int32_t)(ctx->eig_dense - eig_d0);
   rep.t_eig = ctx->eig_seconds - eig_t0;
-  if (status == CHFSI_ERR_NOCONV) set_err(ctx, "ChFSI: max_loops reached before nev eigenpairs converged");
+  if (status == CHFSI_ERR_NOCONV && ctx->err.empty())
+    set_err(ctx, "ChFSI: max_loops reached before nev eigenpairs converged");
   return status;
 }
 
