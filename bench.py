@@ -438,8 +438,11 @@ def rank_main(args, cf, rank, world, local_rank, group):
     t_k1 = rmax(sum(r["t_filter_kernel"] for r in reps))
     k1_launches = sum(r["filter_launches"] for r in reps)
     value = flops / (ms * 1e-3) / 1e12
-    filt_tf = flops / t_filter / 1e12  # whole filter calls (incl. the Y -> state copy, finite check)
-    k1_tf = flops / t_k1 / 1e12        # inside the K1 launches only
+    # per-GPU kernel rates: every rank executes 1/world of the filter flops (its row panel) in its own
+    # K1 launches (emulated ranks share one GPU: their kernel intervals overlap, so no per-GPU rate exists)
+    gpus = 1 if args.emulate_ranks > 1 else world
+    filt_tf = flops / gpus / t_filter / 1e12  # whole filter calls (incl. the Y -> state copy, finite check)
+    k1_tf = flops / gpus / t_k1 / 1e12        # inside the K1 launches only
     e2e = None
     if not args.no_e2e:
         out2, ms2, _, _ = run_pass(True)
@@ -491,12 +494,14 @@ def rank_main(args, cf, rank, world, local_rank, group):
                 "frac": k1_tensor_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
                 "kernel": f"K1 filter_step_kernel ({args.zmul}M complex arithmetic, DMMA.8x8x4, TMA, persistent stream-K)",
                 "launches": k1_launches, "avg_launch_ms": 1e3 * t_k1 / max(k1_launches, 1),
-                "flops_per_launch": flops * tensor_per_zmac / 8.0 / max(k1_launches, 1),
+                "flops_per_launch": flops / gpus * tensor_per_zmac / 8.0 / max(k1_launches, 1),
                 "achieved_def": (f"{tensor_per_zmac:g} n^2 sum(deg) (the real FP64 tensor flops of the {args.zmul}M "
                                  "complex product) over the timed problems / sum of CUDA-event times of the K1 launches"),
                 "achieved_zgemm_equivalent": k1_tf, "traffic_launch": traffic_info,
                 "peak_source": "measured FP64 DMMA peak (register-only DMMA loop, 1965 MHz), profiles/r01_fp64_peaks.txt"}
 
+    if args.emulate_ranks > 1:  # P ranks on one GPU: the launches of different ranks overlap in time
+        roofline = None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # a bounded sample of the same workload (~10 s of the oracle on the box's host cores)
@@ -524,7 +529,8 @@ def rank_main(args, cf, rank, world, local_rank, group):
                        "eigensolver": args.eig,
                        "l2": "inputs larger than L2 (H panel per problem >> 126 MB)"},
             "time_per_eigenproblem_s": ms / K / 1e3,
-            "filter_kernel_tflops": filt_tf, "frac_of_peak": filt_tf * tensor_per_zmac / 8.0 / FP64_PEAK_TFLOPS,
+            "filter_kernel_tflops": filt_tf if args.emulate_ranks == 1 else None,
+            "frac_of_peak": filt_tf * tensor_per_zmac / 8.0 / FP64_PEAK_TFLOPS if args.emulate_ranks == 1 else None,
             "flop_convention": ("value / filter_kernel_tflops count 8 n^2 sum(deg) (ZGEMM convention); frac_of_peak "
                                 f"and roofline count the {tensor_per_zmac:g} real tensor flops per complex MAC "
                                 f"the {args.zmul}M kernel executes"),
