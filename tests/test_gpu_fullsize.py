@@ -9,6 +9,7 @@ import pytest
 import gen as G
 import oracle as O
 from gen.configs import CONFIGS, HNORM
+from parity_checks import check_perturbed
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -45,40 +46,6 @@ def test_filter_c2_full_width(gpu_lib, c2):
     assert rel.max() <= 1e-11
 
 
-def _check_perturbed(H, lam, X, nev, tol, seed, inertia):
-    """Oracle checks of one converged eigenproblem of a perturbed sequence (SURVEY 8(c) c4 rows (ii) and
-    (iii); Alg 1 "Ensure" and locking), all in the oracle's naive loops:
-      (i)  residuals ||H x - lam x|| / ||H|| <= tol on 9 sampled eigenvectors (0..2, the middle three,
-           nev-3..nev-1), normalised by a certified LOWER bound of ||H||_2: the largest |Ritz value| of the
-           oracle's Lanczos tridiagonal (Ritz values are Rayleigh quotients, so |theta| <= ||H||_2);
-      (ii) the Kato-Temple bound r^2 / gap (<= 1e-12 |rho| asserted) on the distance from the oracle's
-           Rayleigh quotient rho of the GPU's vector to the eigenvalue it approximates, the gap taken from
-           the neighbouring Rayleigh quotients minus their residuals (for nev-1 the neighbour above is the
-           first buffer vector); with |lam_gpu - rho| it bounds the GPU eigenvalue's error by 1e-10 |rho| (J);
-      (iii) completeness ("the nev smallest"): Sylvester inertia of H - sigma I (Bunch-Kaufman) with sigma
-           just above the largest wanted eigenvalue counts exactly nev eigenvalues below."""
-    m = nev // 2
-    windows = [list(range(0, 4)), list(range(m - 2, m + 3)), list(range(nev - 4, nev + 1))]
-    cols = sorted({j for w in windows for j in w})
-    rho, ra = O.rayleigh_quotients(H, X[:, cols])
-    R = dict(zip(cols, zip(rho, ra)))
-    tmin, tmax, _ = O.lanczos(H, 25, seed)
-    h_lo = max(abs(tmin), abs(tmax))
-    sample = [0, 1, 2, m - 1, m, m + 1, nev - 3, nev - 2, nev - 1]
-    res = O.residuals(H, X[:, sample], lam[sample], h_lo)  # (i)
-    assert res.max() <= tol, res
-    for j in sample:  # (ii): |lam_gpu - lam_true| <= |lam_gpu - rho| + r^2 / gap <= 1e-10 |rho| (J)
-        r, rj = R[j]
-        gaps = [abs(R[i][0] - r) - R[i][1] for i in (j - 1, j + 1) if i in R]
-        gap = min(gaps)
-        assert gap > 0, (j, gaps)
-        assert rj * rj / gap <= 1e-12 * abs(r), (j, rj, gap)
-        assert abs(lam[j] - r) + rj * rj / gap <= 1e-10 * abs(r), (j, lam[j], r, rj, gap)
-    if inertia:  # (iii)
-        sigma = lam[nev - 1] + min(1e-6, 0.5 * (R[nev][0] - lam[nev - 1]))
-        assert O.count_below(H, sigma) == nev
-
-
 def test_solve_c2_sequence_perturbed(gpu_lib, c2):
     """The c2 sequence exactly as bench.py solves it (H^(1), then H^(l+1) = H^(l) + delta 40 G_l, the
     hand-off of each problem seeding the next, the same options), through problem 4 -- the first problem
@@ -106,7 +73,7 @@ def test_solve_c2_sequence_perturbed(gpu_lib, c2):
     assert np.max(np.abs(out["lam"][0] - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
     assert np.abs(X[:, :nev].conj().T @ X[:, :nev] - np.eye(nev)).max() <= 1e-12
     assert out["resid"].max() <= cf["tol"]
-    _check_perturbed(H, out["lam"][-1], X, nev, cf["tol"], cf["seed"] + nprob - 1, inertia=True)
+    check_perturbed(H, out["lam"][-1], X, nev, cf["tol"], cf["seed"] + nprob - 1, inertia=True)
 
 
 def test_filter_c3_full_width(gpu_lib):
@@ -163,7 +130,7 @@ def test_solve_c3_sequence_perturbed(gpu_lib):
     assert np.max(np.abs(out["lam"][0] - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10
     sample = [0, nev // 2, nev - 1]
     assert np.abs(X[:, sample].conj().T @ X[:, :nev] - np.eye(nev)[sample]).max() <= 1e-12
-    _check_perturbed(H, out["lam"][1], X, nev, cf["tol"], cf["seed"] + 1, inertia=False)
+    check_perturbed(H, out["lam"][1], X, nev, cf["tol"], cf["seed"] + 1, inertia=False)
 
 
 def _real_sym_known(n, nd, seed):

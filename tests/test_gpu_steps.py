@@ -8,6 +8,7 @@ import pytest
 import gen as G
 import oracle as O
 from gen.configs import CONFIGS, DEG0, HNORM
+from parity_checks import check_perturbed
 
 pytestmark = pytest.mark.gpu
 
@@ -326,6 +327,8 @@ def test_solve_c1_sequence(gpu_lib, ctx):
     full = np.linalg.eigvalsh(Hl)
     sigma = lam[-1] + min(1e-6, 0.5 * (full[nev] - full[nev - 1]))
     assert O.count_below(Hl, sigma) == nev
+    # the last (perturbed) problem against the oracle alone: residuals, Kato-Temple, inertia
+    check_perturbed(np.asfortranarray(Hl), lam, Xd.cpu().numpy(), nev, cf["tol"], cf["seed"], inertia=True)
     loops = [r["loops"] for r in out["reports"]]
     assert all(l <= loops[0] for l in loops[1:])  # reuse of the previous eigenvectors pays
 
@@ -375,10 +378,13 @@ def test_solve_batch_independent_sequences(gpu_lib, ctx):
         seqs.append((lambda ell, Hs=Hs: Hs[ell], 2, gpu_lib.to_colmajor(X0)))
         np.testing.assert_allclose(serial[-1]["lam"][0], w.lam[:nev], rtol=1e-10)
     outs = gpu_lib.solve_batch(0, 2, seqs, nev, nex, 1e-10, deg_cap=24, seed=7)
-    for o, s in zip(outs, serial):
+    for i, (o, s) in enumerate(zip(outs, serial)):
         assert o["status"] == 0
         np.testing.assert_allclose(o["lam"], s["lam"], rtol=1e-13)
         assert [r["loops"] for r in o["reports"]] == [r["loops"] for r in s["reports"]]
+        # each sequence's perturbed problem 2 against the oracle (not only against the serial path)
+        H2 = np.asfortranarray(seqs[i][0](1).cpu().numpy())
+        check_perturbed(H2, o["lam"][1], seqs[i][2].cpu().numpy(), nev, 1e-10, 7, inertia=True)
 
 
 def test_library_owned_nccl_communicator(gpu_lib):
