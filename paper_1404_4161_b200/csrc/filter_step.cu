@@ -1,5 +1,6 @@
 // filter_step.cu -- instantiations and launcher of K1 (see filter_step.cuh).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <vector>
 
@@ -159,7 +160,8 @@ void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
   const int64_t tiles = tm * (tn / cl);  // schedule tiles (pair tiles when cl = 2)
   const int64_t iters = tiles * p.num_kt;
   const int64_t slots = (int64_t)num_sms * t.occ / cl;  // schedule ids (clusters)
-  const int64_t grid = iters < slots ? iters : slots;
+  int64_t grid = iters < slots ? iters : slots;
+  if (grid > StepParams::kMaxGrid) grid = StepParams::kMaxGrid;  // the sk_bounds table's capacity
   p.tiles_n = (int32_t)tn;
   p.grid = (int32_t)grid;
   int64_t dp = tiles / grid;
@@ -211,16 +213,25 @@ void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
   double want_sum = 0.0;
   std::vector<double> want(grid);
   for (int64_t c = 0; c < grid; ++c) want_sum += (want[c] = std::max(0.0, target - dpw[c]));
-  // walk the tail iterations, closing CTA c's range once its (normalised) share of the work is reached
-  int64_t g = 0;           // tail iteration cursor
+  // walk the tail, closing CTA c's range once its (normalised) share of the work is reached: whole tiles
+  // at a time, then the iteration inside the tile where the share ends (each iteration goes to the side
+  // it overlaps more)
+  int64_t g = 0;  // tail iteration cursor
   double acc = 0.0, goal = 0.0;
   for (int64_t c = 0; c < grid; ++c) {
     goal += want[c] * tail_work / want_sum;
     while (g < p.tail_iters) {
-      const double w = cost(p.tail_tile0 + g / KT);
-      if (acc + 0.5 * w > goal) break;  // the iteration goes to whichever side it overlaps more
-      acc += w;
-      ++g;
+      const int64_t u = g / KT, left = (u + 1) * KT - g;  // iterations left in the cursor's tile
+      const double w = cost(p.tail_tile0 + u);
+      if (acc + w * (double)left <= goal) {  // the rest of the tile fits the share
+        acc += w * (double)left;
+        g += left;
+        continue;
+      }
+      const int64_t take = std::max<int64_t>(0, std::min<int64_t>(left, (int64_t)std::floor((goal - acc) / w + 0.5)));
+      acc += w * (double)take;
+      g += take;
+      break;
     }
     p.sk_bounds[c + 1] = (int32_t)(c + 1 == grid ? p.tail_iters : g);
   }
