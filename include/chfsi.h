@@ -211,12 +211,14 @@ chfsi_status chfsi_back_transform(chfsi_ctx ctx, int64_t n, const void* L, int64
  * the same (n, row0, nloc). The assembled H is Hermitian bit for bit across the ranks (R13).
  * Bp (in, device n x nloc, ldb >= n): the column slab B[:, row0:row0+nloc] of the Hermitian positive
  * definite B; not modified. L (out, device n x n, ldl >= n, caller-owned): the full Cholesky factor
- * B = L L^H in its lower triangle (identical on every rank: factored once on rank 0 and broadcast; the
- * strict upper triangle holds B's), for chfsi_back_transform_panel.
- * Work: B and A gathered on every rank (two n x n scratch uses of 16 n^2 bytes), ZPOTRF (n^3 / 3, rank 0),
- * 2 ZTRSM + 1 ZGEMM with nloc right-hand sides per rank. Errors: CHFSI_ERR_ARG (dims / panel,
- * B not positive definite -- returned by every rank, pivot in chfsi_last_error), CHFSI_ERR_CUDA,
- * CHFSI_ERR_NCCL, CHFSI_ERR_NOMEM. */
+ * B = L L^H in its lower triangle (identical bits on every rank; the strict upper triangle is
+ * unspecified), for chfsi_back_transform_panel.
+ * Work: B = L L^H factored on the ranks' column slabs (right-looking panels of <= 256 columns: the
+ * panel's owner runs ZPOTRF + ZTRSM, the panel is broadcast, every rank updates its own trailing
+ * columns with ZGEMM; p = 1: one ZPOTRF), L and A gathered on every rank (16 n^2 bytes of scratch),
+ * then 2 ZTRSM + 1 ZGEMM with nloc right-hand sides per rank. Errors: CHFSI_ERR_ARG (dims / panel,
+ * B not positive definite -- returned by every rank, the first failing pivot in chfsi_last_error),
+ * CHFSI_ERR_CUDA, CHFSI_ERR_NCCL, CHFSI_ERR_NOMEM. */
 chfsi_status chfsi_reduce_generalized_panel(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, void* Ap,
                                             int64_t lda, const void* Bp, int64_t ldb, void* L, int64_t ldl);
 /* Row-panel back-transformation, collective: X (in/out, device nloc x k, ldx >= nloc) holds this

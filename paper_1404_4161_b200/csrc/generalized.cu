@@ -1,9 +1,11 @@
 // generalized.cu -- the generalised front / back end: Cholesky of B,
 // H = L^{-1} A L^{-H}, and the back-transformation c = L^{-H} y. The n^3 steps are plain library
 // calls (cuSOLVER ZPOTRF, cuBLAS ZTRSM / ZGEMM); the Hermitisation is the library's own kernel. The
-// row-panel forms (p >= 1) gather the operand slabs, factor B once on rank 0 and compute each rank's
-// columns of H with O(n^2 n_loc) work.
+// row-panel forms (p >= 1) factor B on the ranks' column slabs (right-looking panels, broadcast over the
+// communicator), gather L and A and compute each rank's columns of H with O(n^2 n_loc) work.
 #include <algorithm>
+#include <string>
+#include <vector>
 
 #include "ctx.cuh"
 #include "small_kernels.cuh"
@@ -53,6 +55,68 @@ chfsi_status gather_slabs(chfsi_ctx ctx, int64_t n, int64_t nloc, const void* S,
   CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(W + n * nloc * ctx->rank, 16 * n, S, 16 * lds, 16 * n, nloc,
                                         cudaMemcpyDeviceToDevice, ctx->stream));
   return comm_allgather_inplace(ctx, reinterpret_cast<double*>(W), (size_t)2 * n * nloc);
+}
+
+// B = L L^H factored on the column slabs (rank q owns global columns [q nloc, (q+1) nloc)): right-looking,
+// in panels of <= kPanel columns that never straddle a slab. The owner factors the panel's diagonal block
+// (ZPOTRF) and solves the rows below it (ZTRSM), the panel (rows j0..n-1) is broadcast, and every rank
+// updates its own trailing columns (ZGEMM). Lp (n x nloc, ld n) in: this rank's slab of B; out: its slab
+// of L in the lower triangle (the strict upper part is unspecified). *bad <- the first failing global
+// pivot + 1 of this rank's panels, or 0.
+constexpr int64_t kPanel = 256;
+
+chfsi_status cholesky_slabs(chfsi_ctx ctx, int64_t n, int64_t nloc, cuDoubleComplex* Lp, int64_t* bad) {
+  const int64_t q0 = nloc * ctx->rank;  // this rank's first global column
+  *bad = 0;
+  TRY(ensure(ctx, ctx->w1, 16 * (size_t)n * (size_t)std::min(kPanel, nloc)));
+  TRY(ensure(ctx, ctx->devinfo, 64));
+  cuDoubleComplex* P = static_cast<cuDoubleComplex*>(ctx->w1.ptr);
+  int* info = static_cast<int*>(ctx->devinfo.ptr);
+  static const cuDoubleComplex kMone = {-1.0, 0.0};
+  for (int64_t j0 = 0; j0 < n;) {
+    const int64_t owner = j0 / nloc, slab_end = (owner + 1) * nloc;
+    const int64_t jb = std::min(kPanel, slab_end - j0);
+    const int64_t below = n - j0 - jb;
+    if (owner == ctx->rank) {
+      cuDoubleComplex* D = Lp + (j0 - q0) * n + j0;  // diagonal block, ld n
+      int lw = 0;
+      if (cusolverDnZpotrf_bufferSize(ctx->cusolver, CUBLAS_FILL_MODE_LOWER, (int)jb, D, (int)n, &lw) !=
+          CUSOLVER_STATUS_SUCCESS) {
+        set_err(ctx, "cusolverDnZpotrf_bufferSize failed");
+        return CHFSI_ERR_CUDA;
+      }
+      TRY(ensure(ctx, ctx->solver_ws, sizeof(cuDoubleComplex) * (size_t)std::max(lw, 1)));
+      if (cusolverDnZpotrf(ctx->cusolver, CUBLAS_FILL_MODE_LOWER, (int)jb, D, (int)n,
+                           static_cast<cuDoubleComplex*>(ctx->solver_ws.ptr), lw, info) != CUSOLVER_STATUS_SUCCESS ||
+          (below > 0 && cublasZtrsm(ctx->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C,
+                                    CUBLAS_DIAG_NON_UNIT, (int)below, (int)jb, &kOne, D, (int)n, D + jb, (int)n) !=
+                            CUBLAS_STATUS_SUCCESS)) {
+        set_err(ctx, "distributed Cholesky: cuSOLVER / cuBLAS failed");
+        return CHFSI_ERR_CUDA;
+      }
+      int hinfo = 0;
+      CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      if (hinfo > 0 && *bad == 0) *bad = j0 + hinfo;
+      // the panel's rows j0..n-1, packed (ld n - j0)
+      CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(P, 16 * (n - j0), D, 16 * n, 16 * (n - j0), jb, cudaMemcpyDeviceToDevice,
+                                            ctx->stream));
+    }
+    TRY(comm_bcast(ctx, reinterpret_cast<double*>(P), (size_t)2 * (n - j0) * jb, (int)owner));
+    // trailing update of this rank's columns c >= j0 + jb, rows c0..n-1 (the lower part and the slab's
+    // diagonal blocks): L[c0:, cols] -= P[c0 - j0:, :] P[cols - j0, :]^H
+    const int64_t c0 = std::max(j0 + jb, q0), c1 = q0 + nloc;
+    if (c0 < c1 && c0 < n) {
+      const cuDoubleComplex* Pr = P + (c0 - j0);
+      if (cublasZgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_C, (int)(n - c0), (int)(c1 - c0), (int)jb, &kMone, Pr,
+                      (int)(n - j0), Pr, (int)(n - j0), &kOne, Lp + (c0 - q0) * n + c0, (int)n) != CUBLAS_STATUS_SUCCESS) {
+        set_err(ctx, "distributed Cholesky: cublasZgemm failed");
+        return CHFSI_ERR_CUDA;
+      }
+    }
+    j0 += jb;
+  }
+  return CHFSI_OK;
 }
 
 bool panel_args_ok(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc) {
@@ -141,7 +205,7 @@ chfsi_status chfsi_reduce_generalized_panel(chfsi_ctx ctx, int64_t n, int64_t ro
   chfsi_status st = ensure(ctx, ctx->gw, 16 * (size_t)n * n);
   if (!st) st = ensure(ctx, ctx->gx, 16 * (size_t)n * nloc);
   if (!st) st = ensure(ctx, ctx->devinfo, 64);
-  if (!st) st = ensure(ctx, ctx->small2, 64);
+  if (!st) st = ensure(ctx, ctx->small2, sizeof(double) * (size_t)std::max(8, ctx->nranks));
   if (st) return st;
   double2* W = static_cast<double2*>(ctx->gw.ptr);
   cuDoubleComplex* w = static_cast<cuDoubleComplex*>(ctx->gw.ptr);
@@ -149,11 +213,37 @@ chfsi_status chfsi_reduce_generalized_panel(chfsi_ctx ctx, int64_t n, int64_t ro
   cuDoubleComplex* l = static_cast<cuDoubleComplex*>(L);
   cuDoubleComplex* a = static_cast<cuDoubleComplex*>(Ap);
   const int ni = (int)n, nl = (int)nloc;
-  // B = L L^H: the whole B on every rank, factored once on rank 0 and broadcast (identical bits)
-  TRY(gather_slabs(ctx, n, nloc, Bp, ldb, W));
+  // B = L L^H. p > 1: factored on the slabs (cholesky_slabs: every rank factors and updates its own
+  // columns, ZPOTRF work shared) and gathered, so every rank holds the same bits of L; p = 1: one ZPOTRF.
   double* dflag = static_cast<double*>(ctx->small2.ptr);
   double hflag = 0.0;
-  if (ctx->rank == 0) {
+  if (ctx->nranks > 1) {
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(X, 16 * n, Bp, 16 * ldb, 16 * n, nloc, cudaMemcpyDeviceToDevice,
+                                          ctx->stream));
+    int64_t bad = 0;
+    TRY(cholesky_slabs(ctx, n, nloc, X, &bad));
+    // every rank learns every rank's verdict (the collectives stay matched): slot r holds rank r's first
+    // failing pivot + 1; the smallest non-zero one is reported
+    std::vector<double> flags(ctx->nranks, 0.0);
+    flags[ctx->rank] = (double)bad;
+    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(dflag, flags.data(), sizeof(double) * flags.size(), cudaMemcpyHostToDevice,
+                                        ctx->stream));
+    TRY(comm_allreduce_sum(ctx, dflag, flags.size()));
+    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(flags.data(), dflag, sizeof(double) * flags.size(), cudaMemcpyDeviceToHost,
+                                        ctx->stream));
+    CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    for (double f : flags)
+      if (f != 0.0 && (hflag == 0.0 || f < hflag)) hflag = f;
+    if (hflag != 0.0) {
+      set_err(ctx, "chfsi_reduce_generalized_panel: B is not positive definite (pivot " +
+                       std::to_string((long long)hflag - 1) + ")");
+      return CHFSI_ERR_ARG;
+    }
+    TRY(gather_slabs(ctx, n, nloc, X, n, W));
+  } else {
+    CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(W, 16 * n, Bp, 16 * ldb, 16 * n, n, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  if (ctx->nranks == 1) {
     int lw = 0;
     if (cusolverDnZpotrf_bufferSize(ctx->cusolver, CUBLAS_FILL_MODE_LOWER, ni, w, ni, &lw) != CUSOLVER_STATUS_SUCCESS) {
       set_err(ctx, "cusolverDnZpotrf_bufferSize failed");
@@ -170,18 +260,12 @@ chfsi_status chfsi_reduce_generalized_panel(chfsi_ctx ctx, int64_t n, int64_t ro
     CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
     hflag = (double)hinfo;
-    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(dflag, &hflag, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   }
-  // every rank learns rank 0's verdict before anyone leaves (the collectives stay matched)
-  TRY(comm_bcast(ctx, dflag, 1, 0));
-  CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&hflag, dflag, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-  CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  if (hflag != 0.0) {
+  if (ctx->nranks == 1 && hflag != 0.0) {
     set_err(ctx, "chfsi_reduce_generalized_panel: B is not positive definite (pivot " +
                      std::to_string((long long)hflag - 1) + ")");
     return CHFSI_ERR_ARG;
   }
-  TRY(comm_bcast(ctx, reinterpret_cast<double*>(W), (size_t)2 * n * n, 0));
   CHFSI_CUDA_TRY(ctx, cudaMemcpy2DAsync(L, 16 * ldl, W, 16 * n, 16 * n, n, cudaMemcpyDeviceToDevice, ctx->stream));
   // this rank's columns of H = L^{-1} A L^{-H}: X = L^{-H} E_cols, then L^{-1} (A X)
   unit_cols_kernel<<<col_grid(n, nloc), 256, 0, ctx->stream>>>(n, nloc, row0, reinterpret_cast<double2*>(X), n);
