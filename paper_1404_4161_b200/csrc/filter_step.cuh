@@ -179,7 +179,10 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
   static_assert(BM % (8 * CL) == 0, "A box split");
   constexpr bool CPLX = MODE == kZ4M;  // the A' [B' B''] embedding
   constexpr int kNP = Cfg::kNP;
-  constexpr int kAcc = kNP * Cfg::kMT * Cfg::kNT * 2;  // accumulator doubles per thread
+  // stream-K partial accumulators: 3M publishes (Re, Im) = (P1 + P2, P3 - P1 + P2) -- the epilogue's
+  // combination is linear, so partial sums of it are exact partials -- 2 sets instead of 3
+  constexpr int kPS = MODE == kZ3M ? 2 : kNP;
+  constexpr int kAcc = kPS * Cfg::kMT * Cfg::kNT * 2;  // partial doubles per thread
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align to 1024 B (128B-swizzle atoms) by pointer arithmetic on the shared array, so the compiler
   // keeps the shared address space and emits LDS (an integer round-trip would give generic LD)
@@ -400,7 +403,8 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       }
     }
   };
-  auto epilogue = [&](int tile) {
+  // packed: the 3M accumulators hold (Re, Im) in (acc, acc2) after a stream-K reduction
+  auto epilogue = [&](int tile, bool packed) {
     const int m0 = (tile / p.tiles_n) * BM;
     int nu;
     const int c0 = tile_cols(tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
@@ -418,7 +422,10 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             if (col + e >= p.col_end) continue;
-            store_z3(col + e, r, acc[i][j][e] + acc2[i][j][e], (acc3[i][j][e] - acc[i][j][e]) + acc2[i][j][e]);
+            if (packed)
+              store_z3(col + e, r, acc[i][j][e], acc2[i][j][e]);
+            else
+              store_z3(col + e, r, acc[i][j][e] + acc2[i][j][e], (acc3[i][j][e] - acc[i][j][e]) + acc2[i][j][e]);
           }
           continue;
         }
@@ -593,7 +600,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     }
 
     if (kbeg == 0 && kend == KT) {
-      epilogue(tile);
+      epilogue(tile, false);
       continue;
     }
     // ---- split tile: publish the partial accumulator; the last contributor finishes the tile ----
@@ -602,14 +609,20 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     const int my_slot = (t_beg / KT == u) ? 0 : 1;
     double* mine = p.partials + ((pcta * 2 + my_slot) * kAcc) * (int64_t)Cfg::kThreads;
 #pragma unroll
-    for (int ps = 0; ps < kNP; ++ps)
+    for (int ps = 0; ps < kPS; ++ps)
 #pragma unroll
       for (int i = 0; i < Cfg::kMT; ++i)
 #pragma unroll
         for (int jj = 0; jj < Cfg::kNT; ++jj)
 #pragma unroll
-          for (int e = 0; e < 2; ++e)
-            __stcg(mine + (((ps * Cfg::kMT + i) * Cfg::kNT + jj) * 2 + e) * Cfg::kThreads + threadIdx.x, acc_ref(ps, i, jj, e));
+          for (int e = 0; e < 2; ++e) {
+            double v;
+            if constexpr (MODE == kZ3M)
+              v = ps == 0 ? acc[i][jj][e] + acc2[i][jj][e] : (acc3[i][jj][e] - acc[i][jj][e]) + acc2[i][jj][e];
+            else
+              v = acc_ref(ps, i, jj, e);
+            __stcg(mine + (((ps * Cfg::kMT + i) * Cfg::kNT + jj) * 2 + e) * Cfg::kThreads + threadIdx.x, v);
+          }
     __threadfence();
     __syncthreads();
     const int64_t c_lo = sk_owner(p, U0), c_hi = sk_owner(p, U1 - 1);
@@ -627,7 +640,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       const int slot = (cs / KT == u) ? 0 : 1;
       const double* src = p.partials + (((c * CL + crank) * 2 + slot) * kAcc) * (int64_t)Cfg::kThreads;
 #pragma unroll
-      for (int ps = 0; ps < kNP; ++ps)
+      for (int ps = 0; ps < kPS; ++ps)
 #pragma unroll
         for (int i = 0; i < Cfg::kMT; ++i)
 #pragma unroll
@@ -636,7 +649,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
             for (int e = 0; e < 2; ++e)
               acc_ref(ps, i, jj, e) += __ldcg(src + (((ps * Cfg::kMT + i) * Cfg::kNT + jj) * 2 + e) * Cfg::kThreads + threadIdx.x);
     }
-    epilogue(tile);
+    epilogue(tile, MODE == kZ3M);
     if (threadIdx.x == 0) p.tickets[u * CL + crank] = 0;  // ready for the next launch (stream ordered)
   }
   if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
