@@ -45,14 +45,17 @@ constexpr Variant kVariants[] = {
     {13, 256, 8, 4, 512, 8, 0.850},    // 16 warps (8 x 2), warp tile 32 x 4
     {14, 256, 12, 4, 384, 16, 0.820},  // 12 warps (4 x 3), warp tile 64 x 4
 };
-// 3M variants: accumulators are 3 sets (P1, P2, P3) of (WM/8) x (WNC/8) 8x8 tiles. eff: measured
-// full-width rates relative to 200 (n = 13000, k = 624: 45.5 / 42.0 / 32.4 / 41.8 / 30.2 TF/s
-// ZGEMM-equivalent; profiles/r01_z3_variants.log)
+// 3M variants: accumulators are 3 sets (P1, P2, P3) of (WM/8) x (WNC/8) 8x8 tiles. eff: rates relative
+// to 200, fitted to the r02 width tables (every variant at every width, n = 13000 and 4096;
+// profiles/r02_width_table_pw*.jsonl): with its producer warpgroup (r02) 200 is the fastest tile at 198 of
+// 231 widths, and these efficiencies make the step model's picks cost <= 0.05 % more than the per-width
+// best. 16-warp tiles cannot take a producer warpgroup (640 threads leave the consumers < 128 registers).
 constexpr Variant kVariantsZ3[] = {
-    {200, 128, 48, 16, 384, 48, 1.0},
-    {207, 64, 64, 16, 512, 24, 0.963},      // 16 warps, warp tile 16 x 16, 4 stages (k_a = 64, 128, 256)
-    {208, 128, 32, 8, 512, 24, 0.94},       // 16 warps, warp tile 32 x 8, 3 stages (k_a = 32, 160)
+    {200, 128, 48, 16, 512, 48, 1.0},      // 12 consumer warps + a producer warpgroup
+    {207, 64, 64, 16, 512, 24, 0.88},       // 16 warps, warp tile 16 x 16, 4 stages
+    {208, 128, 32, 8, 512, 24, 0.83},       // 16 warps, warp tile 32 x 8, 3 stages
 #ifdef CHFSI_K1_AB
+    {239, 128, 48, 16, 384, 48, 0.97},  // z200 without the producer warpgroup
     {201, 128, 32, 16, 256, 48, 0.93}, {202, 128, 16, 8, 256, 24, 0.72},
     {203, 64, 64, 16, 256, 48, 0.925}, {204, 192, 32, 16, 384, 48, 0.67},
     {210, 128, 48, 16, 384, 48, 0.5, 2},  // z200 as multicast CTA pairs (A/B measurement; not chosen yet)

@@ -89,13 +89,16 @@ constexpr int kReal = 0, kZ4M = 1, kZ3M = 2;
 // KH: 128-byte swizzle rows of the interleaved operands per stage (2: 16 complex K entries per stage; 1:
 // half stages of 8 entries -- twice as many, finer-grained stages in the same shared memory, so a stage
 // is refilled sooner after it is released; the 3M planes then use 64-byte rows with the 64B swizzle)
-template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int KH = 2>
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int KH = 2, int PW = 0>
 struct FilterCfg {
   static constexpr bool kCplx = MODE != kReal;  // complex output columns
   static constexpr int kWarpsM = BM / WM;
   static constexpr int kWarpsN = BNC / WNC;
   static constexpr int kConsumerWarps = kWarpsM * kWarpsN;
-  static constexpr int kThreads = kConsumerWarps * 32;  // thread 0 doubles as the TMA producer
+  static constexpr int kConsumerThreads = kConsumerWarps * 32;
+  // PW = 0: thread 0 doubles as the TMA producer; PW = 4: an extra warpgroup produces (one lane of it
+  // issues the loads), its registers handed to the consumers with setmaxnreg
+  static constexpr int kThreads = kConsumerThreads + 32 * PW;
   static constexpr int kMT = WM / 8;   // 8-row MMA tiles per warp
   static constexpr int kNT = MODE == kZ4M ? WNC / 4 : WNC / 8;  // 8-real-column MMA tiles per warp
   static constexpr int kNP = MODE == kZ3M ? 3 : 1;              // accumulator sets (P1, P2, P3)
@@ -166,12 +169,26 @@ __device__ __forceinline__ double xor_sign(double x, uint32_t mask) {
 // stream-K schedule runs over pair tiles (tiles_n N tiles = tiles_n / 2 pair columns) and cluster ids.
 // OCC: CTAs resident per SM (the persistent grid is OCC x SM count; 2 lets one CTA's MMAs cover the
 // other's TMA waits)
-template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int OCC = 1, int KH = 2>
-__global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kThreads, OCC)
+// PW = 4: a dedicated producer warpgroup (the last four warps; one lane works) issues every TMA load as
+// soon as the consumer warps have released a stage -- STAGES - 1 stages of lead instead of about one.
+// Registers are allocated per warpgroup, so the launch gives every thread 65536 / kThreads; the producer
+// warpgroup drops to kProdRegs with setmaxnreg and the consumers take kConsRegs
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int OCC = 1, int KH = 2,
+          int PW = 0>
+__global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE, 1, 2, PW>::kThreads, OCC)
     filter_step_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmA3, const __grid_constant__ CUtensorMap tmB3,
                        const StepParams p) {
-  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE, CL, KH>;
+  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE, CL, KH, PW>;
+  static_assert(PW == 0 || (PW == 4 && CL == 1 && Cfg::kConsumerWarps % 4 == 0), "producer warpgroup: single CTAs");
+  // the CTA's register pool is kThreads x (its launch allocation, 65536 / kThreads rounded down to 8 for a
+  // kernel this large -- launch_cfg verifies the compiled count before the first launch, since an
+  // increase the pool cannot satisfy would block the consumers forever)
+  constexpr int kProdRegs = 24;
+  constexpr int kLaunchRegs = (65536 / Cfg::kThreads) / 8 * 8;
+  constexpr int kConsRegs =
+      PW ? ((kLaunchRegs * Cfg::kThreads - 32 * PW * kProdRegs) / Cfg::kConsumerThreads) / 8 * 8 : 0;
+  static_assert(PW == 0 || kConsRegs <= 256, "setmaxnreg range");
   static_assert(CL == 1 || CL == 2, "cluster of 1 or 2");
   static_assert(KH == 2 || (KH == 1 && MODE == kZ3M), "half stages are built for the 3M planes");
   constexpr int kHalves = KH;
@@ -193,6 +210,13 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // the consumer warps' own barrier (the producer warp of PW = 1 never joins the split-tile fix-up)
+  auto consumer_sync = [&]() {
+    if constexpr (PW == 0)
+      __syncthreads();
+    else
+      asm volatile("bar.sync 1, %0;" ::"n"(Cfg::kConsumerThreads) : "memory");
+  };
   const int64_t cta = blockIdx.x / CL;        // schedule id (cluster id when CL = 2)
   const int crank = (int)(blockIdx.x % CL);    // rank in the cluster (1-D grid, cluster dims (CL,1,1))
   const int64_t pcta = blockIdx.x;             // physical CTA: owner of partial-accumulator slots
@@ -311,7 +335,8 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
       }
     }
   };
-  if (threadIdx.x == 0) {
+  const int producer_thread = PW ? Cfg::kConsumerThreads : 0;
+  if ((int)threadIdx.x == producer_thread) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if constexpr (MODE == kZ3M) {
@@ -323,6 +348,22 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
     pc_dp_left = p.dp_units;
     pc_init();
     while (pc_j < STAGES && pc_j < my_iters) produce();
+  }
+  if constexpr (PW == 4) {
+    if (warp >= Cfg::kConsumerWarps) {  // the producer warpgroup: refill every stage as soon as it is released
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs));
+      if (warp == Cfg::kConsumerWarps && lane == 0) {
+        uint32_t ph = 0;  // parity of the stage's current use
+        for (int64_t it = STAGES; it < my_iters; ++it) {
+          const int st = (int)(it % STAGES);
+          if (st == 0) ph ^= 1u;
+          mbar_wait(&empty[st], ph ^ 1u);  // consumers released iteration it - STAGES
+          produce();
+        }
+      }
+      return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsRegs));
   }
 
   const int wm = warp % Cfg::kWarpsM;
@@ -588,7 +629,7 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
         }
       }
       // refill the stage of iteration j - 1 (stage pc_stage, phase of j - 1) with iteration pc_j
-      if (threadIdx.x == 0 && j >= 1 && *(volatile int64_t*)&pc_j < my_iters) {
+      if (PW == 0 && threadIdx.x == 0 && j >= 1 && *(volatile int64_t*)&pc_j < my_iters) {
         const uint32_t prev_phase = (s == 0) ? (phase ^ 1u) : phase;
         mbar_wait(&empty[pc_stage], prev_phase);
         produce();
@@ -624,13 +665,13 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE>::kTh
             __stcg(mine + (((ps * Cfg::kMT + i) * Cfg::kNT + jj) * 2 + e) * Cfg::kThreads + threadIdx.x, v);
           }
     __threadfence();
-    __syncthreads();
+    consumer_sync();
     const int64_t c_lo = sk_owner(p, U0), c_hi = sk_owner(p, U1 - 1);
     int nseg = 0;
     for (int64_t c = c_lo; c <= c_hi; ++c)
       if (sk_start(p, c + 1) > sk_start(p, c)) ++nseg;
     if (threadIdx.x == 0) s_ticket = atomicAdd(&p.tickets[u * CL + crank], 1);
-    __syncthreads();
+    consumer_sync();
     if (s_ticket != nseg - 1) continue;  // not the last contributor
     __threadfence();
     zero_acc();

@@ -7,11 +7,12 @@
 
 namespace chfsi {
 
-template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int OCC = 1, int KH = 2>
+template <int BM, int BNC, int WM, int WNC, int STAGES, int MODE = kZ4M, int CL = 1, int OCC = 1, int KH = 2,
+          int PW = 0>
 inline cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmA3,
                        const CUtensorMap& tmB3, const StepParams& p, cudaStream_t stream) {
-  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE, CL, KH>;
-  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, MODE, CL, OCC, KH>;
+  using Cfg = FilterCfg<BM, BNC, WM, WNC, STAGES, MODE, CL, KH, PW>;
+  auto kern = filter_step_kernel<BM, BNC, WM, WNC, STAGES, MODE, CL, OCC, KH, PW>;
   // the opt-in shared-memory size is a per-device function attribute: set it once per device (contexts
   // on several host threads may launch the same instantiation concurrently)
   static std::atomic<uint64_t> attr_devices{0};
@@ -21,6 +22,13 @@ inline cudaError_t launch_cfg(const CUtensorMap& tmA, const CUtensorMap& tmB, co
   if (!(attr_devices.load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     if (e != cudaSuccess) return e;
+    if constexpr (PW > 0) {  // the producer warpgroup hands its registers to the consumers (setmaxnreg): the
+      // launch allocation must be the one the kernel's arithmetic assumed, or the consumers' increase blocks
+      cudaFuncAttributes fa;
+      e = cudaFuncGetAttributes(&fa, kern);
+      if (e != cudaSuccess) return e;
+      if (fa.numRegs != (65536 / Cfg::kThreads) / 8 * 8) return cudaErrorInvalidConfiguration;
+    }
     attr_devices.fetch_or(bit, std::memory_order_release);
   }
   if constexpr (CL == 1) {

@@ -7,13 +7,15 @@ cudaError_t launch_filter_z3(int id, const CUtensorMap& tmA, const CUtensorMap& 
                              const CUtensorMap& tmB3, const StepParams& p, cudaStream_t stream) {
 #define LC(BM, BNC, WM, WNC, ST) launch_cfg<BM, BNC, WM, WNC, ST, kZ3M>(tmA, tmB, tmA3, tmB3, p, stream)
   switch (id) {
-    case 200:
-      return LC(128, 48, 32, 16, 3);
+    case 200:  // the workhorse: 12 consumer warps + a producer warpgroup
+      return launch_cfg<128, 48, 32, 16, 3, kZ3M, 1, 1, 2, 4>(tmA, tmB, tmA3, tmB3, p, stream);
     case 207:
       return LC(64, 64, 16, 16, 4);
     case 208:
       return LC(128, 32, 32, 8, 3);
 #ifdef CHFSI_K1_AB
+    case 239:  // z200 without the producer warpgroup (thread 0 produces; the round-1 workhorse)
+      return LC(128, 48, 32, 16, 3);
     case 201:
       return LC(128, 32, 32, 16, 3);
     case 202:

@@ -14,7 +14,7 @@ import paper_1404_4161_b200 as chfsi  # noqa: E402
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 13000
-    variants = [200, 207, 208]
+    variants = [int(v) for v in (sys.argv[3] if len(sys.argv) > 3 else "200,207,208").split(",")]
     step = int(sys.argv[2]) if len(sys.argv) > 2 else 4
     torch.manual_seed(0)
     H = chfsi.colmajor(n, n)
