@@ -65,15 +65,20 @@ constexpr Variant kVariantsZ3[] = {
     {227, 64, 64, 16, 512, 24, 0.5, 1, 1, 1},    // z207 in 8 half stages (A/B measurement)
 #endif
 };
-// real-symmetric variants (columns are real columns; kNT = WNC / 8). eff relative to 103 (n = 13000,
-// k = 624: 33.6 / 32.1 / 31.7 / 29.2 / 32.9 / 32.6 TF/s for 103 / 100 / 101 / 102 / 104 / 105;
-// profiles/r01_real_variants.log)
+// real-symmetric variants (columns are real columns; kNT = WNC / 8). eff fitted to the r02 width table
+// (every variant at widths 28..636, n = 13000; profiles/r02_width_table_real.jsonl): with a producer
+// warpgroup 135 / 133 / 132 run 34.0-35.2 TF/s at k = 624 against 33.2-33.8 without (r02_ab_pw_real.log),
+// and these efficiencies make the step model's picks cost 0.007 % more than the per-width best (3.3 %
+// with the r01 set 102-105).
 constexpr Variant kVariantsReal[] = {
 #ifdef CHFSI_K1_AB
     {100, 128, 96, 32, 384, 32, 0.955}, {101, 128, 64, 32, 256, 32, 0.94},
+    {102, 128, 32, 16, 256, 16, 0.87},  {103, 192, 64, 32, 384, 32, 0.97}, {105, 128, 48, 16, 384, 16, 0.97},
 #endif
-    {102, 128, 32, 16, 256, 16, 0.87},
-    {103, 192, 64, 32, 384, 32, 1.0},   {104, 128, 64, 16, 512, 16, 0.98}, {105, 128, 48, 16, 384, 16, 0.97},
+    {104, 128, 64, 16, 512, 16, 0.98},   // 16 warps (no room for a producer warpgroup)
+    {132, 128, 32, 16, 384, 16, 0.97},   // 8 consumer warps + a producer warpgroup
+    {133, 192, 64, 32, 512, 32, 1.0},    // 12 consumer warps + a producer warpgroup
+    {135, 128, 48, 16, 512, 16, 1.0},    // 12 consumer warps + a producer warpgroup
 };
 
 // Model time of one step of `ncols` active columns over `nrows` rows for variant V, in units of a

@@ -12,7 +12,7 @@ import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["102", "103", "104", "105"])
+@pytest.fixture(params=["104", "132", "133", "135"])
 def rvariant(request):
     os.environ["CHFSI_FILTER_VARIANT_REAL"] = request.param
     yield request.param

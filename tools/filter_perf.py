@@ -1,7 +1,7 @@
 """Quick K1 throughput probe: chfsi_filter at a fixed shape for each tile variant (CUDA events).
 usage: filter_perf.py n k1,k2 m variants [real]
 variants: comma list of 4M ids (0..9), 3M ids (200..204), 'auto3' / 'auto4' (the chooser under 3M / 4M),
-'auto' (= auto3); real: the real-symmetric ids (100..102) / 'auto'. Flops are 8 n^2 k m (complex,
+'auto' (= auto3); real: the real-symmetric ids (104, 132, 133, 135; 100-105 with -DCHFSI_K1_AB) / 'auto'. Flops are 8 n^2 k m (complex,
 the 4M convention of SURVEY 8(d)) or 2 n^2 k m (real)."""
 import json, os, sys, time
 import torch
@@ -27,6 +27,7 @@ def main():
         Y0 = chfsi.colmajor(n, k, dtype=dt); Y0.copy_(torch.randn(n, k, dtype=dt, device="cuda"))
         Y = chfsi.colmajor(n, k, dtype=dt)
         deg = [m] * k
+        Yref = None
         for v in variants:
             for e in ENVS:
                 os.environ.pop(e, None)
@@ -53,7 +54,10 @@ def main():
                 e0.record(); filt(H, Y, deg, -2.2, 0.6, 1.6); e1.record(); torch.cuda.synchronize()
                 best = min(best, e0.elapsed_time(e1))
             fl = (2.0 if real else 8.0) * n * n * k * m
-            print(json.dumps({"n": n, "k": k, "m": m, "variant": v, "real": real,
+            if Yref is None:
+                Yref = Y.clone()
+            diff = float((Y - Yref).abs().max() / Yref.abs().max())
+            print(json.dumps({"rel_diff_vs_first": diff, "n": n, "k": k, "m": m, "variant": v, "real": real,
                               "mults": None if real else mults, "ms": best, "tflops": fl / best / 1e9,
                               "tensor_tflops": (fl if real or mults == 4 else 0.75 * fl) / best / 1e9}), flush=True)
 
