@@ -18,7 +18,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libchfsi.so")
+# CHFSI_LIB: another build of the same library (A/B measurements of two builds in one session)
+LIB_PATH = os.environ.get("CHFSI_LIB") or os.path.join(_HERE, "libchfsi.so")
 MAX_DEGREE = 64
 
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NONFINITE", 3: "ERR_NOCONV", 4: "ERR_QR", 5: "ERR_CUDA", 6: "ERR_NCCL",

@@ -97,7 +97,19 @@ constexpr double kSkWoff = 0.75;  // per-iteration cost of a tile's stage traffi
 
 static double warp_cover(int warps) { return warps >= 12 ? 1.0 : warps >= 8 ? 0.85 : warps >= 4 ? 0.6 : 0.4; }
 
-static double step_cost(const Variant& V, int64_t nrows, int64_t ncols, double speed, double hbm_cols) {
+// Column units a step of `ncols` active columns costs under variant (wnc, mma_cols): the block's last
+// unit counts one half when only its first half is active and the warp tile holds an even number of
+// MMA tiles (the kernel then skips the inactive half's MMAs; mma_cols = 8 real / 3M columns, 4 complex
+// columns under 4M)
+static double work_units(int64_t ncols, int wnc, int mma_cols) {
+  const int64_t units = (ncols + wnc - 1) / wnc;
+  const int64_t rag = ncols % wnc;
+  const bool half = (wnc / mma_cols) % 2 == 0 && rag != 0 && 2 * rag <= wnc;
+  return (double)units - (half ? 0.5 : 0.0);
+}
+
+static double step_cost(const Variant& V, int64_t nrows, int64_t ncols, double speed, double hbm_cols,
+                        int mma_cols) {
   const int64_t tm = (nrows + V.bm - 1) / V.bm;
   const int64_t units = (ncols + V.wnc - 1) / V.wnc;
   const int64_t tn = (ncols + V.bnc - 1) / V.bnc;
@@ -105,10 +117,11 @@ static double step_cost(const Variant& V, int64_t nrows, int64_t ncols, double s
   const int warps = V.threads / 32;
   const int warps_m = warps / (V.bnc / V.wnc);
   const double cover = warp_cover((int)per * warps_m) / warp_cover(warps);
-  // work-weighted stream-K (schedule_filter_step): the step costs the average tile, (units / tn + woff)
+  // work-weighted stream-K (schedule_filter_step): the step costs the average tile, (work / tn + woff)
   // per iteration, against a full tile's (per + woff); without weighting every tile costs the widest
-  const double fill = ((double)units / (double)tn + kSkWoff) / ((double)per + kSkWoff);
-  const double cols = (double)(tn * per * V.wnc) * (units % tn ? fill : 1.0);
+  const double wu = work_units(ncols, V.wnc, mma_cols);
+  const double fill = (wu / (double)tn + kSkWoff) / ((double)per + kSkWoff);
+  const double cols = (double)(tn * per * V.wnc) * (wu != (double)(tn * per) ? fill : 1.0);
   const double rows = (double)tm * V.bm;
   const double compute = rows * cols / (V.eff * cover * speed);
   const double memory = rows * hbm_cols * (1.0 + 0.25 * (double)(tn - 1));
@@ -119,7 +132,7 @@ static double step_cost(const Variant& V, int64_t nrows, int64_t ncols, double s
 
 template <size_t N>
 static TileChoice choose(const Variant (&vs)[N], const char* env, int64_t nrows, int64_t ncols, double speed,
-                         double hbm_cols) {
+                         double hbm_cols, int mma_cols) {
   // test hook: the environment variable forces one variant (parity tests cover every instantiation)
   const char* fs = getenv(env);
   const int forced = fs ? atoi(fs) : -1;
@@ -127,7 +140,7 @@ static TileChoice choose(const Variant (&vs)[N], const char* env, int64_t nrows,
   double best_cost = 1e300;
   for (size_t v = 0; v < N; ++v) {
     if (forced >= 0 && vs[v].id != forced) continue;
-    const double cost = step_cost(vs[v], nrows, ncols, speed, hbm_cols);
+    const double cost = step_cost(vs[v], nrows, ncols, speed, hbm_cols, mma_cols);
     if (best < 0 || cost < best_cost * 0.999) {
       best_cost = cost;
       best = (int)v;
@@ -145,17 +158,17 @@ static TileChoice choose(const Variant (&vs)[N], const char* env, int64_t nrows,
 
 TileChoice choose_filter_tile(int64_t nrows, int64_t ncols, int num_sms) {
   (void)num_sms;  // the persistent stream-K schedule removes wave quantisation
-  return choose(kVariants, "CHFSI_FILTER_VARIANT", nrows, ncols, 1.0, 11.8);
+  return choose(kVariants, "CHFSI_FILTER_VARIANT", nrows, ncols, 1.0, 11.8, 4);
 }
 
 TileChoice choose_filter_tile_z3(int64_t nrows, int64_t ncols, int num_sms) {
   (void)num_sms;
-  return choose(kVariantsZ3, "CHFSI_FILTER_VARIANT_Z3", nrows, ncols, 45.5 / 34.9, 17.7);
+  return choose(kVariantsZ3, "CHFSI_FILTER_VARIANT_Z3", nrows, ncols, 45.5 / 34.9, 17.7, 8);
 }
 
 TileChoice choose_filter_tile_real(int64_t nrows, int64_t ncols, int num_sms) {
   (void)num_sms;  // real: 2 n flops per column-row; speed / memory in the same relative units
-  return choose(kVariantsReal, "CHFSI_FILTER_VARIANT_REAL", nrows, ncols, 1.0, 20.0);
+  return choose(kVariantsReal, "CHFSI_FILTER_VARIANT_REAL", nrows, ncols, 1.0, 20.0, 8);
 }
 
 void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
@@ -197,11 +210,14 @@ void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
   const int64_t U = p.units_n, base = U / tn, extra = U % tn;
   const char* we = getenv("CHFSI_SK_WEIGHT");
   const char* wo = getenv("CHFSI_SK_WOFF");
-  const bool weighted = !(we && we[0] == '0') && cl == 1 && extra != 0;
+  // the block's last N tile is half a unit cheaper when the kernel skips the inactive half of its last
+  // unit (work_units)
+  const double half = (double)U - work_units(ncols, t.wnc, t.id < 100 ? 4 : 8);
+  const bool weighted = !(we && we[0] == '0') && cl == 1 && (extra != 0 || half != 0.0);
   const double woff = wo ? atof(wo) : kSkWoff;
   auto cost = [&](int64_t tile) {  // per-iteration cost of schedule tile `tile`
     const int64_t n = tile % ntn;
-    return (double)(base + (n < extra ? 1 : 0)) + woff;
+    return (double)(base + (n < extra ? 1 : 0)) + woff - (n == ntn - 1 ? half : 0.0);
   };
   p.sk_bounds[0] = 0;
   if (!weighted || tail_tiles == 0) {

@@ -146,6 +146,11 @@ __device__ __forceinline__ int64_t sk_owner(const StepParams& p, int64_t g) {
   return lo;
 }
 
+template <int N>
+struct IntC {
+  static constexpr int value = N;
+};
+
 // balanced N split: N tile i covers column units [i*(U/T) + min(i, U%T), ...) of width U/T (+1 for
 // the first U%T tiles), so every tile has (nearly) the same number of active warps and the stream-K
 // split by iterations stays balanced; returns the first column (relative to col0) and the units
@@ -519,106 +524,119 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE, 1, 2
     }
     zero_acc();
 
-    // a warp whose columns all lie past the active block (ragged last N tile) skips the MMAs: the
-    // DMMA pipe is shared per SM sub-partition, so the padding costs no tensor-core time
+    // Active 8-column MMA tiles of this warp (4 complex columns under 4M): a warp whose columns all lie
+    // past the active block (ragged last N tile) skips its MMAs, and the warp holding the block's last,
+    // partly active column unit skips the MMA tiles of its inactive half -- the DMMA pipe is shared per
+    // SM sub-partition, so neither the padding unit nor the padding half costs tensor-core time.
+    // NA is a compile-time count (kNT, kNT / 2 or 0) so the k-loop keeps its full unrolling.
     int nu;
-    tile_cols(tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
-    const bool warp_active = wn < nu;
+    const int tc0 = tile_cols(tile % p.tiles_n, p.tiles_n, p.units_n, WNC, &nu);
+    const int wcols = min(nu * WNC, p.col_end - p.col0 - tc0) - wn * WNC;
+    constexpr bool kHalfOk = Cfg::kNT % 2 == 0;
+    const int na = wcols <= 0 ? 0 : (kHalfOk && 2 * wcols <= WNC) ? Cfg::kNT / 2 : Cfg::kNT;
+    // the MMAs of one stage for NA active MMA tiles (the branch stays inside the k-loop so the loop
+    // control keeps to the uniform datapath)
+    auto mma_stage = [&](auto na_tag, const uint8_t* sa, const uint8_t* sb) {
+      constexpr int NA = decltype(na_tag)::value;
+      if constexpr (MODE == kZ3M) {
+        const uint8_t* a3 = sa + kHalves * BM * 128;
+        const uint8_t* b3 = sb + kHalves * Cfg::kBRow;
+#pragma unroll
+        for (int h = 0; h < kHalves; ++h) {
+          const uint8_t* ah = sa + h * BM * 128;
+          const uint8_t* bh = sb + h * Cfg::kBRow;
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {
+            // P1, P2: complex entry 2*qd + sub of this half -> (a_r, a_i) and (y_r, y_i) in one LDS.128
+            const int chunk = 2 * qd + sub;
+            double2 av[Cfg::kMT], bv[NA];
+#pragma unroll
+            for (int i = 0; i < Cfg::kMT; ++i) av[i] = *reinterpret_cast<const double2*>(ah + swz(a_row0 + i * 8, chunk));
+#pragma unroll
+            for (int jj = 0; jj < NA; ++jj) bv[jj] = *reinterpret_cast<const double2*>(bh + swz(b_row0 + jj * 8, chunk));
+#pragma unroll
+            for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+              for (int jj = 0; jj < NA; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], av[i].x, bv[jj].x);
+#pragma unroll
+            for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+              for (int jj = 0; jj < NA; ++jj) dmma_8x8x4(acc2[i][jj][0], acc2[i][jj][1], av[i].y, bv[jj].y);
+          }
+          // P3: plane entries 2c, 2c+1 of chunk c. KH = 2: c = 2qd + h of the 128-byte row (h = 0, 1
+          // cover all 16 entries; even/odd chunks for the two rows of a quarter-warp keep the LDS.128
+          // conflict-free under the 128B swizzle, c' = c ^ (row & 7)). KH = 1: c = qd of the 64-byte row
+          // (64B swizzle: c' = c ^ ((row >> 1) & 3); rows g, g+1 of a quarter-warp land in opposite
+          // 64-byte halves of the bank space -> conflict-free)
+          {
+            double2 cv[Cfg::kMT], dv[NA];
+            if constexpr (KH == 2) {
+              const int chunk = 2 * qd + h;
+#pragma unroll
+              for (int i = 0; i < Cfg::kMT; ++i) cv[i] = *reinterpret_cast<const double2*>(a3 + swz(a_row0 + i * 8, chunk));
+#pragma unroll
+              for (int jj = 0; jj < NA; ++jj) dv[jj] = *reinterpret_cast<const double2*>(b3 + swz(b_row0 + jj * 8, chunk));
+            } else {
+#pragma unroll
+              for (int i = 0; i < Cfg::kMT; ++i) cv[i] = *reinterpret_cast<const double2*>(a3 + swz64(a_row0 + i * 8, qd));
+#pragma unroll
+              for (int jj = 0; jj < NA; ++jj) dv[jj] = *reinterpret_cast<const double2*>(b3 + swz64(b_row0 + jj * 8, qd));
+            }
+#pragma unroll
+            for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+              for (int jj = 0; jj < NA; ++jj) dmma_8x8x4(acc3[i][jj][0], acc3[i][jj][1], cv[i].x, dv[jj].x);
+#pragma unroll
+            for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+              for (int jj = 0; jj < NA; ++jj) dmma_8x8x4(acc3[i][jj][0], acc3[i][jj][1], cv[i].y, dv[jj].y);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < kHalves; ++h) {
+          const uint8_t* ah = sa + h * BM * 128;
+          const uint8_t* bh = sb + h * Cfg::kBRow;
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {
+            // k-steps 2*sub, 2*sub+1 of this half: lane qd covers doubles 4*qd + 2*sub + {0,1}
+            const int chunk = 2 * qd + sub;
+            double2 av[Cfg::kMT], bv[NA];
+#pragma unroll
+            for (int i = 0; i < Cfg::kMT; ++i) av[i] = *reinterpret_cast<const double2*>(ah + swz(a_row0 + i * 8, chunk));
+#pragma unroll
+            for (int jj = 0; jj < NA; ++jj) {
+              if constexpr (CPLX) {
+                // B' (even g): (re, im) as stored; B'' (odd g): (im, -re) -- two lane-offset LDS.64 do the
+                // swap, one integer XOR the sign (no select, no FP64 op)
+                const double* y = reinterpret_cast<const double*>(bh + swz(b_row0 + jj * 4, chunk));
+                bv[jj].x = y[odd ? 1 : 0];
+                bv[jj].y = xor_sign(y[odd ? 0 : 1], sign_mask);
+              } else {
+                bv[jj] = *reinterpret_cast<const double2*>(bh + swz(b_row0 + jj * 8, chunk));
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+              for (int jj = 0; jj < NA; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], av[i].x, bv[jj].x);
+#pragma unroll
+            for (int i = 0; i < Cfg::kMT; ++i)
+#pragma unroll
+              for (int jj = 0; jj < NA; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], av[i].y, bv[jj].y);
+          }
+        }
+      }
+    };
     for (int kt = kbeg; kt < kend; ++kt, ++j) {
       const int s = stage;
       mbar_wait(&full[s], phase);
       const uint8_t* sa = smem + s * Cfg::kStageBytes;
       const uint8_t* sb = sa + Cfg::kABytes;
-      if constexpr (MODE == kZ3M) {
-        if (warp_active) {
-          const uint8_t* a3 = sa + kHalves * BM * 128;
-          const uint8_t* b3 = sb + kHalves * Cfg::kBRow;
-#pragma unroll
-          for (int h = 0; h < kHalves; ++h) {
-            const uint8_t* ah = sa + h * BM * 128;
-            const uint8_t* bh = sb + h * Cfg::kBRow;
-#pragma unroll
-            for (int sub = 0; sub < 2; ++sub) {
-              // P1, P2: complex entry 2*qd + sub of this half -> (a_r, a_i) and (y_r, y_i) in one LDS.128
-              const int chunk = 2 * qd + sub;
-              double2 av[Cfg::kMT], bv[Cfg::kNT];
-#pragma unroll
-              for (int i = 0; i < Cfg::kMT; ++i) av[i] = *reinterpret_cast<const double2*>(ah + swz(a_row0 + i * 8, chunk));
-#pragma unroll
-              for (int jj = 0; jj < Cfg::kNT; ++jj) bv[jj] = *reinterpret_cast<const double2*>(bh + swz(b_row0 + jj * 8, chunk));
-#pragma unroll
-              for (int i = 0; i < Cfg::kMT; ++i)
-#pragma unroll
-                for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], av[i].x, bv[jj].x);
-#pragma unroll
-              for (int i = 0; i < Cfg::kMT; ++i)
-#pragma unroll
-                for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc2[i][jj][0], acc2[i][jj][1], av[i].y, bv[jj].y);
-            }
-            // P3: plane entries 2c, 2c+1 of chunk c. KH = 2: c = 2qd + h of the 128-byte row (h = 0, 1
-            // cover all 16 entries; even/odd chunks for the two rows of a quarter-warp keep the LDS.128
-            // conflict-free under the 128B swizzle, c' = c ^ (row & 7)). KH = 1: c = qd of the 64-byte row
-            // (64B swizzle: c' = c ^ ((row >> 1) & 3); rows g, g+1 of a quarter-warp land in opposite
-            // 64-byte halves of the bank space -> conflict-free)
-            {
-              double2 cv[Cfg::kMT], dv[Cfg::kNT];
-              if constexpr (KH == 2) {
-                const int chunk = 2 * qd + h;
-#pragma unroll
-                for (int i = 0; i < Cfg::kMT; ++i) cv[i] = *reinterpret_cast<const double2*>(a3 + swz(a_row0 + i * 8, chunk));
-#pragma unroll
-                for (int jj = 0; jj < Cfg::kNT; ++jj) dv[jj] = *reinterpret_cast<const double2*>(b3 + swz(b_row0 + jj * 8, chunk));
-              } else {
-#pragma unroll
-                for (int i = 0; i < Cfg::kMT; ++i) cv[i] = *reinterpret_cast<const double2*>(a3 + swz64(a_row0 + i * 8, qd));
-#pragma unroll
-                for (int jj = 0; jj < Cfg::kNT; ++jj) dv[jj] = *reinterpret_cast<const double2*>(b3 + swz64(b_row0 + jj * 8, qd));
-              }
-#pragma unroll
-              for (int i = 0; i < Cfg::kMT; ++i)
-#pragma unroll
-                for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc3[i][jj][0], acc3[i][jj][1], cv[i].x, dv[jj].x);
-#pragma unroll
-              for (int i = 0; i < Cfg::kMT; ++i)
-#pragma unroll
-                for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc3[i][jj][0], acc3[i][jj][1], cv[i].y, dv[jj].y);
-            }
-          }
-        }
-      } else
-#pragma unroll
-      for (int h = 0; h < kHalves && warp_active; ++h) {
-        const uint8_t* ah = sa + h * BM * 128;
-        const uint8_t* bh = sb + h * Cfg::kBRow;
-#pragma unroll
-        for (int sub = 0; sub < 2; ++sub) {
-          // k-steps 2*sub, 2*sub+1 of this half: lane qd covers doubles 4*qd + 2*sub + {0,1}
-          const int chunk = 2 * qd + sub;
-          double2 av[Cfg::kMT], bv[Cfg::kNT];
-#pragma unroll
-          for (int i = 0; i < Cfg::kMT; ++i) av[i] = *reinterpret_cast<const double2*>(ah + swz(a_row0 + i * 8, chunk));
-#pragma unroll
-          for (int jj = 0; jj < Cfg::kNT; ++jj) {
-            if constexpr (CPLX) {
-              // B' (even g): (re, im) as stored; B'' (odd g): (im, -re) -- two lane-offset LDS.64 do the
-              // swap, one integer XOR the sign (no select, no FP64 op)
-              const double* y = reinterpret_cast<const double*>(bh + swz(b_row0 + jj * 4, chunk));
-              bv[jj].x = y[odd ? 1 : 0];
-              bv[jj].y = xor_sign(y[odd ? 0 : 1], sign_mask);
-            } else {
-              bv[jj] = *reinterpret_cast<const double2*>(bh + swz(b_row0 + jj * 8, chunk));
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < Cfg::kMT; ++i)
-#pragma unroll
-            for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], av[i].x, bv[jj].x);
-#pragma unroll
-          for (int i = 0; i < Cfg::kMT; ++i)
-#pragma unroll
-            for (int jj = 0; jj < Cfg::kNT; ++jj) dmma_8x8x4(acc[i][jj][0], acc[i][jj][1], av[i].y, bv[jj].y);
-        }
-      }
+      if (na == Cfg::kNT)
+        mma_stage(IntC<Cfg::kNT>{}, sa, sb);
+      else if (kHalfOk && na == Cfg::kNT / 2)
+        mma_stage(IntC<(kHalfOk ? Cfg::kNT / 2 : Cfg::kNT)>{}, sa, sb);
       __syncwarp();
       if (lane == 0) {
         if constexpr (CL == 1) {
