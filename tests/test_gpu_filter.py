@@ -245,3 +245,31 @@ def test_filter_stream_k_hybrid_schedule(gpu_lib, ctx, env, vid, mults):
     for hy in ("1", "0"):
         assert colrel(out[hy], Yc).max() <= 1e-11
     assert colrel(out["1"], out["0"]).max() <= 1e-13
+
+
+@pytest.mark.parametrize("vid", ["200", "207", "7", "1"])
+def test_filter_every_last_unit_residue(gpu_lib, ctx, vid):
+    """The kernel skips the MMA tiles of the inactive half of the block's last column unit (WNC = 16
+    columns: z200 / z207 skip 8 of 16, 4M v7 / v1 skip 8 of 16 complex columns). Every residue of the
+    active width modulo the unit -- all steps at the same width (one degree for every column), and a
+    width over several N tiles -- against the diagonal closed form."""
+    z3 = int(vid) >= 200
+    env = "CHFSI_FILTER_VARIANT_Z3" if z3 else "CHFSI_FILTER_VARIANT"
+    ctx.set_complex_mult(3 if z3 else 4)
+    os.environ[env] = vid
+    try:
+        rng = np.random.default_rng(int(vid))
+        n = 1100
+        d = np.sort(rng.uniform(-2.0, 40.0, n))
+        Hd = gpu_lib.to_colmajor(np.diag(d.astype(complex)))
+        l1, a, b = -2.3, -1.2, 40.5
+        c, e = (a + b) / 2, (b - a) / 2
+        for k in list(range(33, 49)) + [100, 105, 153]:
+            Y0 = crand(rng, n, k)
+            deg = [3] * k
+            Yd = gpu_lib.to_colmajor(Y0)
+            assert ctx.filter(Hd, Yd, deg, l1, c, e) == 3 * k
+            Yc = O.filter_diag_closed(d, Y0, deg, l1, c, e)
+            assert colrel(Yd.cpu().numpy(), Yc).max() <= 1e-13, k
+    finally:
+        os.environ.pop(env, None)

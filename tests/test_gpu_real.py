@@ -178,3 +178,23 @@ def test_solve_real_multirank_odd_panels(gpu_lib):
     for o in outs:
         assert o["status"] == 0
         assert np.max(np.abs(o["lam"][0] - lam[:nev]) / np.abs(lam[:nev])) <= 1e-10
+
+
+def test_filter_real_every_last_unit_residue(gpu_lib, rvariant):
+    """Real tiles skip the MMA tiles of the inactive half of the last column unit (WNC 16 or 32 real
+    columns): every residue of the active width modulo 16 / 32 at one degree, against the closed form."""
+    rng = np.random.default_rng(int(rvariant))
+    n = 777
+    d = np.sort(rng.uniform(-2.0, 40.0, n))
+    l1, a, b = -2.3, -1.2, 40.5
+    c, e = (a + b) / 2, (b - a) / 2
+    ctx = gpu_lib.Context(0)
+    Hd = gpu_lib.to_colmajor(np.diag(d), real=True)
+    for k in list(range(65, 97)) + [150]:
+        Y0 = rng.standard_normal((n, k))
+        Yd = gpu_lib.to_colmajor(Y0, real=True)
+        ctx.filter_real(Hd, Yd, [4] * k, l1, c, e)
+        Yc = O.filter_diag_closed(d, Y0.astype(complex), [4] * k, l1, c, e).real
+        rel = np.linalg.norm(Yd.cpu().numpy() - Yc, axis=0) / np.linalg.norm(Yc, axis=0)
+        assert rel.max() <= 1e-13, k
+    ctx.close()
