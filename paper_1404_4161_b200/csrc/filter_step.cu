@@ -215,9 +215,20 @@ void schedule_filter_step(const TileChoice& t, int num_sms, StepParams& p) {
   const double half = (double)U - work_units(ncols, t.wnc, t.id < 100 ? 4 : 8);
   const bool weighted = !(we && we[0] == '0') && cl == 1 && (extra != 0 || half != 0.0);
   const double woff = wo ? atof(wo) : kSkWoff;
+  // Per-unit speed of a tile one warp column short of full (u = bnc / wnc - 1) relative to a full tile:
+  // measured 1.1 -- its fewer warps per SM sub-partition run their MMAs slightly faster per unit
+  // (profiles/r02_ab_cover.txt: against 1.0, 0.5 % less K1 time over 24 mid widths of the c2 mix, full
+  // width unchanged; 0.8 / 0.9 were 1-2 % slower). CHFSI_SK_C2 / CHFSI_SK_C1 set the speed of tiles one /
+  // two units short (A/B hooks, read once)
+  static const double cov_env = getenv("CHFSI_SK_C2") ? atof(getenv("CHFSI_SK_C2")) : 1.1;
+  const double cov_short1 = t.id == 200 ? cov_env : 1.0;  // measured on the workhorse z200 only
+  static const double cov_short2 = getenv("CHFSI_SK_C1") ? atof(getenv("CHFSI_SK_C1")) : 1.0;
+  const int64_t wn_full = t.bnc / t.wnc;
   auto cost = [&](int64_t tile) {  // per-iteration cost of schedule tile `tile`
     const int64_t n = tile % ntn;
-    return (double)(base + (n < extra ? 1 : 0)) + woff - (n == ntn - 1 ? half : 0.0);
+    const int64_t u = base + (n < extra ? 1 : 0);
+    const double cov = u == wn_full - 1 ? cov_short1 : u == wn_full - 2 ? cov_short2 : 1.0;
+    return ((double)u - (n == ntn - 1 ? half : 0.0)) / cov + woff;
   };
   p.sk_bounds[0] = 0;
   if (!weighted || tail_tiles == 0) {
