@@ -261,14 +261,13 @@ __global__ void __launch_bounds__(FilterCfg<BM, BNC, WM, WNC, STAGES, MODE, 1, 2
       kt = (int)(g % KT);
     }
   };
-  // TMA producer = thread 0 (a dedicated producer warp would round the CTA to 12 warps of register
-  // allocation and cap the consumers at 168 registers). Stage s is refilled once every consumer warp
-  // has released it; thread 0 refills one iteration behind its own progress, so it blocks only if
-  // another warp is more than one k-tile behind. The producer walks the CTA's iterations in order
-  // with an incremental cursor and runs across tile boundaries, so the next tile's first stages
-  // stream in during an epilogue.
-  // producer cursor in shared memory: only thread 0 touches it, and keeping it out of the register
-  // file leaves the consumers their full budget
+  // TMA producer. PW = 4: one lane of the producer warpgroup refills each stage as soon as every
+  // consumer warp has released it (STAGES - 1 stages of lead). PW = 0: thread 0, itself a consumer,
+  // refills one iteration behind its own progress, so it blocks only if another warp is more than one
+  // k-tile behind. Either way the producer walks the CTA's iterations in order with an incremental
+  // cursor and runs across tile boundaries, so the next tile's first stages stream in during an
+  // epilogue. The cursor lives in shared memory: one thread touches it, and keeping it out of the
+  // register file leaves the consumers their full budget
   __shared__ struct {
     int64_t j;
     int tile, kt, dp_left, stage;
