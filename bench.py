@@ -368,8 +368,15 @@ def rank_main(args, cf, rank, world, local_rank, group):
     ctx.set_complex_mult(args.zmul)
     ctx.set_eigensolver(0 if args.eig == "refine" else 1)
     ctx.reserve(n, nloc, k)
+    exchange = args.exchange if world > 1 else None
     if world > 1 and args.exchange == "push":
-        ctx.set_exchange(1)  # collective: maps every rank's operand buffers
+        try:
+            ctx.set_exchange(1)  # collective: maps every rank's operand buffers
+        except RuntimeError as ex:  # every rank gets the same verdict (the library agrees on it)
+            ctx.set_exchange(0)
+            exchange = "allgather (peer push unavailable: %s)" % ex
+            if rank == 0:
+                print("warning: " + exchange, file=sys.stderr)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -525,7 +532,7 @@ def rank_main(args, cf, rank, world, local_rank, group):
                        "problems": f"{W} warm-up + {K} timed of the correlated sequence",
                        "parallelism": (f"1-D row panels over {world} emulated ranks on one GPU" if args.emulate_ranks > 1
                                        else f"1-D row panels over {world} GPU(s)" if world > 1 else "single GPU"),
-                       "exchange": args.exchange if world > 1 else None, "complex_mult": f"{args.zmul}M",
+                       "exchange": exchange, "complex_mult": f"{args.zmul}M",
                        "eigensolver": args.eig,
                        "l2": "inputs larger than L2 (H panel per problem >> 126 MB)"},
             "time_per_eigenproblem_s": ms / K / 1e3,

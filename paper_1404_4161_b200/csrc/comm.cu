@@ -294,15 +294,19 @@ chfsi_status comm_open_peers(chfsi_ctx ctx) {
     ctx->peer_R_bytes = mn;
     return CHFSI_OK;
   }
-  // separate processes: CUDA IPC handles of R0 / R1, gathered over the library's NCCL communicator
+  // separate processes: CUDA IPC handles of R0 / R1, gathered over the library's NCCL communicator.
+  // Every rank takes part in every collective below whatever fails locally, and the ranks agree on the
+  // outcome at the end (a failure count, allreduced), so either all ranks map their peers or all
+  // return the same error -- a rank that failed alone would otherwise leave the others in a collective
   PeerInfo me{};
-  CHFSI_CUDA_TRY(ctx, cudaIpcGetMemHandle(&me.h0, ctx->R0.ptr));
-  CHFSI_CUDA_TRY(ctx, cudaIpcGetMemHandle(&me.h1, ctx->R1.ptr));
+  bool ok = cudaIpcGetMemHandle(&me.h0, ctx->R0.ptr) == cudaSuccess &&
+            cudaIpcGetMemHandle(&me.h1, ctx->R1.ptr) == cudaSuccess;
+  if (!ok) cudaGetLastError();
   me.bytes = mine;
-  me.device = ctx->device;
+  me.device = ok ? ctx->device : -1;  // -1: this rank has no handles to offer
   const size_t chunk = (sizeof(PeerInfo) + 7) / 8;  // in doubles
   double* d = nullptr;
-  CHFSI_CUDA_TRY(ctx, cudaMalloc(&d, sizeof(double) * chunk * P));
+  CHFSI_CUDA_TRY(ctx, cudaMalloc(&d, sizeof(double) * (chunk * P + 1)));
   std::vector<PeerInfo> all(P);
   chfsi_status st = CHFSI_OK;
   if (cudaMemcpyAsync(d + chunk * ctx->rank, &me, sizeof(me), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
@@ -312,17 +316,24 @@ chfsi_status comm_open_peers(chfsi_ctx ctx) {
     if (cudaMemcpyAsync(&all[q], d + chunk * q, sizeof(PeerInfo), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
       st = CHFSI_ERR_CUDA;
   if (!st && cudaStreamSynchronize(ctx->stream) != cudaSuccess) st = CHFSI_ERR_CUDA;
-  cudaFree(d);
-  if (st) {
+  if (st) {  // the gather itself failed (a communicator problem every rank sees)
+    cudaFree(d);
     set_err(ctx, "peer exchange: gathering the IPC handles failed");
     return st;
   }
+  std::string why = ok ? "" : "cudaIpcGetMemHandle failed on this rank";
   size_t mn = mine;
   for (int q = 0; q < P; ++q) {
     mn = std::min<size_t>(mn, all[q].bytes);
     if (q == ctx->rank) {
       ctx->peer_R0[q] = static_cast<double*>(ctx->R0.ptr);
       ctx->peer_R1[q] = static_cast<double*>(ctx->R1.ptr);
+      continue;
+    }
+    if (!ok) continue;
+    if (all[q].device < 0) {
+      ok = false;
+      why = "rank " + std::to_string(q) + " could not export its operand buffers";
       continue;
     }
     int can = 0;
@@ -337,17 +348,35 @@ chfsi_status comm_open_peers(chfsi_ctx ctx) {
         cudaIpcOpenMemHandle(&p1, all[q].h1, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
       cudaGetLastError();
       if (p0) cudaIpcCloseMemHandle(p0);
-      comm_close_peers(ctx);
-      set_err(ctx, "peer exchange: cudaIpcOpenMemHandle failed for rank " + std::to_string(q));
-      return CHFSI_ERR_CUDA;
+      ok = false;
+      why = "cudaIpcOpenMemHandle failed for rank " + std::to_string(q);
+      continue;
     }
     ctx->ipc_opened.push_back(p0);
     ctx->ipc_opened.push_back(p1);
     ctx->peer_R0[q] = static_cast<double*>(p0);
     ctx->peer_R1[q] = static_cast<double*>(p1);
   }
+  // agreement: the number of ranks that failed (also the barrier after which peers may be written)
+  double* fails = d + chunk * P;
+  const double mine_fail = ok ? 0.0 : 1.0;
+  double total_fail = 0.0;
+  st = CHFSI_OK;
+  if (cudaMemcpyAsync(fails, &mine_fail, sizeof(double), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
+    st = CHFSI_ERR_CUDA;
+  if (!st) st = comm_allreduce_sum(ctx, fails, 1);
+  if (!st && (cudaMemcpyAsync(&total_fail, fails, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+              cudaStreamSynchronize(ctx->stream) != cudaSuccess))
+    st = CHFSI_ERR_CUDA;
+  cudaFree(d);
+  if (st || total_fail > 0.0) {
+    comm_close_peers(ctx);
+    set_err(ctx, "peer exchange unavailable: " +
+                     (why.empty() ? std::to_string((int)total_fail) + " other rank(s) failed to map their peers" : why));
+    return st ? st : CHFSI_ERR_CUDA;
+  }
   ctx->peer_R_bytes = mn;
-  return comm_barrier(ctx, ctx->stream);
+  return CHFSI_OK;
 }
 
 void comm_close_peers(chfsi_ctx ctx) {
