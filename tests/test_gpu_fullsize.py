@@ -212,3 +212,28 @@ def test_generalized_c2_first_problem(gpu_lib):
     r = np.linalg.norm(A_h @ C - BC * lam[sample], axis=0) / (HNORM * np.linalg.norm(BC, axis=0))
     assert r.max() <= 1e-9
     assert np.abs(C.conj().T @ BC - np.eye(len(sample))).max() <= 1e-10
+
+
+@pytest.mark.parametrize("k", [256, 1024])
+def test_filter_c4_shape_sampled(gpu_lib, k):
+    """BASELINE configs[4] shape as the sweep times it: n = 8192 GUE (stream (5, n)), the fixed interval,
+    the sorted ramp of degrees 8..40 over k columns (every width from k down to the last few columns,
+    3M and the 4M narrow tail); the oracle's Alg 2 on sampled columns (first, middle, last: degrees 8,
+    ~24, 40) within the filter tolerance."""
+    from gen.configs import C4_INTERVAL, c4_ramp
+
+    n = 8192
+    iv = C4_INTERVAL
+    c, e = (iv["alpha"] + iv["beta"]) / 2, (iv["beta"] - iv["alpha"]) / 2
+    Hh = G.gue(n, 5, G.stream(5, n))
+    Y0 = G.start_basis(n, k, 5)
+    deg = c4_ramp(k)
+    ctx = gpu_lib.Context(0)
+    Yd = gpu_lib.to_colmajor(Y0)
+    assert ctx.filter(gpu_lib.to_colmajor(Hh), Yd, deg, iv["lambda1"], c, e) == sum(deg)
+    cols = [0, k // 2, k - 1]
+    Yg = Yd.cpu().numpy()[:, cols]
+    ctx.close()
+    Yo, _ = O.chebyshev_filter(Hh, Y0[:, cols], [deg[j] for j in cols], iv["lambda1"], c, e)
+    rel = np.linalg.norm(Yg - Yo, axis=0) / np.linalg.norm(Yo, axis=0)
+    assert rel.max() <= 1e-11, rel
