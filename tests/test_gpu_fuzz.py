@@ -82,3 +82,72 @@ def test_filter_fuzz_vs_closed_form(gpu_lib, seed):
     Yc = O.filter_wy_closed(w, Y0, deg, l1, c, e)
     rel = np.linalg.norm(Y - Yc, axis=0) / np.linalg.norm(Yc, axis=0)
     assert rel.max() <= 1e-11, (cs | {"deg": (min(deg), max(deg))}, float(rel.max()))
+
+
+def draw_solve(seed):
+    rng = np.random.default_rng(1404416200 + seed)
+    P = int(rng.choice([1, 1, 2, 4]))
+    n = P * int(rng.integers(240 // P, 1600 // P + 1))
+    nev = int(rng.integers(4, max(5, n // 20)))
+    nex = int(rng.integers(max(4, nev // 4), nev // 2 + 6))  # the method's regime (a few % of n, >= nev / 4)
+    cap = int(rng.choice([20, 30, 36, 40]))
+    deg0 = int(rng.integers(2, min(cap, 10) + 1))
+    zmul = int(rng.choice([3, 3, 4]))
+    push = P > 1 and bool(rng.random() < 0.5)
+    return dict(P=P, n=n, nev=nev, nex=nex, cap=cap, deg0=deg0, zmul=zmul, push=push,
+                nd=int(n * rng.uniform(0.6, 0.95)), wseed=int(rng.integers(1, 1 << 30)),
+                nprob=int(rng.integers(1, 4)), delta=float(rng.choice([0.0, 1e-4, 1e-3])))
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_solve_fuzz(gpu_lib, seed):
+    """Seeded random ChFSI sequences (1 .. 3 problems, the later ones perturbed; 1 / 2 / 4 emulated ranks;
+    random nev, nex, degree cap, starting degree, 3M / 4M): problem 1's eigenvalues equal the generator's
+    exact spectrum to 1e-10 and every problem's residuals ||H x - lambda x|| / ||H||_2 stay <= tol, with
+    ||H^(l)||_2 bounded by 40 + the perturbations' norm."""
+    from gen.configs import HNORM
+
+    cs = draw_solve(seed)
+    P, n, nev, nex, nprob = cs["P"], cs["n"], cs["nev"], cs["nex"], cs["nprob"]
+    w = G.wy(n, cs["nd"], cs["wseed"])
+    Hl = [w.full()]
+    for ell in range(1, nprob):
+        H = Hl[-1].copy(order="F")
+        if cs["delta"] > 0:
+            G.perturb(H, cs["wseed"], ell, cs["delta"] * HNORM)
+        Hl.append(H)
+    X0 = G.start_basis(n, nev + nex, cs["wseed"])
+    tol = 1e-10
+    if P == 1:
+        ctx = gpu_lib.Context(0)
+        ctx.set_complex_mult(cs["zmul"])
+        Hd = [gpu_lib.to_colmajor(H) for H in Hl]
+        Xd = gpu_lib.to_colmajor(X0)
+        out = ctx.solve_sequence(lambda ell: Hd[ell], nprob, Xd, nev, nex, tol, deg_cap=cs["cap"], deg0=cs["deg0"],
+                                 seed=cs["wseed"])
+        X = Xd.cpu().numpy()
+        ctx.close()
+    else:
+        Hs = [slabs(gpu_lib, H, P)[0] for H in Hl]
+        nloc = n // P
+        Xs = [gpu_lib.to_colmajor(X0[r * nloc:(r + 1) * nloc]) for r in range(P)]
+
+        def fn(r, ctx):
+            ctx.set_complex_mult(cs["zmul"])
+            return ctx.solve_sequence(lambda ell: Hs[ell][r], nprob, Xs[r], nev, nex, tol, deg_cap=cs["cap"],
+                                      deg0=cs["deg0"], seed=cs["wseed"], n=n, row0=r * nloc)
+
+        outs = run_ranks(gpu_lib, P, fn, None, (n, nloc, nev + nex) if cs["push"] else None)
+        for o in outs[1:]:
+            assert np.array_equal(o["lam"], outs[0]["lam"])  # identical bits on every rank
+        out = outs[0]
+        X = np.concatenate([x.cpu().numpy() for x in Xs], axis=0)
+    assert out["status"] == 0, cs
+    lam = np.asarray(out["lam"])
+    assert np.max(np.abs(lam[0] - w.lam[:nev]) / np.abs(w.lam[:nev])) <= 1e-10, cs
+    # the final block holds the last problem's eigenvectors (first nev columns, ascending)
+    Xn = X[:, :nev]
+    Hn = Hl[-1]
+    hnorm = HNORM + 2.5 * cs["delta"] * HNORM * (nprob - 1)  # ||G|| ~ 2 per perturbation (d2)
+    res = np.linalg.norm(Hn @ Xn - Xn * lam[-1], axis=0) / np.linalg.norm(Xn, axis=0) / hnorm
+    assert res.max() <= tol, (cs, float(res.max()))
