@@ -89,7 +89,7 @@ def draw_solve(seed):
     P = int(rng.choice([1, 1, 2, 4]))
     n = P * int(rng.integers(240 // P, 1600 // P + 1))
     nev = int(rng.integers(4, max(5, n // 20)))
-    nex = int(rng.integers(max(4, nev // 4), nev // 2 + 6))  # the method's regime (a few % of n, >= nev / 4)
+    nex = int(rng.integers(max(4, nev // 4), nev // 2 + 6))  # the configurations use nex = 20-50 % of nev
     cap = int(rng.choice([20, 30, 36, 40]))
     deg0 = int(rng.integers(2, min(cap, 10) + 1))
     zmul = int(rng.choice([3, 3, 4]))
