@@ -449,7 +449,7 @@ def rank_main(args, cf, rank, world, local_rank, group):
     # K1 launches (emulated ranks share one GPU: their kernel intervals overlap, so no per-GPU rate exists)
     gpus = 1 if args.emulate_ranks > 1 else world
     filt_tf = flops / gpus / t_filter / 1e12  # whole filter calls (incl. the Y -> state copy, finite check)
-    k1_tf = flops / gpus / t_k1 / 1e12        # inside the K1 launches only
+    k1_tf = flops / gpus / t_k1 / 1e12 if t_k1 > 0 else float("nan")  # inside the K1 launches only
     e2e = None
     if not args.no_e2e:
         out2, ms2, _, _ = run_pass(True)

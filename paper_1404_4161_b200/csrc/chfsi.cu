@@ -435,10 +435,15 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
   CUtensorMap tmA, tmA3;
   int last_bm = -1, last_bm3 = -1;
   bool h3_built = false;
-  // CUDA events around every K1 launch (read back after the final synchronisation)
+  // CUDA events timing K1 (read back after the final synchronisation): around every launch where it is
+  // needed -- the per-launch trace (CHFSI_K1_LOG), the timeline, and p > 1, where exchanges separate the
+  // launches -- otherwise one pair around the call's back-to-back launches (an event record between two
+  // launches costs ~5 us of GPU time: c1 eigenproblems 1.6 % faster without them,
+  // profiles/r02_ab_k1_events.txt); the K1 time then includes the few-us launch gaps
+  static const bool k1_log = getenv("CHFSI_K1_LOG") != nullptr;  // per-launch trace (diagnostics)
   st = ensure_events(ctx, ctx->k1_events, (size_t)2 * (mk + 1) * G, cudaEventDefault);
   if (st) return st;
-  int nev_used = 0;
+  int nev_used = 0, call_launches = 0;
   std::vector<std::pair<int, int>> launch_log;  // (active columns, variant) per K1 launch
   // timeline (CHFSI_TIMELINE): K1 intervals come from k1_events; exchanges get their own event pairs
   static const char* tl_prefix = getenv("CHFSI_TIMELINE");
@@ -451,6 +456,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
   };
   std::vector<TlRec> tl_log;
   int tl_used = 0;
+  const bool per_launch = k1_log || tl || p > 1;
   if (tl) {
     st = ensure_events(ctx, ctx->tl_events, (size_t)2 * (mk + 2) * G + 1, cudaEventDefault);
     if (st) return st;
@@ -550,12 +556,15 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       if (st) return st;
       // this group's operand for step i is complete once its allgather (comm stream) has landed
       if (p > 1) CHFSI_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->grp_ag[g], 0));
-      CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used], ctx->stream));
+      if (per_launch || call_launches == 0) CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used], ctx->stream));
       CHFSI_CUDA_TRY(ctx, launch_filter_step(t, tmA, op.tm, z3k ? tmA3 : tmA, op.tm3, sp, ctx->stream));
       launch_log.emplace_back((int)ka, t.id);
       if (tl) tl_log.push_back({0, g, i, nev_used});
-      CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used + 1], ctx->stream));
-      nev_used += 2;
+      ++call_launches;
+      if (per_launch) {
+        CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[nev_used + 1], ctx->stream));
+        nev_used += 2;
+      }
       ctx->launches++;
       if (push && ka_next > 0) {  // every rank's pushes of step i land before anyone's step i+1
         st = comm_barrier(ctx, ctx->stream);
@@ -568,6 +577,10 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
         CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->grp_ag[g], ctx->comm_stream));
       }
     }
+  }
+  if (!per_launch && call_launches > 0) {  // close the call's single K1 interval
+    CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->k1_events[1], ctx->stream));
+    nev_used = 2;
   }
   if (p > 1) {  // nothing on the comm stream outlives the call
     CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->join_ev, ctx->comm_stream));
@@ -590,12 +603,11 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
       fclose(f);
     }
   }
-  static const bool k1_log = getenv("CHFSI_K1_LOG") != nullptr;  // per-launch trace (diagnostics)
   for (int q = 0; q < nev_used; q += 2) {
     float ms = 0;
     CHFSI_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->k1_events[q], ctx->k1_events[q + 1]));
     ctx->k1_seconds += ms * 1e-3;
-    ctx->k1_launches++;
+    ctx->k1_launches += per_launch ? 1 : call_launches;
     if (k1_log)
       fprintf(stderr, "k1 rank %d n %lld nloc %lld ka %d variant %d ms %.4f\n", ctx->rank, (long long)n,
               (long long)nloc, launch_log[q / 2].first, launch_log[q / 2].second, ms);
