@@ -586,6 +586,9 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
     CHFSI_CUDA_TRY(ctx, cudaEventRecord(ctx->join_ev, ctx->comm_stream));
     CHFSI_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   }
+  int h_nonfinite = 0;  // read with the call's one synchronisation (no extra host round trip)
+  if (check_finite)
+    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&h_nonfinite, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   if (tl) {  // one JSON line per interval, times in ms from the call's origin event
     ctx->tl_calls++;
@@ -613,9 +616,7 @@ chfsi_status filter_impl(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, c
               (long long)nloc, launch_log[q / 2].first, launch_log[q / 2].second, ms);
   }
   if (check_finite) {
-    int h = 0;
-    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    int h = h_nonfinite;
     if (p > 1) {  // a non-finite value lives in one rank's rows: every rank takes the same branch
       double hv = h ? 1.0 : 0.0;
       double* dv = reinterpret_cast<double*>(flag) + 1;

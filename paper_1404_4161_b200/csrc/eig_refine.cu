@@ -196,7 +196,8 @@ chfsi_status eig_refine(chfsi_ctx ctx, int64_t ka, T* G, double* dmu, bool* done
   CHFSI_CUDA_TRY(ctx, launch_col_gather(ka, ka, reinterpret_cast<const D*>(X), ka, perm, reinterpret_cast<D*>(G), ka,
                                         ctx->stream));
   ctx->launches++;
-  CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // host vectors above are staged by value
+  // no synchronisation: a copy from pageable host memory returns once its source has been staged, so
+  // ord / sorted may go out of scope; the caller synchronises before it reads the results
   *done = true;
   return CHFSI_OK;
 }
