@@ -748,6 +748,8 @@ void chfsi_ctx_destroy(chfsi_ctx ctx) {
   for (cudaEvent_t ev : ctx->grp_ag) cudaEventDestroy(ev);
   for (cudaEvent_t ev : ctx->tl_events) cudaEventDestroy(ev);
   if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+  if (ctx->lz_exec) cudaGraphExecDestroy(ctx->lz_exec);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   for (cudaEvent_t ev : ctx->eig_ev)
     if (ev) cudaEventDestroy(ev);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);

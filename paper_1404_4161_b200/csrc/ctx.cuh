@@ -115,6 +115,12 @@ struct chfsi_ctx_s {
   chfsi::DevBuf solver_ws;       // cuSOLVER workspace
   chfsi::DevBuf devinfo;
   chfsi::DevBuf lz;              // Lanczos basis
+  // p == 1: the Lanczos steps as one captured CUDA graph, replayed for every problem (the panel pointer
+  // travels through a device slot); re-captured when its shape or workspace changes
+  cudaGraphExec_t lz_exec = nullptr;
+  std::vector<int64_t> lz_key;
+  bool lz_graph_off = false;  // capture failed once (or CHFSI_GRAPHS=0): launch the steps directly
+  cudaStream_t cap_stream = nullptr;  // capture happens here (the legacy default stream cannot be captured)
   chfsi::DevBuf ya, xl, tb, idx;  // solver: active block, locked block, filter block, column indices
   chfsi::DevBuf qsave, qrn;      // QR: the projected block (Householder / R23 restart), column norms
   chfsi::DevBuf eigw;            // k x k eigensolve: refinement workspace (eig_refine.cu)

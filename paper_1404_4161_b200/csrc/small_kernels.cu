@@ -7,11 +7,12 @@ namespace chfsi {
 
 namespace {
 
-__global__ void hemv_kernel(int64_t n, int64_t nloc, const double2* __restrict__ Hp, int64_t ldh,
-                            const double2* __restrict__ v, double2* __restrict__ w) {
+__global__ void hemv_kernel(int64_t n, int64_t nloc, const double2* __restrict__ Hp, const void* const* hpp,
+                            int64_t ldh, const double2* __restrict__ v, double2* __restrict__ w) {
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= nloc) return;
+  if (hpp) Hp = static_cast<const double2*>(*hpp);  // H through a device slot (the captured Lanczos graph)
   const double2* h = Hp + r * ldh;
   double sr0 = 0, si0 = 0, sr1 = 0, si1 = 0;
   int64_t q = lane;
@@ -172,6 +173,21 @@ __global__ void scale_kernel(int64_t rows, double2* x, double s) {
   }
 }
 
+template <typename D>
+__global__ void scale_rnorm_kernel(int64_t rows, D* x, const double* nrm2) {
+  const double s = 1.0 / sqrt(*nrm2);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    if constexpr (sizeof(D) == 16) {
+      const double2 a = reinterpret_cast<const double2*>(x)[r];
+      reinterpret_cast<double2*>(x)[r] = make_double2(a.x * s, a.y * s);
+    } else {
+      reinterpret_cast<double*>(x)[r] *= s;
+    }
+  }
+}
+
+__global__ void store_ptr_kernel(const void** slot, const void* ptr) { *slot = ptr; }
+
 // Lanczos step on the device (no host round trip): beta = sqrt(||w||^2), v_next = w / beta (nullable),
 // alpha = Re(coef_j) (nullable); beta and alpha land in the step's slots of the device arrays
 template <typename D>
@@ -223,9 +239,9 @@ inline unsigned grid1(int64_t rows, int threads) {
 }  // namespace
 
 cudaError_t launch_hemv(int64_t n, int64_t nloc, const double2* Hp, int64_t ldh, const double2* v, double2* w,
-                        cudaStream_t st) {
+                        cudaStream_t st, const void* const* hpp) {
   const int warps = 8;
-  hemv_kernel<<<(unsigned)((nloc + warps - 1) / warps), warps * 32, 0, st>>>(n, nloc, Hp, ldh, v, w);
+  hemv_kernel<<<(unsigned)((nloc + warps - 1) / warps), warps * 32, 0, st>>>(n, nloc, Hp, hpp, ldh, v, w);
   return cudaGetLastError();
 }
 
@@ -290,11 +306,12 @@ cudaError_t launch_orth_err(int64_t k, const double2* G, int64_t ldg, double* ou
 // real-symmetric counterparts
 namespace {
 
-__global__ void hemv_real_kernel(int64_t n, int64_t nloc, const double* __restrict__ Hp, int64_t ldh,
-                                 const double* __restrict__ v, double* __restrict__ w) {
+__global__ void hemv_real_kernel(int64_t n, int64_t nloc, const double* __restrict__ Hp, const void* const* hpp,
+                                 int64_t ldh, const double* __restrict__ v, double* __restrict__ w) {
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= nloc) return;
+  if (hpp) Hp = static_cast<const double*>(*hpp);
   const double* h = Hp + r * ldh;
   double s0 = 0, s1 = 0;
   int64_t q = lane;
@@ -389,9 +406,9 @@ __global__ void orth_err_real_kernel(int64_t k, const double* G, int64_t ldg, un
 }  // namespace
 
 cudaError_t launch_hemv(int64_t n, int64_t nloc, const double* Hp, int64_t ldh, const double* v, double* w,
-                        cudaStream_t st) {
+                        cudaStream_t st, const void* const* hpp) {
   const int warps = 8;
-  hemv_real_kernel<<<(unsigned)((nloc + warps - 1) / warps), warps * 32, 0, st>>>(n, nloc, Hp, ldh, v, w);
+  hemv_real_kernel<<<(unsigned)((nloc + warps - 1) / warps), warps * 32, 0, st>>>(n, nloc, Hp, hpp, ldh, v, w);
   return cudaGetLastError();
 }
 cudaError_t launch_colnorm2(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* out, cudaStream_t st) {
@@ -470,6 +487,19 @@ cudaError_t launch_lanczos_next(int64_t rows, const double2* w, double2* vn, con
 cudaError_t launch_lanczos_next(int64_t rows, const double* w, double* vn, const double* nrm2, const double* coef_j,
                                 double* beta_out, double* alpha_out, cudaStream_t st) {
   lanczos_next_kernel<double><<<grid1(rows, 256), 256, 0, st>>>(rows, w, vn, nrm2, coef_j, beta_out, alpha_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_rnorm(int64_t rows, double2* x, const double* nrm2, cudaStream_t st) {
+  scale_rnorm_kernel<double2><<<grid1(rows, 256), 256, 0, st>>>(rows, x, nrm2);
+  return cudaGetLastError();
+}
+cudaError_t launch_scale_rnorm(int64_t rows, double* x, const double* nrm2, cudaStream_t st) {
+  scale_rnorm_kernel<double><<<grid1(rows, 256), 256, 0, st>>>(rows, x, nrm2);
+  return cudaGetLastError();
+}
+cudaError_t launch_store_ptr(const void** slot, const void* ptr, cudaStream_t st) {
+  store_ptr_kernel<<<1, 1, 0, st>>>(slot, ptr);
   return cudaGetLastError();
 }
 

@@ -9,8 +9,10 @@ namespace chfsi {
 
 // w[r] = sum_q conj(Hp[q, r]) v[q] for the nloc local rows r (K2: one warp per row, HBM-bound:
 // 16 n nloc bytes per call)
+// hpp (nullable): read the panel pointer from this device slot instead of Hp (a captured graph replays
+// against whatever panel the slot holds)
 cudaError_t launch_hemv(int64_t n, int64_t nloc, const double2* Hp, int64_t ldh, const double2* v, double2* w,
-                        cudaStream_t st);
+                        cudaStream_t st, const void* const* hpp = nullptr);
 // out[j] = sum_r |X[r, j]|^2 (rows x cols)
 cudaError_t launch_colnorm2(int64_t rows, int64_t cols, const double2* X, int64_t ldx, double* out, cudaStream_t st);
 // out[j] = sum_r |HY[r, j] - mu[j] Y[r, j]|^2 (mu on device)
@@ -52,9 +54,15 @@ cudaError_t launch_lanczos_next(int64_t rows, const double2* w, double2* vn, con
 cudaError_t launch_lanczos_next(int64_t rows, const double* w, double* vn, const double* nrm2, const double* coef_j,
                                 double* beta_out, double* alpha_out, cudaStream_t st);
 
+// x *= 1 / sqrt(*nrm2) (device scalar; the Lanczos start vector without a host round trip)
+cudaError_t launch_scale_rnorm(int64_t rows, double2* x, const double* nrm2, cudaStream_t st);
+cudaError_t launch_scale_rnorm(int64_t rows, double* x, const double* nrm2, cudaStream_t st);
+// *slot = ptr (stream-ordered)
+cudaError_t launch_store_ptr(const void** slot, const void* ptr, cudaStream_t st);
+
 // ---- real-symmetric (NEXT-3) counterparts, same semantics on double data ----
 cudaError_t launch_hemv(int64_t n, int64_t nloc, const double* Hp, int64_t ldh, const double* v, double* w,
-                        cudaStream_t st);
+                        cudaStream_t st, const void* const* hpp = nullptr);
 cudaError_t launch_colnorm2(int64_t rows, int64_t cols, const double* X, int64_t ldx, double* out, cudaStream_t st);
 cudaError_t launch_resid2(int64_t rows, int64_t cols, const double* HY, int64_t ld1, const double* Y, int64_t ld2,
                           const double* mu, double* out, cudaStream_t st);

@@ -80,31 +80,21 @@ chfsi_status lanczos_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
   if (steps > n) steps = (int32_t)n;
   const int p = ctx->nranks;
   const int64_t ldv = nloc;
-  TRY(ensure(ctx, ctx->lz, sizeof(D) * ((size_t)ldv * (steps + 1) + (size_t)n + (size_t)nloc)));
+  TRY(ensure(ctx, ctx->lz, sizeof(D) * ((size_t)ldv * (steps + 1) + (size_t)n + (size_t)nloc) + 64));
   TRY(ensure(ctx, ctx->small3, sizeof(double) * (2 * (size_t)(steps + 8) + 2 * (size_t)steps + 8)));
   D* V = static_cast<D*>(ctx->lz.ptr);
   D* vfull = V + (size_t)ldv * (steps + 1);
   D* w = vfull + n;
+  const void** hslot = reinterpret_cast<const void**>(w + nloc);  // the panel pointer of the graph path
   D* coef = static_cast<D*>(ctx->small3.ptr);
   double* nrm = static_cast<double*>(ctx->small3.ptr) + 2 * (steps + 2);
   double* dalpha = nrm + 8;             // alpha_j, beta_j of every step stay on the device until the end
   double* dbeta = dalpha + steps;
   std::vector<double> al(steps), be(steps);
-  for (int restart = 0; restart <= 3; ++restart) {
-    CHFSI_CUDA_TRY(ctx, launch_random_block(nloc, 1, row0, seed, (4ull << 16) | (uint64_t)restart, 0, V, ldv,
-                                            ctx->stream));
-    ctx->launches++;
-    double h = 0;
-    CHFSI_CUDA_TRY(ctx, launch_colnorm2(nloc, 1, V, ldv, nrm, ctx->stream));
-    ctx->launches++;
-    TRY(comm_allreduce_sum(ctx, nrm, 1));
-    CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(&h, nrm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CHFSI_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    CHFSI_CUDA_TRY(ctx, launch_scale(nloc, V, 1.0 / std::sqrt(h), ctx->stream));
-    ctx->launches++;
-    // the steps run without host round trips: beta_j = ||w||, v_{j+1} = w / beta_j and alpha_j are formed
-    // on the device; the breakdown test (beta_j < 1e-14 ||T||_est) runs on the host afterwards, and a
-    // breakdown discards the (then meaningless) later steps and restarts
+  // the steps run without host round trips: beta_j = ||w||, v_{j+1} = w / beta_j and alpha_j are formed
+  // on the device; the breakdown test (beta_j < 1e-14 ||T||_est) runs on the host afterwards, and a
+  // breakdown discards the (then meaningless) later steps and restarts
+  auto issue_steps = [&](const void* const* hpp) -> chfsi_status {
     for (int j = 0; j < steps; ++j) {
       D* vj = V + (size_t)j * ldv;
       const D* vin = vj;
@@ -114,7 +104,7 @@ chfsi_status lanczos_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
         TRY(comm_allgather_inplace(ctx, reinterpret_cast<double*>(vfull), (size_t)S::elem * nloc));
         vin = vfull;
       }
-      CHFSI_CUDA_TRY(ctx, launch_hemv(n, nloc, static_cast<const D*>(Hp), ldh, vin, w, ctx->stream));
+      CHFSI_CUDA_TRY(ctx, launch_hemv(n, nloc, static_cast<const D*>(Hp), ldh, vin, w, ctx->stream, hpp));
       ctx->launches++;
       for (int pass = 0; pass < 2; ++pass) {
         CUBLAS_TRY(ctx, S::gemv(ctx->cublas, S::opH, (int)nloc, j + 1, &one, reinterpret_cast<const T*>(V), (int)ldv,
@@ -132,6 +122,73 @@ chfsi_status lanczos_t(chfsi_ctx ctx, int64_t n, int64_t row0, int64_t nloc, con
       D* vn = j + 1 < steps ? V + (size_t)(j + 1) * ldv : nullptr;
       CHFSI_CUDA_TRY(ctx, launch_lanczos_next(nloc, w, vn, nrm, nullptr, dbeta + j, nullptr, ctx->stream));
       ctx->launches++;
+    }
+    return CHFSI_OK;
+  };
+  // One rank: the 25 steps (~7 small launches each) are launch-bound at small n, so they run as a CUDA
+  // graph captured once per shape / workspace and replayed for every problem, the panel read through
+  // hslot. Several ranks keep direct launches (their collectives order against the other ranks).
+  static const bool graphs_env = !(getenv("CHFSI_GRAPHS") && getenv("CHFSI_GRAPHS")[0] == '0');
+  bool use_graph = p == 1 && graphs_env && !ctx->lz_graph_off;
+  if (use_graph) {
+    const std::vector<int64_t> key = {n, nloc, ldh, steps, (int64_t)S::elem, (int64_t)(intptr_t)V,
+                                      (int64_t)(intptr_t)coef, (int64_t)(intptr_t)ctx->cublas};
+    if (!ctx->lz_exec || ctx->lz_key != key) {
+      if (ctx->lz_exec) {
+        cudaGraphExecDestroy(ctx->lz_exec);
+        ctx->lz_exec = nullptr;
+      }
+      cudaGraph_t graph = nullptr;
+      const int64_t launches0 = ctx->launches;
+      // capture on a library-owned stream (the context's may be the legacy default stream, which cannot
+      // be captured): the steps are recorded, not run, so no ordering with the context stream is needed
+      bool ok = ctx->cap_stream || cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) == cudaSuccess;
+      cudaStream_t home = ctx->stream;
+      if (ok) {
+        ctx->stream = ctx->cap_stream;
+        ok = cublasSetStream(ctx->cublas, ctx->cap_stream) == CUBLAS_STATUS_SUCCESS &&
+             cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+          const chfsi_status st = issue_steps(reinterpret_cast<const void* const*>(hslot));
+          ok = cudaStreamEndCapture(ctx->cap_stream, &graph) == cudaSuccess && st == CHFSI_OK;
+        }
+        ctx->stream = home;
+        cublasSetStream(ctx->cublas, home);
+      }
+      if (ok) ok = cudaGraphInstantiate(&ctx->lz_exec, graph, 0) == cudaSuccess;
+      if (graph) cudaGraphDestroy(graph);
+      if (!ok) {  // e.g. a library call that cannot be captured: launch directly from now on
+        const cudaError_t ce = cudaGetLastError();
+        if (getenv("CHFSI_GRAPHS_DEBUG"))
+          fprintf(stderr, "chfsi: Lanczos graph capture failed (%s; %s); direct launches\n", cudaGetErrorString(ce),
+                  ctx->err.c_str());
+        if (ctx->lz_exec) cudaGraphExecDestroy(ctx->lz_exec);
+        ctx->lz_exec = nullptr;
+        ctx->lz_graph_off = true;
+        use_graph = false;
+        ctx->err.clear();
+      } else {
+        ctx->lz_key = key;
+        if (getenv("CHFSI_GRAPHS_DEBUG")) fprintf(stderr, "chfsi: Lanczos steps captured (n %lld, %d steps)\n", (long long)n, steps);
+      }
+      ctx->launches = launches0;  // captured, not launched
+    }
+  }
+  for (int restart = 0; restart <= 3; ++restart) {
+    CHFSI_CUDA_TRY(ctx, launch_random_block(nloc, 1, row0, seed, (4ull << 16) | (uint64_t)restart, 0, V, ldv,
+                                            ctx->stream));
+    ctx->launches++;
+    CHFSI_CUDA_TRY(ctx, launch_colnorm2(nloc, 1, V, ldv, nrm, ctx->stream));
+    ctx->launches++;
+    TRY(comm_allreduce_sum(ctx, nrm, 1));
+    CHFSI_CUDA_TRY(ctx, launch_scale_rnorm(nloc, V, nrm, ctx->stream));  // v_0 / ||v_0||, on the device
+    ctx->launches++;
+    if (use_graph) {
+      CHFSI_CUDA_TRY(ctx, launch_store_ptr(hslot, Hp, ctx->stream));
+      CHFSI_CUDA_TRY(ctx, cudaGraphLaunch(ctx->lz_exec, ctx->stream));
+      ctx->launches += 1 + 3 * (int64_t)steps;  // store + the graph's own kernels (hemv, colnorm, next per step)
+    } else {
+      TRY(issue_steps(nullptr));
     }
     CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(al.data(), dalpha, sizeof(double) * steps, cudaMemcpyDeviceToHost, ctx->stream));
     CHFSI_CUDA_TRY(ctx, cudaMemcpyAsync(be.data(), dbeta, sizeof(double) * steps, cudaMemcpyDeviceToHost, ctx->stream));
