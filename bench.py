@@ -226,6 +226,9 @@ def main():
     if args.emulate_ranks > 1:
         run_emulated(args, cf)
         return
+    if args.gpus != world and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE = {world}: launch N > 1 under torch.distributed.run; "
+              f"measuring {world} GPU(s)", file=sys.stderr)
     import torch
 
     import paper_1404_4161_b200 as chfsi
