@@ -273,3 +273,34 @@ def test_filter_every_last_unit_residue(gpu_lib, ctx, vid):
             assert colrel(Yd.cpu().numpy(), Yc).max() <= 1e-13, k
     finally:
         os.environ.pop(env, None)
+
+
+@pytest.mark.parametrize("n,k", [(300, 37), (517, 100)])
+def test_filter_guard_bands_every_variant(gpu_lib, ctx, variant, n, k):
+    """Out-of-bounds write check without a sanitizer (compute-sanitizer is unavailable on the GPU pool):
+    Y is a view of a larger allocation with guard rows below every column and guard columns after the
+    block, H a view with guard rows and columns; after a filter call with ragged tiles in M, N and K,
+    every guard value is bit-identical and H is unchanged, for every tile variant."""
+    import torch
+
+    w = G.wy(n, int(0.9 * n), n + k)
+    H = w.full()
+    rng = np.random.default_rng(n + k)
+    Y0 = crand(rng, n, k)
+    deg = sorted(rng.integers(1, 16, k).tolist())
+    l1, a, b = w.lam[0] - 0.05, w.lam[k], 45.0
+    c, e = (a + b) / 2, (b - a) / 2
+    sentinel = complex(1234.5, -6789.25)
+    Hbig = gpu_lib.colmajor(n + 9, n + 5)
+    Hbig.fill_(sentinel)
+    Hbig[:n, :n].copy_(torch.as_tensor(H))
+    Hguard = Hbig.clone()
+    Ybig = gpu_lib.colmajor(n + 13, k + 3)
+    Ybig.fill_(sentinel)
+    Ybig[:n, :k].copy_(torch.as_tensor(Y0))
+    ctx.filter(Hbig[:n, :n], Ybig[:n, :k], deg, l1, c, e)
+    assert bool((Ybig[n:, :] == sentinel).all())      # guard rows of every column
+    assert bool((Ybig[:, k:] == sentinel).all())      # guard columns after the block
+    assert torch.equal(Hbig, Hguard)                  # H (and its guards) read-only
+    Yo, _ = O.chebyshev_filter(H, Y0, deg, l1, c, e)
+    assert colrel(Ybig[:n, :k].cpu().numpy(), Yo).max() <= 1e-11
