@@ -105,8 +105,11 @@ chfsi_status chfsi_ctx_set_eigensolver(chfsi_ctx ctx, int32_t mode);
  *          the local group's event barrier) separates consecutive steps.
  * Mode 1 supports up to 8 ranks (one 8-GPU NVSwitch box) and requires the workspace to be reserved first (chfsi_ctx_reserve with the largest n, nloc and
  * block width to be used); the ranks' buffers are then pinned: a later chfsi_ctx_reserve or filter
- * call needing a larger block returns CHFSI_ERR_ARG. Errors: CHFSI_ERR_ARG (null ctx, bad mode, no
- * reservation), CHFSI_ERR_CUDA (IPC mapping failed), CHFSI_ERR_NCCL. No-op at nranks == 1. */
+ * call needing a larger block returns CHFSI_ERR_ARG. The ranks agree on the outcome: if any rank
+ * fails to export or map the IPC handles, every rank returns CHFSI_ERR_CUDA with the exchange left at
+ * mode 0 (so a caller can fall back collectively). Errors: CHFSI_ERR_ARG (null ctx, bad mode, no
+ * reservation), CHFSI_ERR_CUDA (IPC mapping failed on some rank), CHFSI_ERR_NCCL. No-op at
+ * nranks == 1. */
 chfsi_status chfsi_ctx_set_exchange(chfsi_ctx ctx, int32_t mode);
 
 /* nranks > 1 only: overlap of the per-step exchange with the filter's MMAs (BASELINE.json north_star
